@@ -1,0 +1,205 @@
+/*
+ * mltune_b200.h — C ABI of libmltune_b200.so, the sm_100a implementation of
+ * the mltune auto-tuner hot path (Falch & Elster, arXiv 1506.00842).
+ *
+ * The reference package `mltune` is pure Python; its "plugin seams" for this
+ * path are Python functions and duck types. Each entry point below replaces
+ * one of them (reference paths relative to /root/reference/pkg/src/mltune):
+ *
+ *   mlt_decode            ParamSpace.decode_indices        paramspace.py:184-193
+ *   mlt_valid_mask        ParamSpace.static_valid_mask     paramspace.py:201-213 (+ ValidityRule.satisfied_mask :92-107)
+ *   mlt_encode            Encoder.encode_indices           model.py:88-97
+ *   mlt_predict_indices   Ensemble.predict_indices         model.py:300-301 (forward_batch :146-154, predict_log_batch :162-164)
+ *   mlt_predict_features  Ensemble.predict_features        model.py:290-294
+ *   mlt_top_m             tuner.top_m_predicted            tuner.py:95-131 (one contiguous slice or an index list)
+ *   mlt_merge_top_m       the final lexsort of tuner.py:128-131, applied to per-GPU lists
+ *   mlt_train_member(s)   model._fit / train_ensemble      model.py:194-249, :308-341
+ *
+ * Conventions
+ *   - Plain C types only; every pointer argument is HOST memory owned by the
+ *     caller unless the name says `dev_`.
+ *   - Return value: MLT_OK (0) or a negative status; mlt_last_error() gives a
+ *     thread-local message. Status -> Python exception mapping:
+ *       MLT_EINVAL -> ValueError, MLT_EMISMATCH -> ConfigMismatchError,
+ *       MLT_EDATA -> InsufficientDataError, MLT_EDIVERGED -> DivergenceError,
+ *       MLT_ECUDA / MLT_EINTERNAL -> RuntimeError.
+ *   - Every call is synchronous on the context's stream (library-owned, or the
+ *     caller's via mlt_ctx_set_stream). One context per device; a context is
+ *     not re-entrant (the reference runner contract is sequential too).
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with MLT_ECUDA.
+ */
+#ifndef MLTUNE_B200_H
+#define MLTUNE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define MLT_API __attribute__((visibility("default")))
+#else
+#define MLT_API
+#endif
+
+#define MLT_ABI_VERSION 1
+
+#define MLT_OK 0
+#define MLT_EINVAL -1
+#define MLT_EMISMATCH -2
+#define MLT_EDATA -3
+#define MLT_EDIVERGED -4
+#define MLT_ECUDA -5
+#define MLT_EINTERNAL -6
+
+#define MLT_MAX_PARAMS 32
+
+/* Validity-rule kinds (paramspace.py:28-31). */
+#define MLT_RULE_MAX_PRODUCT 0
+#define MLT_RULE_MAX_WEIGHTED_SUM 1
+#define MLT_RULE_FORBIDDEN 2
+
+/* A finite parameter space: mixed radix, last parameter fastest
+ * (paramspace.py:110-193), plus static validity rules evaluated on VALUES
+ * with numpy int64 (wrap-around) semantics (paramspace.py:92-107). */
+typedef struct mlt_space {
+  int32_t n_params;            /* P, 1..MLT_MAX_PARAMS */
+  const int32_t* radix;        /* [P] value count per parameter */
+  const int64_t* values;       /* [sum(radix)] value lists, parameter-major */
+  int32_t n_rules;             /* R >= 0 */
+  const int32_t* rule_kind;    /* [R] MLT_RULE_* */
+  const int32_t* rule_nops;    /* [R] operand count per rule */
+  const int32_t* rule_pos;     /* [sum(nops)] operand parameter positions */
+  const int64_t* rule_coeff;   /* [sum(nops)] coefficients (banned values for FORBIDDEN) */
+  const int64_t* rule_bound;   /* [R] bound (unused for FORBIDDEN) */
+} mlt_space;
+
+/* A bagged ensemble of k one-hidden-layer sigmoid networks (model.py:114-170,
+ * :272-301) plus its encoder (value counts; feature = rank / max(count-1, 1)). */
+typedef struct mlt_ensemble {
+  int32_t k;                   /* members */
+  int32_t d;                   /* inputs (= encoder parameters) */
+  int32_t h;                   /* hidden units per member (30 in mltune) */
+  const int32_t* counts;       /* [d] encoder value counts */
+  const double* w1;            /* [k][h][d] weights_hidden */
+  const double* b1;            /* [k][h]    biases_hidden */
+  const double* w2;            /* [k][h]    weights_out */
+  const double* b2;            /* [k]       bias_out */
+  const double* mean;          /* [k]       target_mean */
+  const double* std;           /* [k]       target_std */
+} mlt_ensemble;
+
+/* Diagnostics of one mlt_top_m call. */
+typedef struct mlt_sweep_stats {
+  int64_t configs;             /* configurations swept */
+  int64_t candidates;          /* guard-band candidates rescored in fp64 */
+  int32_t path;                /* 0 = fp32 sweep + fp64 guard band, 1 = fp64 materialise + sort */
+  int32_t group;               /* hidden units per reciprocal in the fp32 sweep (1..3) */
+  double delta;                /* a-priori bound on |fp32 - fp64| mean log time */
+  float sweep_ms;              /* device time of the sweep kernel (profiling on) */
+  float total_ms;              /* device time of the whole call   (profiling on) */
+  int32_t launches;            /* kernels launched by this call */
+  int32_t split;               /* parameters in the inner (per-thread) factor */
+} mlt_sweep_stats;
+
+typedef struct mlt_ctx mlt_ctx;
+
+MLT_API int mlt_abi_version(void);
+MLT_API const char* mlt_last_error(void);
+
+MLT_API int mlt_ctx_create(int device, mlt_ctx** out);
+MLT_API int mlt_ctx_destroy(mlt_ctx* ctx);
+/* Use `stream` (a cudaStream_t) for all work; NULL restores the library stream. */
+MLT_API int mlt_ctx_set_stream(mlt_ctx* ctx, void* stream);
+/* When on, mlt_top_m records CUDA events around its kernels (mlt_sweep_stats). */
+MLT_API int mlt_ctx_set_profiling(mlt_ctx* ctx, int on);
+/* Kernels launched by this context so far. */
+MLT_API int64_t mlt_ctx_launches(mlt_ctx* ctx);
+/* Tuning / test knobs (value -1 restores the default):
+ *   MLT_OPT_PATH      0 = force the fp32 sweep + fp64 guard band, 1 = force fp64 materialise + sort
+ *   MLT_OPT_GROUP     hidden units per reciprocal in the fp32 sweep (1, 2 or 3)
+ *   MLT_OPT_CAND_CAP  capacity of the guard-band candidate buffer (entries)         */
+#define MLT_OPT_PATH 1
+#define MLT_OPT_GROUP 2
+#define MLT_OPT_CAND_CAP 3
+MLT_API int mlt_ctx_set_option(mlt_ctx* ctx, int key, int64_t value);
+
+/* A1: values[n][P] = decode(idx[n]).                 paramspace.py:184-193 */
+MLT_API int mlt_decode(mlt_ctx* ctx, const mlt_space* space, const int64_t* idx, int64_t n,
+               int64_t* values_out);
+/* A2: mask[n] = every rule satisfied.               paramspace.py:201-213 */
+MLT_API int mlt_valid_mask(mlt_ctx* ctx, const mlt_space* space, const int64_t* idx, int64_t n,
+                   uint8_t* mask_out);
+/* A3: feat[n][d] = digit / max(count-1, 1).         model.py:88-97 */
+MLT_API int mlt_encode(mlt_ctx* ctx, const int32_t* counts, int32_t d, const int64_t* idx, int64_t n,
+               double* feat_out);
+/* A4-A6: fp64 predicted seconds for configuration indices. model.py:300-301 */
+MLT_API int mlt_predict_indices(mlt_ctx* ctx, const mlt_ensemble* ens, const int64_t* idx, int64_t n,
+                        double* pred_out);
+/* A6: fp64 predicted seconds for a feature matrix X[n][d]. model.py:290-294 */
+MLT_API int mlt_predict_features(mlt_ctx* ctx, const mlt_ensemble* ens, const double* x, int64_t n,
+                         double* pred_out);
+
+/* A4: raw member outputs out[k][n] = w2 . sigmoid(W1 x + b1) + b2 for a
+ * feature matrix X[n][d] (Network.forward_batch, model.py:146-154). */
+MLT_API int mlt_member_outputs(mlt_ctx* ctx, const mlt_ensemble* ens, const double* x, int64_t n,
+                       double* out);
+
+/* A7: the m statically-valid configurations with the lowest predicted time
+ * (ascending; ties by ascending index) among
+ *   - the contiguous slice [begin, end) of the space, when idx_list == NULL, or
+ *   - the n_list indices of idx_list (sweep_cap subset, tuner.py:104-105).
+ * Writes *out_n <= m results. tuner.py:95-131. */
+MLT_API int mlt_top_m(mlt_ctx* ctx, const mlt_space* space, const mlt_ensemble* ens, int64_t m,
+              int64_t begin, int64_t end, const int64_t* idx_list, int64_t n_list,
+              int64_t* out_idx, double* out_pred, int64_t* out_n, mlt_sweep_stats* stats);
+
+/* Resident variant for repeated sweeps of one (space, ensemble): uploads the
+ * descriptors once; mlt_plan_top_m then does the whole step on the device. */
+typedef struct mlt_plan mlt_plan;
+MLT_API int mlt_plan_create(mlt_ctx* ctx, const mlt_space* space, const mlt_ensemble* ens, mlt_plan** out);
+MLT_API int mlt_plan_top_m(mlt_plan* plan, int64_t m, int64_t begin, int64_t end,
+                   int64_t* out_idx, double* out_pred, int64_t* out_n, mlt_sweep_stats* stats);
+MLT_API int mlt_plan_destroy(mlt_plan* plan);
+
+/* Merge per-shard top-m lists (e.g. after an all-gather across GPUs) into the
+ * global top-m by (prediction, index). Entries with idx < 0 are padding.
+ * dev_idx / dev_pred are DEVICE pointers on the context's device. */
+MLT_API int mlt_merge_top_m(mlt_ctx* ctx, const int64_t* dev_idx, const double* dev_pred, int64_t n,
+                    int64_t m, int64_t* out_idx, double* out_pred, int64_t* out_n);
+
+/* A9-A10: train k members with mini-batch momentum SGD in fp64 (model.py:194-249).
+ * All random draws are made by the caller with the reference RNG stream:
+ *   x[n_rows][d]            training features (all valid rows)
+ *   t[sum(n_m)]             standardized targets, member-major, member m uses rows rows[off_m + r]
+ *   rows[sum(n_m)]          row index into x for member m's r-th example
+ *   n_m[k]                  examples per member
+ *   init_w1[k][h][d], init_w2[k][h]   initial weights (b1 = 0, b2 = 0)
+ *   perms[sum(epochs*n_m)]  per-epoch permutations, member-major then epoch-major
+ * Outputs (per member): w1[k][h][d], b1[k][h], w2[k][h], b2[k], loss_first[k],
+ * loss_final[k], diverged_epoch[k] (0 = finite throughout). */
+typedef struct mlt_train_desc {
+  int32_t k, d, h;
+  int32_t epochs, batch_size;
+  double learning_rate, momentum;
+  int64_t n_rows;
+  const double* x;
+  const double* t;
+  const int32_t* rows;
+  const int32_t* n_m;
+  const double* init_w1;
+  const double* init_w2;
+  const int32_t* perms;
+} mlt_train_desc;
+
+MLT_API int mlt_train_members(mlt_ctx* ctx, const mlt_train_desc* desc, double* w1, double* b1,
+                      double* w2, double* b2, double* loss_first, double* loss_final,
+                      int32_t* diverged_epoch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MLTUNE_B200_H */

@@ -1,0 +1,226 @@
+"""ctypes binding of libmltune_b200.so (the C ABI in include/mltune_b200.h).
+
+Packs duck-typed space / ensemble objects — this package's own or the
+reference `mltune`'s — into the plain C descriptors, owns one library context
+per CUDA device, and maps native status codes to the tuner's exceptions.
+Nothing here computes: every numeric entry point runs on the B200. If the
+library or the device is missing, calls raise NativeUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from . import errors
+
+_LIB_PATH = Path(__file__).resolve().parent / "libmltune_b200.so"
+
+MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
+MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP = 1, 2, 3
+RULE_KIND = {"max-product": 0, "max-weighted-sum": 1, "forbidden-combination": 2}
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class MltSpace(C.Structure):
+    _fields_ = [("n_params", C.c_int32), ("radix", _i32p), ("values", _i64p), ("n_rules", C.c_int32),
+                ("rule_kind", _i32p), ("rule_nops", _i32p), ("rule_pos", _i32p), ("rule_coeff", _i64p),
+                ("rule_bound", _i64p)]
+
+
+class MltEnsemble(C.Structure):
+    _fields_ = [("k", C.c_int32), ("d", C.c_int32), ("h", C.c_int32), ("counts", _i32p), ("w1", _f64p),
+                ("b1", _f64p), ("w2", _f64p), ("b2", _f64p), ("mean", _f64p), ("std", _f64p)]
+
+
+class MltSweepStats(C.Structure):
+    _fields_ = [("configs", C.c_int64), ("candidates", C.c_int64), ("path", C.c_int32), ("group", C.c_int32),
+                ("delta", C.c_double), ("sweep_ms", C.c_float), ("total_ms", C.c_float),
+                ("launches", C.c_int32), ("split", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class MltTrainDesc(C.Structure):
+    _fields_ = [("k", C.c_int32), ("d", C.c_int32), ("h", C.c_int32), ("epochs", C.c_int32),
+                ("batch_size", C.c_int32), ("learning_rate", C.c_double), ("momentum", C.c_double),
+                ("n_rows", C.c_int64), ("x", _f64p), ("t", _f64p), ("rows", _i32p), ("n_m", _i32p),
+                ("init_w1", _f64p), ("init_w2", _f64p), ("perms", _i32p)]
+
+
+# (name, restype, argtypes) of every exported entry point of the header.
+_SIGNATURES = [
+    ("mlt_abi_version", C.c_int, []),
+    ("mlt_last_error", C.c_char_p, []),
+    ("mlt_ctx_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("mlt_ctx_destroy", C.c_int, [C.c_void_p]),
+    ("mlt_ctx_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mlt_ctx_set_profiling", C.c_int, [C.c_void_p, C.c_int]),
+    ("mlt_ctx_launches", C.c_int64, [C.c_void_p]),
+    ("mlt_ctx_set_option", C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
+    ("mlt_decode", C.c_int, [C.c_void_p, C.POINTER(MltSpace), _i64p, C.c_int64, _i64p]),
+    ("mlt_valid_mask", C.c_int, [C.c_void_p, C.POINTER(MltSpace), _i64p, C.c_int64, _u8p]),
+    ("mlt_encode", C.c_int, [C.c_void_p, _i32p, C.c_int32, _i64p, C.c_int64, _f64p]),
+    ("mlt_predict_indices", C.c_int, [C.c_void_p, C.POINTER(MltEnsemble), _i64p, C.c_int64, _f64p]),
+    ("mlt_predict_features", C.c_int, [C.c_void_p, C.POINTER(MltEnsemble), _f64p, C.c_int64, _f64p]),
+    ("mlt_member_outputs", C.c_int, [C.c_void_p, C.POINTER(MltEnsemble), _f64p, C.c_int64, _f64p]),
+    ("mlt_top_m", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltEnsemble), C.c_int64, C.c_int64,
+                            C.c_int64, _i64p, C.c_int64, _i64p, _f64p, _i64p, C.POINTER(MltSweepStats)]),
+    ("mlt_plan_create", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltEnsemble), C.POINTER(C.c_void_p)]),
+    ("mlt_plan_top_m", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, _i64p, _f64p, _i64p,
+                                 C.POINTER(MltSweepStats)]),
+    ("mlt_plan_destroy", C.c_int, [C.c_void_p]),
+    ("mlt_merge_top_m", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _i64p, _f64p, _i64p]),
+    ("mlt_train_members", C.c_int, [C.c_void_p, C.POINTER(MltTrainDesc), _f64p, _f64p, _f64p, _f64p, _f64p,
+                                     _f64p, _i32p]),
+]
+EXPORTS = tuple(name for name, _, _ in _SIGNATURES)
+
+_lib = None
+_lib_lock = threading.Lock()
+_ctxs: dict[int, C.c_void_p] = {}
+
+
+def lib():
+    """Load the in-tree library (fails loudly; there is no fallback)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not _LIB_PATH.exists():
+                raise errors.NativeUnavailableError(
+                    f"{_LIB_PATH} is not built; run __graft_entry__.build() (nvcc, sm_100a)")
+            h = C.CDLL(str(_LIB_PATH))
+            for name, res, args in _SIGNATURES:
+                fn = getattr(h, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = h
+    return _lib
+
+
+def last_error() -> str:
+    return (lib().mlt_last_error() or b"").decode(errors="replace")
+
+
+def check(rc: int, what: str = "", epoch: int | None = None):
+    if rc == MLT_OK:
+        return
+    msg = last_error() or what
+    if rc == MLT_EINVAL:
+        raise ValueError(msg)
+    if rc == MLT_EMISMATCH:
+        raise errors.active["ConfigMismatchError"](msg)
+    if rc == MLT_EDATA:
+        raise errors.active["InsufficientDataError"](msg)
+    if rc == MLT_EDIVERGED:
+        raise errors.active["DivergenceError"](msg, epoch=epoch if epoch is not None else -1)
+    if rc == MLT_ECUDA:
+        raise errors.NativeUnavailableError(msg)
+    raise RuntimeError(f"libmltune_b200 internal error: {msg}")
+
+
+def default_device() -> int:
+    env = os.environ.get("MLTUNE_B200_DEVICE")
+    if env is not None:
+        return int(env)
+    try:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return torch.cuda.current_device()
+    except Exception:  # torch is optional plumbing
+        pass
+    return 0
+
+
+def ctx(device: int | None = None) -> C.c_void_p:
+    """The library context of `device` (created on first use)."""
+    dev = default_device() if device is None else int(device)
+    if dev not in _ctxs:
+        h = C.c_void_p()
+        check(lib().mlt_ctx_create(dev, C.byref(h)), "mlt_ctx_create")
+        _ctxs[dev] = h
+    return _ctxs[dev]
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+# ---- descriptor packing ------------------------------------------------------
+
+class PackedSpace:
+    """mlt_space over host arrays kept alive by this object."""
+
+    def __init__(self, space):
+        params = list(space.params)
+        names = [p.name for p in params]
+        pos = {n: i for i, n in enumerate(names)}
+        self.radix = np.ascontiguousarray([len(p.values) for p in params], dtype=np.int32)
+        self.values = np.ascontiguousarray([int(v) for p in params for v in p.values], dtype=np.int64)
+        kinds, nops, rpos, coeff, bound = [], [], [], [], []
+        for r in getattr(space, "rules", ()):
+            kinds.append(RULE_KIND[r.kind])
+            ops = list(r.operands)
+            co = [int(c) for c in r.coefficients]
+            if not co and r.kind != "forbidden-combination":
+                co = [1] * len(ops)
+            nops.append(len(ops))
+            rpos.extend(pos[o] for o in ops)
+            coeff.extend(co)
+            bound.append(int(r.bound))
+        self.kind = np.ascontiguousarray(kinds or [0], dtype=np.int32)
+        self.nops = np.ascontiguousarray(nops or [0], dtype=np.int32)
+        self.rpos = np.ascontiguousarray(rpos or [0], dtype=np.int32)
+        self.coeff = np.ascontiguousarray(coeff or [0], dtype=np.int64)
+        self.bound = np.ascontiguousarray(bound or [0], dtype=np.int64)
+        self.c = MltSpace(len(params), ptr(self.radix, C.c_int32), ptr(self.values, C.c_int64), len(kinds),
+                          ptr(self.kind, C.c_int32), ptr(self.nops, C.c_int32), ptr(self.rpos, C.c_int32),
+                          ptr(self.coeff, C.c_int64), ptr(self.bound, C.c_int64))
+        self.card = int(np.prod(self.radix.astype(object)))
+
+
+class PackedEnsemble:
+    """mlt_ensemble over host arrays: [k][h][d] W1, [k][h] b1/w2, [k] b2/mean/std."""
+
+    def __init__(self, ensemble):
+        members = list(ensemble.members)
+        enc = ensemble.encoder
+        self.counts = np.ascontiguousarray([len(vals) for _, vals in enc.params], dtype=np.int32)
+        h, d = np.asarray(members[0].weights_hidden).shape
+        self.w1 = np.ascontiguousarray(np.stack([np.asarray(m.weights_hidden, dtype=np.float64) for m in members]))
+        self.b1 = np.ascontiguousarray(np.stack([np.asarray(m.biases_hidden, dtype=np.float64) for m in members]))
+        self.w2 = np.ascontiguousarray(np.stack([np.asarray(m.weights_out, dtype=np.float64) for m in members]))
+        self.b2 = np.ascontiguousarray([float(m.bias_out) for m in members], dtype=np.float64)
+        self.mean = np.ascontiguousarray([float(m.target_mean) for m in members], dtype=np.float64)
+        self.std = np.ascontiguousarray([float(m.target_std) for m in members], dtype=np.float64)
+        if self.w1.shape != (len(members), h, d) or self.counts.shape[0] != d:
+            raise ValueError("member input dimensions do not match the encoder")
+        self.c = MltEnsemble(len(members), d, h, ptr(self.counts, C.c_int32), ptr(self.w1, C.c_double),
+                             ptr(self.b1, C.c_double), ptr(self.w2, C.c_double), ptr(self.b2, C.c_double),
+                             ptr(self.mean, C.c_double), ptr(self.std, C.c_double))
+
+
+_pack_cache: dict[int, tuple] = {}
+
+
+def packed(obj, kind):
+    """Cache packed descriptors by object identity (spaces and ensembles are
+    immutable in the reference API); the cache pins the object so ids stay unique."""
+    key = id(obj)
+    hit = _pack_cache.get(key)
+    if hit is not None and hit[0] is obj:
+        return hit[1]
+    pk = PackedSpace(obj) if kind == "space" else PackedEnsemble(obj)
+    if len(_pack_cache) > 64:
+        _pack_cache.clear()
+    _pack_cache[key] = (obj, pk)
+    return pk

@@ -1,0 +1,1027 @@
+// abi.cu — host side of libmltune_b200.so: the extern "C" entry points of
+// include/mltune_b200.h, device-memory management, the fp32-sweep setup
+// (split choice, centring, range checks, a-priori error bound) and the
+// selection (CUB radix sort by (prediction, index)).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace mlt;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(MLT_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define TRY(expr)            \
+  do {                       \
+    int rc_ = (expr);        \
+    if (rc_ != MLT_OK) return rc_; \
+  } while (0)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct mlt_ctx {
+  int dev = 0;
+  int sms = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  bool prof = false;
+  int64_t launches = 0;
+  int opt_path = -1, opt_group = -1;
+  int64_t cand_cap = 1 << 20;
+  std::vector<void*> slots = std::vector<void*>(32, nullptr);
+  std::vector<size_t> sizes = std::vector<size_t>(32, 0);
+  void* pinned = nullptr;       // small pinned staging for scalars
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+enum Slot {
+  S_SPACE_VALUES, S_SPACE_RPOS, S_SPACE_RCOEFF, S_ENS, S_IDX, S_OUT_A, S_OUT_B, S_OUT_C, S_OUT_D,
+  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT
+};
+
+int ws(mlt_ctx* c, int slot, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (c->sizes[slot] < bytes) {
+    if (c->slots[slot]) CU(cudaFree(c->slots[slot]));
+    c->slots[slot] = nullptr;
+    c->sizes[slot] = 0;
+    size_t want = bytes + bytes / 4;
+    CU(cudaMalloc(&c->slots[slot], want));
+    c->sizes[slot] = want;
+  }
+  *out = c->slots[slot];
+  return MLT_OK;
+}
+
+template <typename T>
+int ws_t(mlt_ctx* c, int slot, size_t count, T** out) {
+  void* p;
+  TRY(ws(c, slot, count * sizeof(T), &p));
+  *out = static_cast<T*>(p);
+  return MLT_OK;
+}
+
+int check_launch(mlt_ctx* c) {
+  c->launches++;
+  CU(cudaGetLastError());
+  return MLT_OK;
+}
+
+int grid_for(mlt_ctx* c, int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)c->sms * 16));
+}
+
+// ---- host copies of the descriptors ---------------------------------------
+struct HostSpace {
+  int P = 0;
+  std::vector<int> radix;
+  std::vector<int64_t> values;
+  std::vector<int> rkind, roff, rpos;
+  std::vector<int64_t> rcoeff, rbound;
+  double card = 0;              // as double for range checks
+  int64_t card_i = 0;           // exact when it fits
+  bool card_fits = true;
+};
+
+int read_space(const mlt_space* s, HostSpace* h) {
+  if (!s) return fail(MLT_EINVAL, "space is NULL");
+  if (s->n_params < 1 || s->n_params > kMaxP)
+    return fail(MLT_EINVAL, "space must have 1..%d parameters, got %d", kMaxP, s->n_params);
+  if (s->n_rules < 0 || s->n_rules > kMaxRules)
+    return fail(MLT_EINVAL, "space must have 0..%d rules, got %d", kMaxRules, s->n_rules);
+  h->P = s->n_params;
+  h->radix.assign(s->radix, s->radix + h->P);
+  int64_t nv = 0;
+  h->card = 1;
+  h->card_i = 1;
+  h->card_fits = true;
+  for (int p = 0; p < h->P; ++p) {
+    if (h->radix[p] < 1) return fail(MLT_EINVAL, "parameter %d has an empty value list", p);
+    nv += h->radix[p];
+    h->card *= h->radix[p];
+    if (h->card_fits && h->card_i > INT64_MAX / h->radix[p]) h->card_fits = false;
+    if (h->card_fits) h->card_i *= h->radix[p];
+  }
+  if (!h->card_fits) return fail(MLT_EINVAL, "space cardinality exceeds 2^63");
+  h->values.assign(s->values, s->values + nv);
+  h->rkind.assign(s->rule_kind, s->rule_kind + s->n_rules);
+  h->roff.assign(1, 0);
+  int nops = 0;
+  for (int r = 0; r < s->n_rules; ++r) {
+    if (h->rkind[r] < 0 || h->rkind[r] > 2) return fail(MLT_EINVAL, "unknown rule kind %d", h->rkind[r]);
+    nops += s->rule_nops[r];
+    h->roff.push_back(nops);
+  }
+  if (nops > kMaxOps) return fail(MLT_EINVAL, "too many rule operands (%d > %d)", nops, kMaxOps);
+  h->rpos.assign(s->rule_pos, s->rule_pos + nops);
+  for (int o = 0; o < nops; ++o)
+    if (h->rpos[o] < 0 || h->rpos[o] >= h->P) return fail(MLT_EINVAL, "rule operand position %d out of range", h->rpos[o]);
+  h->rcoeff.assign(s->rule_coeff, s->rule_coeff + nops);
+  h->rbound.assign(s->rule_bound, s->rule_bound + s->n_rules);
+  return MLT_OK;
+}
+
+int upload_space(mlt_ctx* c, const HostSpace& h, DSpace* d, int base_slot_values = S_SPACE_VALUES) {
+  std::memset(d, 0, sizeof *d);
+  d->P = h.P;
+  d->R = (int)h.rkind.size();
+  int off = 0;
+  for (int p = 0; p < h.P; ++p) {
+    d->radix[p] = h.radix[p];
+    d->voff[p] = off;
+    off += h.radix[p];
+  }
+  int64_t* vals;
+  TRY(ws_t(c, base_slot_values, h.values.size(), &vals));
+  CU(cudaMemcpyAsync(vals, h.values.data(), h.values.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  d->values = vals;
+  for (int r = 0; r < d->R; ++r) {
+    d->rkind[r] = h.rkind[r];
+    d->rbound[r] = h.rbound[r];
+  }
+  for (int r = 0; r <= d->R; ++r) d->roff[r] = h.roff[r];
+  int* rp;
+  int64_t* rc;
+  TRY(ws_t(c, S_SPACE_RPOS, std::max<size_t>(1, h.rpos.size()), &rp));
+  TRY(ws_t(c, S_SPACE_RCOEFF, std::max<size_t>(1, h.rcoeff.size()), &rc));
+  if (!h.rpos.empty()) {
+    CU(cudaMemcpyAsync(rp, h.rpos.data(), h.rpos.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(rc, h.rcoeff.data(), h.rcoeff.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  d->rpos = rp;
+  d->rcoeff = rc;
+  return MLT_OK;
+}
+
+struct HostEns {
+  int k = 0, d = 0, h = 0;
+  std::vector<int> counts;
+  std::vector<double> packed;   // [w1 | b1 | w2 | b2 | mean | std]
+  const double* w1() const { return packed.data(); }
+  const double* b1() const { return w1() + (size_t)k * h * d; }
+  const double* w2() const { return b1() + (size_t)k * h; }
+  const double* b2() const { return w2() + (size_t)k * h; }
+  const double* mean() const { return b2() + k; }
+  const double* sd() const { return mean() + k; }
+};
+
+int read_ens(const mlt_ensemble* e, HostEns* h) {
+  if (!e) return fail(MLT_EINVAL, "ensemble is NULL");
+  if (e->k < 1) return fail(MLT_EINVAL, "an ensemble needs at least one member");
+  if (e->d < 1 || e->d > kMaxP) return fail(MLT_EINVAL, "input dimension must be 1..%d, got %d", kMaxP, e->d);
+  if (e->h < 1 || e->h > 4096) return fail(MLT_EINVAL, "bad hidden size %d", e->h);
+  h->k = e->k;
+  h->d = e->d;
+  h->h = e->h;
+  h->counts.assign(e->counts, e->counts + e->d);
+  for (int p = 0; p < e->d; ++p)
+    if (h->counts[p] < 1) return fail(MLT_EINVAL, "encoder parameter %d has no values", p);
+  const size_t nw = (size_t)e->k * e->h * e->d, nh = (size_t)e->k * e->h;
+  h->packed.resize(nw + 2 * nh + 3 * (size_t)e->k);
+  double* o = h->packed.data();
+  std::memcpy(o, e->w1, nw * 8);
+  std::memcpy(o + nw, e->b1, nh * 8);
+  std::memcpy(o + nw + nh, e->w2, nh * 8);
+  std::memcpy(o + nw + 2 * nh, e->b2, (size_t)e->k * 8);
+  std::memcpy(o + nw + 2 * nh + e->k, e->mean, (size_t)e->k * 8);
+  std::memcpy(o + nw + 2 * nh + 2 * e->k, e->std, (size_t)e->k * 8);
+  for (double x : h->packed)
+    if (!std::isfinite(x)) return fail(MLT_EINVAL, "network weights must be finite");
+  return MLT_OK;
+}
+
+int upload_ens(mlt_ctx* c, const HostEns& h, DEns* d, int slot = S_ENS) {
+  std::memset(d, 0, sizeof *d);
+  d->k = h.k;
+  d->d = h.d;
+  d->h = h.h;
+  for (int p = 0; p < h.d; ++p) d->counts[p] = h.counts[p];
+  double* buf;
+  TRY(ws_t(c, slot, h.packed.size(), &buf));
+  CU(cudaMemcpyAsync(buf, h.packed.data(), h.packed.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  const size_t nw = (size_t)h.k * h.h * h.d, nh = (size_t)h.k * h.h;
+  d->w1 = buf;
+  d->b1 = buf + nw;
+  d->w2 = buf + nw + nh;
+  d->b2 = buf + nw + 2 * nh;
+  d->mean = d->b2 + h.k;
+  d->std_ = d->mean + h.k;
+  return MLT_OK;
+}
+
+int launch_predict64(mlt_ctx* c, const DEns& e, const DSpace& s, int check_rules, int64_t begin,
+                     const int64_t* idx, const double* feat, int64_t n, double* pred, int64_t* idx_out,
+                     const float* band_v = nullptr, float band_theta = 0.f) {
+  if (n <= 0) return MLT_OK;
+  const size_t smem = predict64_smem(e);
+  if (smem > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem);
+  CU(cudaFuncSetAttribute(k_predict64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int nb = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_predict64, 128, smem));
+  nb = std::max(nb, 1);
+  const int64_t want = (n + 127) / 128;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nb * c->sms));
+  k_predict64<<<grid, 128, smem, c->stream>>>(e, s, check_rules, begin, idx, feat, n, pred, idx_out, band_v,
+                                              band_theta);
+  return check_launch(c);
+}
+
+// Sort (pred, idx) pairs ascending by pred, ties by idx. If `by_idx_first`,
+// the input is not already in index order and an index sort runs first
+// (radix sort is stable). Result lands in (*pred, *idx) (pointers may swap).
+int sort_pairs(mlt_ctx* c, double** pred, int64_t** idx, double* pred_alt, int64_t* idx_alt, int64_t n,
+               bool by_idx_first) {
+  if (n <= 1) return MLT_OK;
+  if (n > INT32_MAX) return fail(MLT_EINVAL, "too many entries to sort (%lld)", (long long)n);
+  cub::DoubleBuffer<double> kp(*pred, pred_alt);
+  cub::DoubleBuffer<int64_t> ki(*idx, idx_alt);
+  size_t tmp_bytes = 0, t2 = 0;
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kp, ki, (int)n, 0, 64, c->stream));
+  CU(cub::DeviceRadixSort::SortPairs(nullptr, t2, ki, kp, (int)n, 0, 64, c->stream));
+  tmp_bytes = std::max(tmp_bytes, t2);
+  void* tmp;
+  TRY(ws(c, S_SORT_TMP, tmp_bytes, &tmp));
+  if (by_idx_first) {
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ki, kp, (int)n, 0, 64, c->stream));
+    c->launches += 4;
+  }
+  CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kp, ki, (int)n, 0, 64, c->stream));
+  c->launches += 4;
+  CU(cudaGetLastError());
+  *pred = kp.Current();
+  *idx = ki.Current();
+  return MLT_OK;
+}
+
+// Copy the first min(m, n) sorted entries to the host; valid ones have idx != INT64_MAX.
+int emit_top(mlt_ctx* c, const double* pred, const int64_t* idx, int64_t n, int64_t m, int64_t* out_idx,
+             double* out_pred, int64_t* out_n) {
+  const int64_t take = std::min(m, n);
+  std::vector<int64_t> hi(take);
+  std::vector<double> hp(take);
+  if (take > 0) {
+    CU(cudaMemcpyAsync(hi.data(), idx, take * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(hp.data(), pred, take * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  int64_t cnt = 0;
+  for (int64_t t = 0; t < take; ++t) {
+    if (hi[t] == INT64_MAX || hi[t] < 0) break;
+    out_idx[cnt] = hi[t];
+    out_pred[cnt] = hp[t];
+    ++cnt;
+  }
+  *out_n = cnt;
+  return MLT_OK;
+}
+
+__global__ void k_merge_prep(const int64_t* idx, const double* pred, int64_t n, int64_t* io, double* po) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx[t];
+    const bool ok = i >= 0 && i != INT64_MAX;
+    io[t] = ok ? i : INT64_MAX;
+    po[t] = ok ? pred[t] : __longlong_as_double(0x7ff0000000000000ll);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan: resident descriptors + the fp32-sweep setup
+// ---------------------------------------------------------------------------
+struct mlt_plan {
+  mlt_ctx* ctx = nullptr;
+  HostSpace hs;
+  HostEns he;
+  // device copies (plan-owned, not workspace slots)
+  int64_t* d_values = nullptr;
+  int* d_rpos = nullptr;
+  int64_t* d_rcoeff = nullptr;
+  double* d_ens = nullptr;
+  double* d_tab = nullptr;      // [cshift | wprime] (k*kH each)
+  float* d_u = nullptr;         // [k*kH]
+  DSpace ds{};
+  DEns de{};
+  // sweep setup
+  bool band_ok = false;
+  std::string band_why;
+  int split = 0, G = 3, dummies = 0;
+  int64_t c_in = 1, c_in_pad = kThreads;
+  double delta = 0, cst = 0;
+};
+
+namespace {
+
+int plan_setup_band(mlt_plan* p) {
+  const HostEns& e = p->he;
+  const HostSpace& s = p->hs;
+  p->band_ok = false;
+  if (e.h > kH) {
+    p->band_why = "hidden size > 30";
+    return MLT_OK;
+  }
+  // split: inner = params [split, P); choose the largest inner cardinality
+  // <= 16384 that pads well to the 128-thread CTA.
+  int best = s.P;
+  int64_t best_cin = 1;
+  {
+    int64_t cin = 1;
+    int fallback = s.P;
+    int64_t fb_cin = 1;
+    for (int sp = s.P - 1; sp >= 0; --sp) {
+      cin *= s.radix[sp];
+      if (cin > 16384) break;
+      const int64_t pad = (cin + kThreads - 1) / kThreads * kThreads;
+      if ((double)cin / pad >= 0.75) {
+        best = sp;
+        best_cin = cin;
+      }
+      fallback = sp;
+      fb_cin = cin;
+    }
+    if (best == s.P) {
+      best = fallback;
+      best_cin = fb_cin;
+    }
+  }
+  p->split = best;
+  p->c_in = best_cin;
+  p->c_in_pad = (best_cin + kThreads - 1) / kThreads * kThreads;
+
+  const int KH = e.k * kH;
+  std::vector<double> cshift(KH, 0.0), wprime(KH, 0.0);
+  std::vector<float> u(KH, 1.0f);
+  double S = 0, log2dmax = -1e300, log2dmin = 1e300;
+  int dummies = 0;
+  bool ok = true;
+  std::string why;
+  for (int m = 0; m < e.k && ok; ++m) {
+    for (int j = 0; j < kH; ++j) {
+      const int mj = m * kH + j;
+      const double wp = (j < e.h) ? e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k : 0.0;
+      if (wp == 0.0) {
+        ++dummies;                // contributes exactly 1/d' = 1/(0*Eb' + 1) = 1
+        continue;
+      }
+      double amin = e.b1()[(size_t)m * e.h + j], amax = amin, bmin = 0, bmax = 0;
+      const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
+      for (int q = 0; q < s.P; ++q) {
+        if (s.radix[q] < 2) continue;
+        const double lo = std::min(0.0, w[q]), hi = std::max(0.0, w[q]);
+        if (q < p->split) {
+          amin += lo;
+          amax += hi;
+        } else {
+          bmin += lo;
+          bmax += hi;
+        }
+      }
+      const double c = 0.5 * (amin - bmin);
+      const double zmin = amin + bmin;
+      const double lw = std::log(std::fabs(wp));
+      const double lim = 80.0;
+      // exp(-A'), exp(-B')/w' and 1/w' must be normal fp32 numbers
+      if (!(amax - c <= lim && -(amin - c) <= lim && (bmax + c) + lw <= lim && -(bmin + c) - lw <= lim &&
+            std::fabs(lw) <= lim)) {
+        ok = false;
+        why = "first-layer range too wide for fp32 tables";
+        break;
+      }
+      cshift[mj] = c;
+      wprime[mj] = wp;
+      u[mj] = (float)(1.0 / wp);
+      S += std::fabs(wp);
+      const double l2max = (std::log1p(std::exp(std::min(-zmin, 700.0))) - lw) / std::log(2.0);
+      log2dmax = std::max(log2dmax, l2max);
+      log2dmin = std::min(log2dmin, -lw / std::log(2.0));
+    }
+  }
+  if (!ok) {
+    p->band_why = why;
+    return MLT_OK;
+  }
+  int G = 0;
+  for (int g = 3; g >= 1; --g) {
+    if (g * std::max(log2dmax, 0.0) < 124.0 && g * std::min(log2dmin, 0.0) > -124.0) {
+      G = g;
+      break;
+    }
+  }
+  if (p->ctx->opt_group >= 1 && p->ctx->opt_group <= 3) G = std::min(G, p->ctx->opt_group);
+  if (G == 0) {
+    p->band_why = "reciprocal products would overflow fp32";
+    return MLT_OK;
+  }
+  p->G = G;
+  p->dummies = dummies;
+  S += dummies;
+  double cst = 0;
+  for (int m = 0; m < e.k; ++m) cst += (e.b2()[m] * e.sd()[m] + e.mean()[m]) / e.k;
+  cst -= dummies;
+  p->cst = cst;
+  const double ngroups = (double)KH / G;
+  const double uu = std::ldexp(1.0, -24);
+  // a-priori |fp32 - exact| bound on the mean log: group
+  // arithmetic <= 30u per unit magnitude, accumulation <= ngroups*u*S, final adds.
+  p->delta = 2.0 * uu * ((32.0 + ngroups) * S + 2.0 * std::fabs(cst) + 2.0) + 1e-12 * (1.0 + std::fabs(cst));
+
+  std::vector<double> tab(2 * (size_t)KH);
+  std::copy(cshift.begin(), cshift.end(), tab.begin());
+  std::copy(wprime.begin(), wprime.end(), tab.begin() + KH);
+  mlt_ctx* c = p->ctx;
+  CU(cudaMalloc(&p->d_tab, tab.size() * 8));
+  CU(cudaMalloc(&p->d_u, (size_t)KH * 4));
+  CU(cudaMemcpyAsync(p->d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(p->d_u, u.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  p->band_ok = true;
+  return MLT_OK;
+}
+
+int plan_upload(mlt_plan* p) {
+  mlt_ctx* c = p->ctx;
+  const HostSpace& h = p->hs;
+  DSpace& d = p->ds;
+  std::memset(&d, 0, sizeof d);
+  d.P = h.P;
+  d.R = (int)h.rkind.size();
+  int off = 0;
+  for (int q = 0; q < h.P; ++q) {
+    d.radix[q] = h.radix[q];
+    d.voff[q] = off;
+    off += h.radix[q];
+  }
+  CU(cudaMalloc(&p->d_values, h.values.size() * 8));
+  CU(cudaMemcpyAsync(p->d_values, h.values.data(), h.values.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  d.values = p->d_values;
+  for (int r = 0; r < d.R; ++r) {
+    d.rkind[r] = h.rkind[r];
+    d.rbound[r] = h.rbound[r];
+  }
+  for (int r = 0; r <= d.R; ++r) d.roff[r] = h.roff[r];
+  CU(cudaMalloc(&p->d_rpos, std::max<size_t>(1, h.rpos.size()) * 4));
+  CU(cudaMalloc(&p->d_rcoeff, std::max<size_t>(1, h.rcoeff.size()) * 8));
+  if (!h.rpos.empty()) {
+    CU(cudaMemcpyAsync(p->d_rpos, h.rpos.data(), h.rpos.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(p->d_rcoeff, h.rcoeff.data(), h.rcoeff.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  d.rpos = p->d_rpos;
+  d.rcoeff = p->d_rcoeff;
+
+  const HostEns& e = p->he;
+  DEns& de = p->de;
+  std::memset(&de, 0, sizeof de);
+  de.k = e.k;
+  de.d = e.d;
+  de.h = e.h;
+  for (int q = 0; q < e.d; ++q) de.counts[q] = e.counts[q];
+  CU(cudaMalloc(&p->d_ens, e.packed.size() * 8));
+  CU(cudaMemcpyAsync(p->d_ens, e.packed.data(), e.packed.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  const size_t nw = (size_t)e.k * e.h * e.d, nh = (size_t)e.k * e.h;
+  de.w1 = p->d_ens;
+  de.b1 = p->d_ens + nw;
+  de.w2 = p->d_ens + nw + nh;
+  de.b2 = p->d_ens + nw + 2 * nh;
+  de.mean = de.b2 + e.k;
+  de.std_ = de.mean + e.k;
+  return MLT_OK;
+}
+
+void plan_free(mlt_plan* p) {
+  cudaFree(p->d_values);
+  cudaFree(p->d_rpos);
+  cudaFree(p->d_rcoeff);
+  cudaFree(p->d_ens);
+  cudaFree(p->d_tab);
+  cudaFree(p->d_u);
+}
+
+// fp64 materialise over a range or list, then sort: exact and general.
+int run_full(mlt_plan* p, int64_t m, int64_t begin, int64_t end, const int64_t* d_list, int64_t n_list,
+             int64_t* out_idx, double* out_pred, int64_t* out_n) {
+  mlt_ctx* c = p->ctx;
+  const int64_t n = d_list ? n_list : end - begin;
+  double *pa, *pb;
+  int64_t *ia, *ib;
+  TRY(ws_t(c, S_OUT_A, n, &pa));
+  TRY(ws_t(c, S_OUT_B, n, &pb));
+  TRY(ws_t(c, S_OUT_C, n, &ia));
+  TRY(ws_t(c, S_OUT_D, n, &ib));
+  TRY(launch_predict64(c, p->de, p->ds, 1, begin, d_list, nullptr, n, pa, ia));
+  TRY(sort_pairs(c, &pa, &ia, pb, ib, n, d_list != nullptr));
+  return emit_top(c, pa, ia, n, m, out_idx, out_pred, out_n);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// extern "C" API
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int mlt_abi_version(void) { return MLT_ABI_VERSION; }
+const char* mlt_last_error(void) { return g_err.c_str(); }
+
+int mlt_ctx_create(int device, mlt_ctx** out) {
+  if (!out) return fail(MLT_EINVAL, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(MLT_ECUDA, "no CUDA device available (%s); libmltune_b200 has no CPU fallback",
+                e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+  if (device < 0 || device >= n) return fail(MLT_EINVAL, "device %d out of range (%d devices)", device, n);
+  CU(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(MLT_ECUDA, "device %d is sm_%d%d; libmltune_b200 is built for sm_100a only", device, prop.major,
+                prop.minor);
+  mlt_ctx* c = new mlt_ctx();
+  c->dev = device;
+  c->sms = prop.multiProcessorCount;
+  CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->stream = c->own;
+  CU(cudaMallocHost(&c->pinned, 4096));
+  for (auto& ev : c->ev) CU(cudaEventCreate(&ev));
+  *out = c;
+  return MLT_OK;
+}
+
+int mlt_ctx_destroy(mlt_ctx* c) {
+  if (!c) return MLT_OK;
+  cudaSetDevice(c->dev);
+  cudaStreamSynchronize(c->stream);
+  for (void* p : c->slots)
+    if (p) cudaFree(p);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return MLT_OK;
+}
+
+int mlt_ctx_set_stream(mlt_ctx* c, void* stream) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  return MLT_OK;
+}
+
+int mlt_ctx_set_profiling(mlt_ctx* c, int on) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  c->prof = on != 0;
+  return MLT_OK;
+}
+
+int64_t mlt_ctx_launches(mlt_ctx* c) { return c ? c->launches : -1; }
+
+int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  switch (key) {
+    case MLT_OPT_PATH: c->opt_path = (int)value; return MLT_OK;
+    case MLT_OPT_GROUP: c->opt_group = (int)value; return MLT_OK;
+    case MLT_OPT_CAND_CAP: c->cand_cap = value < 0 ? (1 << 20) : std::max<int64_t>(value, 1); return MLT_OK;
+    default: return fail(MLT_EINVAL, "unknown option %d", key);
+  }
+}
+
+int mlt_decode(mlt_ctx* c, const mlt_space* space, const int64_t* idx, int64_t n, int64_t* values_out) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  if (n == 0) return MLT_OK;
+  CU(cudaSetDevice(c->dev));
+  HostSpace hs;
+  TRY(read_space(space, &hs));
+  for (int64_t t = 0; t < n; ++t)
+    if (idx[t] < 0 || idx[t] >= hs.card_i)
+      return fail(MLT_EINVAL, "index %lld out of range for %lld configurations", (long long)idx[t],
+                  (long long)hs.card_i);
+  DSpace ds;
+  TRY(upload_space(c, hs, &ds));
+  int64_t *di, *dv;
+  TRY(ws_t(c, S_IDX, n, &di));
+  TRY(ws_t(c, S_OUT_C, (size_t)n * hs.P, &dv));
+  CU(cudaMemcpyAsync(di, idx, n * 8, cudaMemcpyHostToDevice, c->stream));
+  k_decode<<<grid_for(c, n, 256), 256, 0, c->stream>>>(ds, di, n, dv);
+  TRY(check_launch(c));
+  CU(cudaMemcpyAsync(values_out, dv, (size_t)n * hs.P * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_valid_mask(mlt_ctx* c, const mlt_space* space, const int64_t* idx, int64_t n, uint8_t* mask_out) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  if (n == 0) return MLT_OK;
+  CU(cudaSetDevice(c->dev));
+  HostSpace hs;
+  TRY(read_space(space, &hs));
+  for (int64_t t = 0; t < n; ++t)
+    if (idx[t] < 0 || idx[t] >= hs.card_i)
+      return fail(MLT_EINVAL, "index %lld out of range for %lld configurations", (long long)idx[t],
+                  (long long)hs.card_i);
+  DSpace ds;
+  TRY(upload_space(c, hs, &ds));
+  int64_t* di;
+  uint8_t* dm;
+  TRY(ws_t(c, S_IDX, n, &di));
+  TRY(ws_t(c, S_OUT_C, n, &dm));
+  CU(cudaMemcpyAsync(di, idx, n * 8, cudaMemcpyHostToDevice, c->stream));
+  k_valid<<<grid_for(c, n, 256), 256, 0, c->stream>>>(ds, di, n, dm);
+  TRY(check_launch(c));
+  CU(cudaMemcpyAsync(mask_out, dm, n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_encode(mlt_ctx* c, const int32_t* counts, int32_t d, const int64_t* idx, int64_t n, double* feat_out) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (d < 1 || d > kMaxP) return fail(MLT_EINVAL, "input dimension must be 1..%d", kMaxP);
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  if (n == 0) return MLT_OK;
+  CU(cudaSetDevice(c->dev));
+  DEns e;
+  std::memset(&e, 0, sizeof e);
+  e.d = d;
+  for (int p = 0; p < d; ++p) {
+    if (counts[p] < 1) return fail(MLT_EINVAL, "encoder parameter %d has no values", p);
+    e.counts[p] = counts[p];
+  }
+  int64_t* di;
+  double* df;
+  TRY(ws_t(c, S_IDX, n, &di));
+  TRY(ws_t(c, S_FEAT, (size_t)n * d, &df));
+  CU(cudaMemcpyAsync(di, idx, n * 8, cudaMemcpyHostToDevice, c->stream));
+  k_encode<<<grid_for(c, n, 256), 256, 0, c->stream>>>(e, di, n, df);
+  TRY(check_launch(c));
+  CU(cudaMemcpyAsync(feat_out, df, (size_t)n * d * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_predict_indices(mlt_ctx* c, const mlt_ensemble* ens, const int64_t* idx, int64_t n, double* pred_out) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  CU(cudaSetDevice(c->dev));
+  HostEns he;
+  TRY(read_ens(ens, &he));
+  if (n == 0) return MLT_OK;
+  for (int64_t t = 0; t < n; ++t)
+    if (idx[t] < 0) return fail(MLT_EINVAL, "negative configuration index %lld", (long long)idx[t]);
+  DEns de;
+  TRY(upload_ens(c, he, &de));
+  DSpace ds;
+  std::memset(&ds, 0, sizeof ds);
+  int64_t* di;
+  double* dp;
+  TRY(ws_t(c, S_IDX, n, &di));
+  TRY(ws_t(c, S_OUT_A, n, &dp));
+  CU(cudaMemcpyAsync(di, idx, n * 8, cudaMemcpyHostToDevice, c->stream));
+  TRY(launch_predict64(c, de, ds, 0, 0, di, nullptr, n, dp, nullptr));
+  CU(cudaMemcpyAsync(pred_out, dp, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_predict_features(mlt_ctx* c, const mlt_ensemble* ens, const double* x, int64_t n, double* pred_out) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  CU(cudaSetDevice(c->dev));
+  HostEns he;
+  TRY(read_ens(ens, &he));
+  if (n == 0) return MLT_OK;
+  DEns de;
+  TRY(upload_ens(c, he, &de));
+  DSpace ds;
+  std::memset(&ds, 0, sizeof ds);
+  double *dx, *dp;
+  TRY(ws_t(c, S_FEAT, (size_t)n * he.d, &dx));
+  TRY(ws_t(c, S_OUT_A, n, &dp));
+  CU(cudaMemcpyAsync(dx, x, (size_t)n * he.d * 8, cudaMemcpyHostToDevice, c->stream));
+  TRY(launch_predict64(c, de, ds, 0, 0, nullptr, dx, n, dp, nullptr));
+  CU(cudaMemcpyAsync(pred_out, dp, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_member_outputs(mlt_ctx* c, const mlt_ensemble* ens, const double* x, int64_t n, double* out) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  CU(cudaSetDevice(c->dev));
+  HostEns he;
+  TRY(read_ens(ens, &he));
+  if (n == 0) return MLT_OK;
+  DEns de;
+  TRY(upload_ens(c, he, &de));
+  double *dx, *dp;
+  TRY(ws_t(c, S_FEAT, (size_t)n * he.d, &dx));
+  TRY(ws_t(c, S_OUT_A, (size_t)n * he.k, &dp));
+  CU(cudaMemcpyAsync(dx, x, (size_t)n * he.d * 8, cudaMemcpyHostToDevice, c->stream));
+  const size_t smem = predict64_smem(de);
+  if (smem > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem);
+  CU(cudaFuncSetAttribute(k_member_out64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_member_out64<<<grid_for(c, n, 128), 128, smem, c->stream>>>(de, dx, n, dp);
+  TRY(check_launch(c));
+  CU(cudaMemcpyAsync(out, dp, (size_t)n * he.k * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, mlt_plan** out) {
+  if (!c || !out) return fail(MLT_EINVAL, "ctx/out is NULL");
+  *out = nullptr;
+  CU(cudaSetDevice(c->dev));
+  mlt_plan* p = new mlt_plan();
+  p->ctx = c;
+  int rc = read_space(space, &p->hs);
+  if (rc == MLT_OK) rc = read_ens(ens, &p->he);
+  if (rc == MLT_OK && p->he.d != p->hs.P)
+    rc = fail(MLT_EMISMATCH, "ensemble has %d inputs but the space has %d parameters", p->he.d, p->hs.P);
+  for (int q = 0; rc == MLT_OK && q < p->hs.P; ++q)
+    if (p->he.counts[q] != p->hs.radix[q])
+      rc = fail(MLT_EMISMATCH, "encoder parameter %d has %d values, space has %d", q, p->he.counts[q],
+                p->hs.radix[q]);
+  if (rc == MLT_OK) rc = plan_upload(p);
+  if (rc == MLT_OK) rc = plan_setup_band(p);
+  if (rc != MLT_OK) {
+    plan_free(p);
+    delete p;
+    return rc;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  *out = p;
+  return MLT_OK;
+}
+
+int mlt_plan_destroy(mlt_plan* p) {
+  if (!p) return MLT_OK;
+  cudaSetDevice(p->ctx->dev);
+  cudaStreamSynchronize(p->ctx->stream);
+  plan_free(p);
+  delete p;
+  return MLT_OK;
+}
+
+static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, const int64_t* idx_list,
+                           int64_t n_list, int64_t* out_idx, double* out_pred, int64_t* out_n,
+                           mlt_sweep_stats* st) {
+  mlt_ctx* c = p->ctx;
+  if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
+  if (!out_idx || !out_pred || !out_n) return fail(MLT_EINVAL, "output pointers are NULL");
+  CU(cudaSetDevice(c->dev));
+  *out_n = 0;
+  mlt_sweep_stats local;
+  std::memset(&local, 0, sizeof local);
+  const int64_t l0 = c->launches;
+  const int64_t card = p->hs.card_i;
+  int64_t n;
+  if (idx_list) {
+    if (n_list < 0) return fail(MLT_EINVAL, "negative list length");
+    for (int64_t t = 0; t < n_list; ++t)
+      if (idx_list[t] < 0 || idx_list[t] >= card)
+        return fail(MLT_EINVAL, "index %lld out of range for %lld configurations", (long long)idx_list[t],
+                    (long long)card);
+    n = n_list;
+  } else {
+    if (begin < 0 || end > card || begin > end)
+      return fail(MLT_EINVAL, "slice [%lld, %lld) outside [0, %lld)", (long long)begin, (long long)end,
+                  (long long)card);
+    n = end - begin;
+  }
+  local.configs = n;
+  local.split = p->hs.P - p->split;
+  if (n == 0) {
+    if (st) *st = local;
+    return MLT_OK;
+  }
+  if (c->prof) CU(cudaEventRecord(c->ev[0], c->stream));
+
+  bool band = !idx_list && p->band_ok && m <= kMaxTopM && n >= 4096;
+  if (c->opt_path == 0 && !idx_list && p->band_ok && m <= kMaxTopM) band = true;
+  if (c->opt_path == 1) band = false;
+
+  if (band) {
+    const int KH = p->he.k * kH;
+    const int64_t o_lo = begin / p->c_in;
+    const int64_t o_hi = (end - 1) / p->c_in + 1;
+    const int n_ob = (int)((o_hi - o_lo + kOB - 1) / kOB);
+    const int n_ib = (int)(p->c_in_pad / kThreads);
+    float *ea, *ebp, *cval;
+    int64_t* cidx;
+    uint32_t* gs;
+    TRY(ws_t(c, S_EA, (size_t)n_ob * KH * kOB, &ea));
+    TRY(ws_t(c, S_EBP, (size_t)KH * p->c_in_pad, &ebp));
+    TRY(ws_t(c, S_GSCAL, 4, &gs));
+    TRY(ws_t(c, S_CIDX, (size_t)c->cand_cap, &cidx));
+    TRY(ws_t(c, S_CVAL, (size_t)c->cand_cap, &cval));
+    TableArgs ta;
+    std::memset(&ta, 0, sizeof ta);
+    ta.k = p->he.k;
+    ta.d = p->he.d;
+    ta.h = p->he.h;
+    ta.split = p->split;
+    for (int q = 0; q < p->hs.P; ++q) ta.radix[q] = p->hs.radix[q];
+    ta.w1 = p->de.w1;
+    ta.b1 = p->de.b1;
+    ta.cshift = p->d_tab;
+    ta.wprime = p->d_tab + KH;
+    ta.o_lo = o_lo;
+    ta.c_in = p->c_in;
+    ta.c_in_pad = p->c_in_pad;
+    ta.n_ob = n_ob;
+    ta.ea = ea;
+    ta.ebp = ebp;
+    uint32_t* hs = static_cast<uint32_t*>(c->pinned);
+    hs[0] = 0xFF800000u;   // fkey(+inf)
+    hs[1] = 0u;
+    CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
+    k_table_outer<<<grid_for(c, (int64_t)n_ob * KH * kOB, 256), 256, 0, c->stream>>>(ta);
+    TRY(check_launch(c));
+    k_table_inner<<<grid_for(c, (int64_t)KH * p->c_in_pad, 256), 256, 0, c->stream>>>(ta);
+    TRY(check_launch(c));
+
+    SweepArgs sa;
+    std::memset(&sa, 0, sizeof sa);
+    sa.k = p->he.k;
+    sa.ea = ea;
+    sa.ebp = ebp;
+    sa.u = p->d_u;
+    sa.c_in = p->c_in;
+    sa.c_in_pad = p->c_in_pad;
+    sa.o_lo = o_lo;
+    sa.n_ob = n_ob;
+    sa.n_ib = n_ib;
+    sa.begin = begin;
+    sa.end = end;
+    sa.cst = (float)p->cst;
+    sa.band = (float)(2.0 * p->delta * (1.0 + 1e-6));
+    sa.m = (int)m;
+    sa.g_theta = gs;
+    sa.g_count = gs + 1;
+    sa.g_cidx = cidx;
+    sa.g_cval = cval;
+    sa.cap = (uint32_t)std::min<int64_t>(c->cand_cap, UINT32_MAX);
+    sa.check_rules = p->ds.R > 0;
+    sa.sp = p->ds;
+    const size_t smem = sweep_smem(p->he.k);
+    if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);
+    void (*kern)(SweepArgs) = p->G == 3 ? k_sweep<3> : (p->G == 2 ? k_sweep<2> : k_sweep<1>);
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));
+    nb = std::max(nb, 1);
+    const int64_t items = (int64_t)n_ob * n_ib;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nb * c->sms));
+    if (c->prof) CU(cudaEventRecord(c->ev[1], c->stream));
+    kern<<<grid, kThreads, smem, c->stream>>>(sa);
+    TRY(check_launch(c));
+    if (c->prof) CU(cudaEventRecord(c->ev[2], c->stream));
+    CU(cudaMemcpyAsync(hs, gs, 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    const uint32_t theta_key = hs[0], count = hs[1];
+    local.group = p->G;
+    local.delta = p->delta;
+    if ((int64_t)count > c->cand_cap) {
+      band = false;   // crowded guard band: fall back to the exact materialising path
+    } else {
+      local.candidates = count;
+      // decode the final threshold on the host (same ordered-key map as the device)
+      uint32_t b = (theta_key & 0x80000000u) ? (theta_key & 0x7fffffffu) : ~theta_key;
+      float theta;
+      std::memcpy(&theta, &b, 4);
+      double *pa, *pb;
+      int64_t *ia, *ib;
+      TRY(ws_t(c, S_OUT_A, std::max<uint32_t>(count, 1), &pa));
+      TRY(ws_t(c, S_OUT_B, std::max<uint32_t>(count, 1), &pb));
+      TRY(ws_t(c, S_OUT_C, std::max<uint32_t>(count, 1), &ia));
+      TRY(ws_t(c, S_OUT_D, std::max<uint32_t>(count, 1), &ib));
+      TRY(launch_predict64(c, p->de, p->ds, 0, 0, cidx, nullptr, count, pa, ia, cval, theta));
+      double* pcur = pa;
+      int64_t* icur = ia;
+      TRY(sort_pairs(c, &pcur, &icur, pb, ib, count, true));
+      TRY(emit_top(c, pcur, icur, count, m, out_idx, out_pred, out_n));
+    }
+    if (c->prof) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
+      local.sweep_ms = ms;
+    }
+  }
+  if (!band) {
+    local.path = 1;
+    local.candidates = 0;
+    const int64_t* dl = nullptr;
+    if (idx_list) {
+      int64_t* di;
+      TRY(ws_t(c, S_IDX, n, &di));
+      CU(cudaMemcpyAsync(di, idx_list, n * 8, cudaMemcpyHostToDevice, c->stream));
+      dl = di;
+    }
+    if (c->prof) CU(cudaEventRecord(c->ev[1], c->stream));
+    TRY(run_full(p, m, begin, end, dl, n, out_idx, out_pred, out_n));
+    if (c->prof) {
+      CU(cudaEventRecord(c->ev[2], c->stream));
+      CU(cudaEventSynchronize(c->ev[2]));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
+      local.sweep_ms = ms;
+    }
+  }
+  if (c->prof) {
+    CU(cudaEventRecord(c->ev[3], c->stream));
+    CU(cudaEventSynchronize(c->ev[3]));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]));
+    local.total_ms = ms;
+  }
+  local.launches = (int32_t)(c->launches - l0);
+  if (st) *st = local;
+  return MLT_OK;
+}
+
+int mlt_plan_top_m(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* out_idx, double* out_pred,
+                   int64_t* out_n, mlt_sweep_stats* st) {
+  if (!p) return fail(MLT_EINVAL, "plan is NULL");
+  return plan_top_m_impl(p, m, begin, end, nullptr, 0, out_idx, out_pred, out_n, st);
+}
+
+int mlt_top_m(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, int64_t m, int64_t begin, int64_t end,
+              const int64_t* idx_list, int64_t n_list, int64_t* out_idx, double* out_pred, int64_t* out_n,
+              mlt_sweep_stats* st) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
+  mlt_plan* p = nullptr;
+  TRY(mlt_plan_create(c, space, ens, &p));
+  const int rc = plan_top_m_impl(p, m, begin, end, idx_list, n_list, out_idx, out_pred, out_n, st);
+  mlt_plan_destroy(p);
+  return rc;
+}
+
+int mlt_merge_top_m(mlt_ctx* c, const int64_t* dev_idx, const double* dev_pred, int64_t n, int64_t m,
+                    int64_t* out_idx, double* out_pred, int64_t* out_n) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  CU(cudaSetDevice(c->dev));
+  *out_n = 0;
+  if (n == 0) return MLT_OK;
+  double *pa, *pb;
+  int64_t *ia, *ib;
+  TRY(ws_t(c, S_OUT_A, n, &pa));
+  TRY(ws_t(c, S_OUT_B, n, &pb));
+  TRY(ws_t(c, S_OUT_C, n, &ia));
+  TRY(ws_t(c, S_OUT_D, n, &ib));
+  k_merge_prep<<<grid_for(c, n, 256), 256, 0, c->stream>>>(dev_idx, dev_pred, n, ia, pa);
+  TRY(check_launch(c));
+  TRY(sort_pairs(c, &pa, &ia, pb, ib, n, true));
+  return emit_top(c, pa, ia, n, m, out_idx, out_pred, out_n);
+}
+
+int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* launches, const mlt_train_desc* dd, double* w1,
+                           double* b1, double* w2, double* b2, double* lf, double* ll, int32_t* div, const char** err);
+
+int mlt_train_members(mlt_ctx* c, const mlt_train_desc* desc, double* w1, double* b1, double* w2, double* b2,
+                      double* loss_first, double* loss_final, int32_t* diverged_epoch) {
+  if (!c || !desc) return fail(MLT_EINVAL, "ctx/desc is NULL");
+  const char* err = "";
+  const int rc = mlt_train_members_impl(c->dev, c->stream, &c->launches, desc, w1, b1, w2, b2, loss_first,
+                                        loss_final, diverged_epoch, &err);
+  if (rc != MLT_OK) return fail(rc, "%s", err);
+  return MLT_OK;
+}
+
+}  // extern "C"

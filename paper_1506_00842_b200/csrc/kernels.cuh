@@ -1,0 +1,68 @@
+// kernels.cuh — declarations shared by the kernel translation units and the
+// host-side C-ABI implementation (abi.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace mlt {
+
+// ---- exact fp64 kernels (predict.cu) --------------------------------------
+__global__ void k_decode(DSpace s, const int64_t* idx, int64_t n, int64_t* out);
+__global__ void k_valid(DSpace s, const int64_t* idx, int64_t n, uint8_t* out);
+__global__ void k_encode(DEns e, const int64_t* idx, int64_t n, double* out);
+__global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, const int64_t* idx,
+                            const double* feat, int64_t n, double* pred, int64_t* idx_out,
+                            const float* band_v, float band_theta);
+__global__ void k_member_out64(DEns e, const double* feat, int64_t n, double* out);
+size_t predict64_smem(const DEns& e);
+
+// ---- fp32 factored sweep (sweep.cu) ---------------------------------------
+constexpr int kThreads = 128;   // inner configurations per work item (one per thread)
+constexpr int kOB = 32;         // outer configurations per work item (per thread)
+constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
+constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
+constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
+
+struct SweepArgs {
+  int k;                        // members
+  const float* ea;              // [n_ob][k*kH][kOB]  exp(-A') of outer configurations
+  const float* ebp;             // [k*kH][c_in_pad]   exp(-B') / w' of inner configurations
+  const float* u;               // [k*kH]             1 / w'
+  int64_t c_in, c_in_pad;       // inner cardinality (and padded to kThreads)
+  int64_t o_lo;                 // outer index of ea block 0, row 0
+  int n_ob, n_ib;               // outer blocks x inner blocks = work items
+  int64_t begin, end;           // configuration range of this call
+  float cst;                    // sum_m (b2*std + mean)/k - (#dummy units)
+  float band;                   // 2*delta (rounded up)
+  int m;
+  uint32_t* g_theta;            // ordered-key threshold (atomicMin)
+  uint32_t* g_count;            // candidates appended (may exceed cap -> overflow)
+  int64_t* g_cidx;
+  float* g_cval;
+  uint32_t cap;
+  int check_rules;
+  DSpace sp;
+};
+
+// Tables of the factored first layer (sweep.cu).
+struct TableArgs {
+  int k, d, h, split;           // params [0, split) are outer, [split, d) inner
+  int radix[kMaxP];
+  const double* w1;             // [k][h][d]
+  const double* b1;             // [k][h]
+  const double* cshift;         // [k*kH] centring constant c
+  const double* wprime;         // [k*kH] w2*std/k (0 for dummy units)
+  int64_t o_lo, c_in, c_in_pad;
+  int n_ob;
+  float* ea;
+  float* ebp;
+};
+
+__global__ void k_table_outer(TableArgs t);
+__global__ void k_table_inner(TableArgs t);
+
+template <int G>
+__global__ void k_sweep(SweepArgs a);
+size_t sweep_smem(int k);
+
+}  // namespace mlt

@@ -1,0 +1,456 @@
+// sweep.cu — the fp32 factored full-space sweep with a streaming guard-band
+// top-m (north-star subsystems 1 + 2; reference tuner.py:95-131 over
+// paramspace.py:184-213 and model.py:88-97, :146-170, :290-301).
+//
+// Algebra (exact, no approximation beyond fp32 rounding):
+//   z_mj(idx) = A_mj(outer digits) + B_mj(inner digits)     (first layer is linear)
+//   E = exp(-z) = Ea(outer) * Eb(inner),  Ea = exp(-(A - c)), Eb = exp(-(B + c))
+//   w'_mj = w2_mj * std_m / k,   w' * sigmoid(z) = 1 / d',   d' = Ea * (Eb/w') + 1/w'
+// so one hidden unit of one member costs ONE fp32 FMA for d' (no exp, no
+// dot product). G units share one reciprocal:
+//   G=3: 1/d0 + 1/d1 + 1/d2 = (d2*(d0+d1) + d0*d1) / (d0*d1*d2)
+// which balances the FMA pipe (8/3 lane-ops per unit) against the MUFU pipe
+// (1/3 reciprocal per unit). Two outer configurations ride in one f32x2
+// register (FFMA2/FMUL2/FADD2), halving issue slots.
+//
+// Mean log time = sum over all units of 1/d' + cst.  Every value within
+// `band` (= 2*delta, an a-priori fp32 error bound) of the running m-th best is
+// kept as a candidate; candidates are rescored exactly in fp64 (k_predict64)
+// and sorted by (prediction, index), which reproduces the reference's
+// lexsort((indices, preds)) selection exactly.
+#include "kernels.cuh"
+
+namespace mlt {
+
+// ---------------------------------------------------------------------------
+// Tables
+// ---------------------------------------------------------------------------
+
+__global__ void k_table_outer(TableArgs t) {
+  const int KH = t.k * kH;
+  const int64_t total = (int64_t)t.n_ob * KH * kOB;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(q % kOB);
+    const int mj = (int)((q / kOB) % KH);
+    const int64_t ob = q / ((int64_t)kOB * KH);
+    const int m = mj / kH, j = mj % kH;
+    float out = 1.0f;
+    if (j < t.h && t.wprime[mj] != 0.0) {
+      uint64_t o = (uint64_t)(t.o_lo + ob * kOB + r);
+      const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
+      double acc = 0.0;
+      for (int p = t.split - 1; p >= 0; --p) {
+        const uint64_t c = (uint64_t)t.radix[p];
+        const uint64_t qq = o / c;
+        const int dig = (int)(o - qq * c);
+        o = qq;
+        const double x = (double)dig / (double)(t.radix[p] > 1 ? t.radix[p] - 1 : 1);
+        acc = fma(x, w[p], acc);
+      }
+      const double a = acc + t.b1[(size_t)m * t.h + j] - t.cshift[mj];
+      out = (float)exp(-a);
+    }
+    t.ea[q] = out;
+  }
+}
+
+__global__ void k_table_inner(TableArgs t) {
+  const int KH = t.k * kH;
+  const int64_t total = (int64_t)KH * t.c_in_pad;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q % t.c_in_pad;
+    const int mj = (int)(q / t.c_in_pad);
+    const int m = mj / kH, j = mj % kH;
+    float out = 0.0f;
+    if (i < t.c_in && j < t.h && t.wprime[mj] != 0.0) {
+      uint64_t r = (uint64_t)i;
+      const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
+      double acc = 0.0;
+      for (int p = t.d - 1; p >= t.split; --p) {
+        const uint64_t c = (uint64_t)t.radix[p];
+        const uint64_t qq = r / c;
+        const int dig = (int)(r - qq * c);
+        r = qq;
+        const double x = (double)dig / (double)(t.radix[p] > 1 ? t.radix[p] - 1 : 1);
+        acc = fma(x, w[p], acc);
+      }
+      out = (float)(exp(-(acc + t.cshift[mj])) / t.wprime[mj]);
+    }
+    t.ebp[q] = out;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// packed fp32 helpers (sm_100: FFMA2 / FMUL2 / FADD2)
+// ---------------------------------------------------------------------------
+typedef unsigned long long f2;
+
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float rcpa(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// G hidden units -> (num, den) with sum_g 1/d_g = num/den.
+template <int G>
+__device__ __forceinline__ void combine(const f2 (&d)[G], f2& num, f2& den);
+template <>
+__device__ __forceinline__ void combine<1>(const f2 (&d)[1], f2& num, f2& den) {
+  num = pk(1.0f, 1.0f);
+  den = d[0];
+}
+template <>
+__device__ __forceinline__ void combine<2>(const f2 (&d)[2], f2& num, f2& den) {
+  num = fadd2(d[0], d[1]);
+  den = fmul2(d[0], d[1]);
+}
+template <>
+__device__ __forceinline__ void combine<3>(const f2 (&d)[3], f2& num, f2& den) {
+  const f2 s = fadd2(d[0], d[1]);
+  const f2 p = fmul2(d[0], d[1]);
+  num = ffma2(d[2], s, p);
+  den = fmul2(p, d[2]);
+}
+
+// ---------------------------------------------------------------------------
+// block-wide radix select: the exact m-th smallest ordered key (1-based)
+// among keys visited by `visit` (each thread visits its own keys).
+// ---------------------------------------------------------------------------
+template <typename V>
+__device__ __forceinline__ uint32_t block_select(V visit, int m, uint32_t* s_hist, uint32_t* s_sel) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t prefix = 0;
+  uint32_t want = (uint32_t)m;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int b = tid; b < 256; b += blockDim.x) s_hist[b] = 0u;
+    __syncthreads();
+    visit([&](uint32_t key) {
+      if (pass == 0 || (key >> (shift + 8)) == prefix) {
+        const uint32_t bin = (key >> shift) & 255u;
+        const uint32_t peers = __match_any_sync(__activemask(), bin);
+        if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], (uint32_t)__popc(peers));
+      }
+    });
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        c[b] = s_hist[lane * 8 + b];
+        tot += c[b];
+      }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - tot;
+      if (excl < want && want <= incl) {
+        uint32_t run = excl;
+        int bin = lane * 8 + 7;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (run + c[b] >= want) {
+            bin = lane * 8 + b;
+            break;
+          }
+          run += c[b];
+        }
+        s_sel[0] = (prefix << 8) | (uint32_t)bin;
+        s_sel[1] = want - run;
+      }
+    }
+    __syncthreads();
+    prefix = s_sel[0];
+    want = s_sel[1];
+  }
+  return prefix;
+}
+
+__device__ __forceinline__ void gappend(const SweepArgs& a, int64_t idx, float v) {
+  const uint32_t slot = atomicAdd(a.g_count, 1u);
+  if (slot < a.cap) {
+    a.g_cidx[slot] = idx;
+    a.g_cval[slot] = v;
+  }
+}
+
+__device__ __forceinline__ void lower_threshold(const SweepArgs& a, uint32_t* s_th, uint32_t nth_key) {
+  // new threshold = (m-th best) + band, rounded up so it stays an upper bound
+  const uint32_t nk = fkey(__fadd_ru(fkey_inv(nth_key), a.band));
+  if (threadIdx.x == 0 && nk < *s_th) {
+    *s_th = nk;
+    atomicMin(a.g_theta, nk);
+  }
+}
+
+size_t sweep_smem(int k) {
+  const size_t KH = (size_t)k * kH;
+  return KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4;
+}
+
+// ---------------------------------------------------------------------------
+// the sweep
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_sweep(SweepArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int KH = a.k * kH;
+  float* s_ea = reinterpret_cast<float*>(smraw);                 // [KH][kOB]
+  float* s_u = s_ea + (size_t)KH * kOB;                          // [KH]
+  int64_t* s_bidx = reinterpret_cast<int64_t*>(s_u + ((KH + 3) & ~3));
+  float* s_bval = reinterpret_cast<float*>(s_bidx + kSB);
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_bval + kSB);
+  __shared__ int s_n, s_tot;
+  __shared__ uint32_t s_th, s_sel[2], s_wsum[kThreads / 32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int q = tid; q < KH; q += kThreads) s_u[q] = a.u[q];
+  if (tid == 0) {
+    s_n = 0;
+    s_th = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
+  }
+  const int ngroups = KH / G;
+  const int n_items = a.n_ob * a.n_ib;
+
+  for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int ob = w / a.n_ib, ib = w - ob * a.n_ib;
+    __syncthreads();
+    {  // stage exp(-A') of this outer block: [KH][kOB] floats, contiguous in global
+      const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)ob * KH * kOB);
+      float4* dst = reinterpret_cast<float4*>(s_ea);
+      for (int q = tid; q < KH * kOB / 4; q += kThreads) dst[q] = __ldg(src + q);
+    }
+    if (tid == 0) {
+      s_tot = 0;
+      const uint32_t g = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
+      if (g < s_th) s_th = g;
+    }
+    __syncthreads();
+
+    const int64_t i = (int64_t)ib * kThreads + tid;
+    const float* ebcol = a.ebp + i;
+    f2 acc[kOB / 2];
+#pragma unroll
+    for (int q = 0; q < kOB / 2; ++q) acc[q] = 0ull;
+
+    float eb[G], uu[G];
+#pragma unroll
+    for (int x = 0; x < G; ++x) {
+      eb[x] = __ldg(ebcol + (size_t)x * a.c_in_pad);
+      uu[x] = s_u[x];
+    }
+#pragma unroll 1
+    for (int gi = 0; gi < ngroups; ++gi) {
+      const int mj0 = gi * G;
+      // prefetch the next group's per-thread factors (global/L2 latency)
+      float ebn[G], un[G];
+      const int mjn = (gi + 1 < ngroups) ? mj0 + G : mj0;
+#pragma unroll
+      for (int x = 0; x < G; ++x) {
+        ebn[x] = __ldg(ebcol + (size_t)(mjn + x) * a.c_in_pad);
+        un[x] = s_u[mjn + x];
+      }
+      const float* E = s_ea + (size_t)mj0 * kOB;
+#pragma unroll
+      for (int q = 0; q < kOB / 4; ++q) {
+        float4 ea[G];
+#pragma unroll
+        for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * kOB + 4 * q);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          f2 d[G];
+#pragma unroll
+          for (int x = 0; x < G; ++x) {
+            const f2 A = half ? pk(ea[x].z, ea[x].w) : pk(ea[x].x, ea[x].y);
+            d[x] = ffma2(A, pk(eb[x], eb[x]), pk(uu[x], uu[x]));
+          }
+          f2 num, den;
+          combine<G>(d, num, den);
+          float dl, dh;
+          upk(den, dl, dh);
+          const f2 r = pk(rcpa(dl), rcpa(dh));
+          acc[2 * q + half] = (G == 1) ? fadd2(acc[2 * q + half], r) : ffma2(num, r, acc[2 * q + half]);
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < G; ++x) {
+        eb[x] = ebn[x];
+        uu[x] = un[x];
+      }
+    }
+
+    // ---- candidates ---------------------------------------------------------
+    float v[kOB];
+#pragma unroll
+    for (int q = 0; q < kOB / 2; ++q) {
+      upk(acc[q], v[2 * q], v[2 * q + 1]);
+      v[2 * q] += a.cst;
+      v[2 * q + 1] += a.cst;
+    }
+    const int64_t obase = a.o_lo + (int64_t)ob * kOB;
+    const bool ival = i < a.c_in;
+    uint32_t mask = 0;
+    {
+      const float thf = fkey_inv(s_th);
+#pragma unroll
+      for (int r = 0; r < kOB; ++r) {
+        const int64_t idx = (obase + r) * a.c_in + i;
+        const bool in = ival && idx >= a.begin && idx < a.end;
+        if (in && !(v[r] > thf)) mask |= 1u << r;   // NaN passes (never silently dropped)
+      }
+    }
+    if (a.check_rules && mask) {
+#pragma unroll 1
+      for (int r = 0; r < kOB; ++r) {
+        if (mask & (1u << r)) {
+          int dig[kMaxP];
+          decode_digits(a.sp, (uint64_t)((obase + r) * a.c_in + i), dig);
+          if (!rules_ok(a.sp, dig)) mask &= ~(1u << r);
+        }
+      }
+    }
+    {
+      int c = __popc(mask);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0 && c) atomicAdd(&s_tot, c);
+    }
+    __syncthreads();
+    if (s_n + s_tot > kSBLimit && s_tot >= a.m) {
+      // too many pass: the m-th best of this work item bounds the global m-th best
+      const uint32_t key = block_select(
+          [&](auto&& f) {
+#pragma unroll
+            for (int r = 0; r < kOB; ++r)
+              if (mask & (1u << r)) f(fkey(v[r]));
+          },
+          a.m, s_hist, s_sel);
+      lower_threshold(a, &s_th, key);
+      __syncthreads();
+      const float thf = fkey_inv(s_th);
+#pragma unroll
+      for (int r = 0; r < kOB; ++r)
+        if (v[r] > thf) mask &= ~(1u << r);
+    }
+    {  // append: warp-aggregated slot reservation
+      const int c = __popc(mask);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int base = 0;
+      if (lane == 31 && incl) base = atomicAdd(&s_n, incl);
+      base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+#pragma unroll
+      for (int r = 0; r < kOB; ++r) {
+        if (mask & (1u << r)) {
+          const int64_t idx = (obase + r) * a.c_in + i;
+          if (base < kSB) {
+            s_bidx[base] = idx;
+            s_bval[base] = v[r];
+          } else {
+            gappend(a, idx, v[r]);
+          }
+          ++base;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_n > kSBLimit) {
+      // compact the CTA buffer around its own m-th best
+      const int n = min(s_n, kSB);
+      if (n >= a.m) {
+        const uint32_t key = block_select(
+            [&](auto&& f) {
+              for (int e = tid; e < n; e += kThreads) f(fkey(s_bval[e]));
+            },
+            a.m, s_hist, s_sel);
+        lower_threshold(a, &s_th, key);
+        __syncthreads();
+      }
+      const float thf = fkey_inv(s_th);
+      constexpr int kPer = kSB / kThreads;
+      int64_t ki[kPer];
+      float kv[kPer];
+      uint32_t keep = 0;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        const int slot = tid * kPer + e;
+        if (slot < n) {
+          ki[e] = s_bidx[slot];
+          kv[e] = s_bval[slot];
+          if (!(kv[e] > thf)) keep |= 1u << e;
+        }
+      }
+      const int c = __popc(keep);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      int off = incl - c, total = 0;
+      for (int q = 0; q < kThreads / 32; ++q) {
+        if (q < warp) off += s_wsum[q];
+        total += s_wsum[q];
+      }
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        if (keep & (1u << e)) {
+          s_bidx[off] = ki[e];
+          s_bval[off] = kv[e];
+          ++off;
+        }
+      }
+      __syncthreads();
+      if (total > kSBLimit) {  // a crowded band: spill everything to the global buffer
+        for (int e = tid; e < total; e += kThreads) gappend(a, s_bidx[e], s_bval[e]);
+        total = 0;
+      }
+      if (tid == 0) s_n = total;
+    }
+  }
+  __syncthreads();
+  {  // final flush of this CTA's candidates
+    const float thf = fkey_inv(s_th);
+    const int n = min(s_n, kSB);
+    for (int e = tid; e < n; e += kThreads)
+      if (!(s_bval[e] > thf)) gappend(a, s_bidx[e], s_bval[e]);
+  }
+}
+
+template __global__ void k_sweep<1>(SweepArgs a);
+template __global__ void k_sweep<2>(SweepArgs a);
+template __global__ void k_sweep<3>(SweepArgs a);
+
+}  // namespace mlt

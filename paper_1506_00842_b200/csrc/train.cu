@@ -1,0 +1,329 @@
+// train.cu — on-device fp64 ensemble training (north-star subsystem 3;
+// reference model.py:194-249 `_fit`, :308-341 `train_ensemble`).
+//
+// One CTA per ensemble member, persistent over all epochs. Lane j of every
+// warp owns hidden unit j (h <= 32); the rows of a mini-batch are split over
+// the CTA's 4 warps, each warp accumulates its rows' gradients in registers,
+// and one reduction through shared memory per step feeds the momentum update.
+// The caller supplies every random draw (initial weights, per-epoch
+// permutations) from the reference's own PCG64 stream, so the device follows
+// the reference step sequence exactly; arithmetic mirrors the reference's
+// rounding sequence (separate multiplies/subtractions where numpy does them),
+// leaving only BLAS summation-order differences (~1e-16 relative per step).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace mlt {
+
+constexpr int kTW = 4;           // warps per member CTA
+constexpr int kTMaxD = 32;
+constexpr int kRowsPerWarp = 8;  // rows of a 32-row chunk per warp
+
+struct TrainArgs {
+  int k, d, h, epochs, B;
+  double lr, mu;
+  const double* x;               // [n_rows][d]
+  const double* t;               // member-major standardized targets
+  const int* rows;               // member-major row ids into x
+  const int* n_m;                // [k]
+  const int64_t* off;            // [k] offset of member m in t/rows
+  const int64_t* poff;           // [k] offset of member m in perms
+  const int* perms;              // per member: epochs x n_m
+  const double* iw1;             // [k][h][d]
+  const double* iw2;             // [k][h]
+  double *ow1, *ob1, *ow2, *ob2, *lfirst, *llast;
+  int* div_epoch;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a) {
+  const int m = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int d = a.d, h = a.h;
+  const int n = a.n_m[m];
+  const double* T = a.t + a.off[m];
+  const int* R = a.rows + a.off[m];
+  const int* PERM = a.perms + a.poff[m];
+
+  __shared__ double W1[kTMaxD][32], V1[kTMaxD][32];
+  __shared__ double B1[32], VB1[32], W2[32], VW2[32];
+  extern __shared__ double part_raw[];   // [kTW][kTMaxD + 2][32] (dynamic: > 48 KB static limit)
+  auto part = reinterpret_cast<double(*)[kTMaxD + 2][32]>(part_raw);
+  __shared__ double pscal[kTW][2];            // per-warp (sum dout, sum r^2)
+  __shared__ double xs[kTW][kRowsPerWarp][kTMaxD];
+  __shared__ double ts[kTW][kRowsPerWarp];
+  __shared__ double s_b2, s_vb2, s_sse;
+  __shared__ int s_stop;
+
+  for (int q = tid; q < kTMaxD * 32; q += blockDim.x) {
+    const int p = q / 32, j = q % 32;
+    W1[p][j] = (p < d && j < h) ? a.iw1[((size_t)m * h + j) * d + p] : 0.0;
+    V1[p][j] = 0.0;
+  }
+  if (tid < 32) {
+    B1[tid] = 0.0;
+    VB1[tid] = 0.0;
+    W2[tid] = tid < h ? a.iw2[(size_t)m * h + tid] : 0.0;
+    VW2[tid] = 0.0;
+  }
+  if (tid == 0) {
+    s_b2 = 0.0;
+    s_vb2 = 0.0;
+    s_stop = 0;
+  }
+  __syncthreads();
+  const bool active = lane < h;
+  double first = nan(""), last = nan("");
+  int diverged = 0;
+
+  for (int e = 1; e <= a.epochs; ++e) {
+    const int* perm = PERM + (size_t)(e - 1) * n;
+    if (tid == 0) s_sse = 0.0;
+    for (int s = 0; s < n; s += a.B) {
+      const int mb = min(a.B, n - s);
+      const double c2m = 2.0 / (double)mb;
+      double gW[kTMaxD];
+#pragma unroll
+      for (int p = 0; p < kTMaxD; ++p) gW[p] = 0.0;
+      double gb1 = 0.0, gw2 = 0.0, gb2 = 0.0, sse = 0.0;
+      const double w2j = W2[lane], b1j = B1[lane], b2 = s_b2;
+      for (int c0 = 0; c0 < mb; c0 += 32) {
+        const int rbase = c0 + warp * kRowsPerWarp;
+        const int nr = max(0, min(kRowsPerWarp, mb - rbase));
+        // stage this warp's rows (features + targets)
+        for (int q = lane; q < nr * d; q += 32) {
+          const int rr = q / d, p = q - rr * d;
+          const int ex = perm[s + rbase + rr];
+          xs[warp][rr][p] = a.x[(size_t)R[ex] * d + p];
+        }
+        if (lane < nr) ts[warp][lane] = T[perm[s + rbase + lane]];
+        __syncwarp();
+        for (int rr = 0; rr < nr; ++rr) {
+          double z = 0.0;
+#pragma unroll
+          for (int p = 0; p < kTMaxD; ++p)
+            if (p < d) z = fma(xs[warp][rr][p], W1[p][lane], z);
+          z = __dadd_rn(z, b1j);
+          const double hj = 1.0 / (1.0 + exp(-z));
+          const double out = __dadd_rn(warp_sum(active ? hj * w2j : 0.0), b2);
+          const double r = __dsub_rn(out, ts[warp][rr]);
+          const double dout = __dmul_rn(c2m, r);
+          sse = fma(r, r, sse);
+          gb2 = __dadd_rn(gb2, dout);
+          if (active) {
+            gw2 = fma(hj, dout, gw2);
+            const double dz = __dmul_rn(__dmul_rn(__dmul_rn(dout, w2j), hj), __dsub_rn(1.0, hj));
+            gb1 = __dadd_rn(gb1, dz);
+#pragma unroll
+            for (int p = 0; p < kTMaxD; ++p)
+              if (p < d) gW[p] = fma(dz, xs[warp][rr][p], gW[p]);
+          }
+        }
+        __syncwarp();
+      }
+      // per-warp partials -> shared memory
+#pragma unroll
+      for (int p = 0; p < kTMaxD; ++p)
+        if (p < d) part[warp][p][lane] = gW[p];
+      part[warp][d][lane] = gb1;
+      part[warp][d + 1][lane] = gw2;
+      if (lane == 0) {
+        pscal[warp][0] = gb2;
+        pscal[warp][1] = sse;
+      }
+      __syncthreads();
+      // momentum update: v = mu*v - lr*g ; w += v   (model.py:233-240)
+      for (int q = tid; q < (d + 2) * 32; q += blockDim.x) {
+        const int p = q / 32, j = q % 32;
+        if (j >= h) continue;
+        double g = part[0][p][j];
+#pragma unroll
+        for (int w = 1; w < kTW; ++w) g = __dadd_rn(g, part[w][p][j]);
+        if (p < d) {
+          const double v = __dsub_rn(__dmul_rn(a.mu, V1[p][j]), __dmul_rn(a.lr, g));
+          V1[p][j] = v;
+          W1[p][j] = __dadd_rn(W1[p][j], v);
+        } else if (p == d) {
+          const double v = __dsub_rn(__dmul_rn(a.mu, VB1[j]), __dmul_rn(a.lr, g));
+          VB1[j] = v;
+          B1[j] = __dadd_rn(B1[j], v);
+        } else {
+          const double v = __dsub_rn(__dmul_rn(a.mu, VW2[j]), __dmul_rn(a.lr, g));
+          VW2[j] = v;
+          W2[j] = __dadd_rn(W2[j], v);
+        }
+      }
+      if (tid == 0) {
+        double g = pscal[0][0], ss = pscal[0][1];
+        for (int w = 1; w < kTW; ++w) {
+          g = __dadd_rn(g, pscal[w][0]);
+          ss = __dadd_rn(ss, pscal[w][1]);
+        }
+        const double v = __dsub_rn(__dmul_rn(a.mu, s_vb2), __dmul_rn(a.lr, g));
+        s_vb2 = v;
+        s_b2 = __dadd_rn(s_b2, v);
+        s_sse = __dadd_rn(s_sse, ss);
+      }
+      __syncthreads();
+    }
+    const double loss = s_sse / (double)n;
+    __syncthreads();   // everyone has read s_sse before thread 0 resets it
+    if (!isfinite(loss)) {
+      diverged = e;
+      break;
+    }
+    if (e == 1) first = loss;
+    last = loss;
+  }
+  // outputs
+  for (int q = tid; q < h * d; q += blockDim.x) {
+    const int j = q / d, p = q % d;
+    a.ow1[((size_t)m * h + j) * d + p] = W1[p][j];
+  }
+  for (int j = tid; j < h; j += blockDim.x) {
+    a.ob1[(size_t)m * h + j] = B1[j];
+    a.ow2[(size_t)m * h + j] = W2[j];
+  }
+  if (tid == 0) {
+    a.ob2[m] = s_b2;
+    a.lfirst[m] = first;
+    a.llast[m] = last;
+    a.div_epoch[m] = diverged;
+  }
+}
+
+}  // namespace mlt
+
+// ---------------------------------------------------------------------------
+// host entry point
+// ---------------------------------------------------------------------------
+namespace {
+thread_local char g_terr[256];
+}
+
+extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* launches, const mlt_train_desc* dd,
+                                      double* w1, double* b1, double* w2, double* b2, double* lf, double* ll,
+                                      int32_t* div, const char** err) {
+  using namespace mlt;
+  *err = g_terr;
+  g_terr[0] = 0;
+  const mlt_train_desc& D = *dd;
+  auto bad = [&](int code, const char* msg) {
+    snprintf(g_terr, sizeof g_terr, "%s", msg);
+    return code;
+  };
+  if (D.k < 1) return bad(MLT_EINVAL, "k must be >= 1");
+  if (D.d < 1 || D.d > kTMaxD) return bad(MLT_EINVAL, "training supports 1..32 inputs");
+  if (D.h < 1 || D.h > 32) return bad(MLT_EINVAL, "training supports 1..32 hidden units");
+  if (D.epochs < 1 || D.batch_size < 1) return bad(MLT_EINVAL, "epochs and batch_size must be positive");
+  std::vector<int64_t> off(D.k), poff(D.k);
+  int64_t tot = 0, ptot = 0;
+  for (int m = 0; m < D.k; ++m) {
+    if (D.n_m[m] < 1) return bad(MLT_EDATA, "a member has no training examples");
+    off[m] = tot;
+    poff[m] = ptot;
+    tot += D.n_m[m];
+    ptot += (int64_t)D.epochs * D.n_m[m];
+  }
+  cudaError_t e = cudaSetDevice(dev);
+  auto cuda_fail = [&](cudaError_t ce) {
+    snprintf(g_terr, sizeof g_terr, "CUDA error in training: %s", cudaGetErrorString(ce));
+    return MLT_ECUDA;
+  };
+  if (e != cudaSuccess) return cuda_fail(e);
+  const size_t kh = (size_t)D.k * D.h;
+  const size_t bytes_x = (size_t)D.n_rows * D.d * 8, bytes_t = tot * 8, bytes_r = tot * 4, bytes_n = D.k * 4,
+               bytes_o = D.k * 8 * 2, bytes_p = ptot * 4, bytes_w1 = kh * D.d * 8, bytes_w2 = kh * 8;
+  const size_t outb = bytes_w1 + 2 * kh * 8 + (size_t)D.k * 8 * 3 + (size_t)D.k * 4;
+  char* buf = nullptr;
+  const size_t total = bytes_x + bytes_t + bytes_r + bytes_n + bytes_o + bytes_p + bytes_w1 + bytes_w2 + outb + 1024;
+  if ((e = cudaMalloc(&buf, total)) != cudaSuccess) return cuda_fail(e);
+  size_t at = 0;
+  auto take = [&](size_t nb) {
+    char* p = buf + at;
+    at += (nb + 15) & ~(size_t)15;
+    return p;
+  };
+  double* dx = (double*)take(bytes_x);
+  double* dt = (double*)take(bytes_t);
+  int* dr = (int*)take(bytes_r);
+  int* dn = (int*)take(bytes_n);
+  int64_t* doff = (int64_t*)take(bytes_o);
+  int64_t* dpoff = doff + D.k;
+  int* dp = (int*)take(bytes_p);
+  double* diw1 = (double*)take(bytes_w1);
+  double* diw2 = (double*)take(bytes_w2);
+  double* ow1 = (double*)take(bytes_w1);
+  double* ob1 = (double*)take(kh * 8);
+  double* ow2 = (double*)take(kh * 8);
+  double* ob2 = (double*)take(D.k * 8);
+  double* olf = (double*)take(D.k * 8);
+  double* oll = (double*)take(D.k * 8);
+  int* odiv = (int*)take(D.k * 4);
+  cudaMemcpyAsync(dx, D.x, bytes_x, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dt, D.t, bytes_t, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dr, D.rows, bytes_r, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dn, D.n_m, bytes_n, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(doff, off.data(), D.k * 8, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dpoff, poff.data(), D.k * 8, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dp, D.perms, bytes_p, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(diw1, D.init_w1, bytes_w1, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(diw2, D.init_w2, bytes_w2, cudaMemcpyHostToDevice, stream);
+  TrainArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.k = D.k;
+  a.d = D.d;
+  a.h = D.h;
+  a.epochs = D.epochs;
+  a.B = D.batch_size;
+  a.lr = D.learning_rate;
+  a.mu = D.momentum;
+  a.x = dx;
+  a.t = dt;
+  a.rows = dr;
+  a.n_m = dn;
+  a.off = doff;
+  a.poff = dpoff;
+  a.perms = dp;
+  a.iw1 = diw1;
+  a.iw2 = diw2;
+  a.ow1 = ow1;
+  a.ob1 = ob1;
+  a.ow2 = ow2;
+  a.ob2 = ob2;
+  a.lfirst = olf;
+  a.llast = oll;
+  a.div_epoch = odiv;
+  const int smem = (int)(sizeof(double) * kTW * (kTMaxD + 2) * 32);
+  cudaFuncSetAttribute(k_train, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_train<<<D.k, kTW * 32, smem, stream>>>(a);
+  (*launches)++;
+  e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    cudaMemcpyAsync(w1, ow1, bytes_w1, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(b1, ob1, kh * 8, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(w2, ow2, kh * 8, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(b2, ob2, D.k * 8, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(lf, olf, D.k * 8, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(ll, oll, D.k * 8, cudaMemcpyDeviceToHost, stream);
+    cudaMemcpyAsync(div, odiv, D.k * 4, cudaMemcpyDeviceToHost, stream);
+    e = cudaStreamSynchronize(stream);
+  }
+  cudaFree(buf);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int m = 0; m < D.k; ++m)
+    if (div[m] != 0) {
+      snprintf(g_terr, sizeof g_terr, "training loss became non-finite at epoch %d (member %d)", div[m], m);
+      return MLT_EDIVERGED;
+    }
+  return MLT_OK;
+}

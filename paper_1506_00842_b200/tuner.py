@@ -1,0 +1,189 @@
+"""Two-stage auto-tuning — the API of `mltune.tuner`
+(/root/reference/pkg/src/mltune/tuner.py) with the full-space sweep on the B200.
+
+`top_m_predicted` is the drop-in for tuner.py:95-131. It never materialises
+the space: the device decodes every index, evaluates the ensemble in fp32
+with an a-priori error bound, keeps every configuration within the guard
+band of the running m-th best, rescores those in fp64 in the reference's
+operation order and sorts by (prediction, index) — the reference's
+`lexsort((indices, preds))`. The orchestration around it (`autotune`,
+`measure_configs`, `exhaustive_search`) is host logic over duck-typed runners,
+as in the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import errors
+from .measurement import STATUS_INVALID_STATIC, Outcome, Sample, SampleSet
+from .model import DEFAULT_BAG_COUNT, TrainConfig, train_ensemble
+
+SWEEP_CHUNK = 1 << 17
+REPORT_SCHEMA_VERSION = 1
+
+
+@dataclass(frozen=True)
+class TunerConfig:
+    """tuner.py:33-53."""
+    n_train: int
+    m_candidates: int
+    k_bag: int = DEFAULT_BAG_COUNT
+    seed: int = 0
+    train_cfg: TrainConfig | None = None
+    max_prediction_sweep: int | None = None
+
+    def __post_init__(self):
+        if self.m_candidates < 1:
+            raise ValueError("m_candidates must be >= 1")
+        if self.n_train < self.k_bag:
+            raise ValueError("n_train must be at least k_bag")
+        if self.max_prediction_sweep is not None and self.max_prediction_sweep < 1:
+            raise ValueError("max_prediction_sweep must be >= 1 when set")
+
+    def resolved_train_cfg(self) -> TrainConfig:
+        return self.train_cfg if self.train_cfg is not None else TrainConfig(seed=self.seed)
+
+
+@dataclass(frozen=True)
+class TuningReport:
+    """tuner.py:56-77."""
+    space_name: str
+    runner_id: str
+    config: TunerConfig
+    stage1_samples: SampleSet
+    stage2_samples: SampleSet
+    stage2_invalid_count: int
+    best_config: tuple | None = None
+    best_index: int | None = None
+    best_time: float | None = None
+    predicted_best_time: float | None = None
+
+    @property
+    def measurements_total(self) -> int:
+        return len(self.stage1_samples) + len(self.stage2_samples)
+
+
+def top_m_arrays(ensemble, space, m: int, begin: int = 0, end: int | None = None, indices=None,
+                 device=None, with_stats: bool = False):
+    """Device top-m over the slice [begin, end) of `space` (or over an index
+    list) -> (indices int64, predictions float64[, stats dict])."""
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    ps = N.packed(space, "space")
+    pe = N.packed(ensemble, "ensemble")
+    card = ps.card
+    end = card if end is None else int(end)
+    out_idx = np.empty(m, dtype=np.int64)
+    out_pred = np.empty(m, dtype=np.float64)
+    out_n = N.C.c_int64(0)
+    st = N.MltSweepStats()
+    if indices is not None:
+        lst = np.ascontiguousarray(indices, dtype=np.int64)
+        lp, ln = N.ptr(lst, N.C.c_int64), lst.shape[0]
+    else:
+        lp, ln = None, 0
+    rc = N.lib().mlt_top_m(N.ctx(device), N.C.byref(ps.c), N.C.byref(pe.c), int(m), int(begin), end, lp, ln,
+                           N.ptr(out_idx, N.C.c_int64), N.ptr(out_pred, N.C.c_double), N.C.byref(out_n),
+                           N.C.byref(st))
+    N.check(rc, "mlt_top_m")
+    n = out_n.value
+    res = (out_idx[:n].copy(), out_pred[:n].copy())
+    return res + (st.as_dict(),) if with_stats else res
+
+
+def top_m_predicted(ensemble, space, m: int, sweep_cap: int | None = None, seed: int = 0) -> list:
+    """The m statically-valid configurations with the lowest predicted times,
+    ascending, ties broken by index; fewer when fewer are valid (tuner.py:95-131)."""
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    card = space.cardinality()
+    if sweep_cap is not None and card > sweep_cap:
+        subset = np.sort(space.sample_indices(sweep_cap, seed))   # host RNG: the reference stream
+        idx, pred = top_m_arrays(ensemble, space, m, indices=subset)
+    else:
+        idx, pred = top_m_arrays(ensemble, space, m)
+    return [(space.config_at(int(i)), float(p)) for i, p in zip(idx, pred)]
+
+
+def measure_configs(space, runner, configs, repetitions: int | None = None) -> list:
+    """Static invalids never reach the runner (tuner.py:80-92)."""
+    out = []
+    for config in configs:
+        if space.is_statically_valid(config):
+            out.append(runner.measure(config, repetitions))
+        else:
+            reps = repetitions if repetitions is not None else getattr(runner, "default_repetitions", 1)
+            out.append(Sample(config, Outcome.invalid(STATUS_INVALID_STATIC), reps))
+    return out
+
+
+def autotune(space, runner, cfg: TunerConfig, jobs: int = 1, sweep=None) -> TuningReport:
+    """Sample -> measure -> train (device) -> sweep + top-M (device) -> re-measure
+    -> best of stage 2 by (time, index) (tuner.py:134-188). `sweep` may replace
+    the top-M function (e.g. the multi-GPU `distributed.top_m_predicted`)."""
+    if space.cardinality() < cfg.n_train:
+        raise ValueError(f"n_train={cfg.n_train} exceeds space cardinality {space.cardinality()}")
+    rid = getattr(runner, "runner_id", "runner")
+    stage1 = SampleSet(space, rid, tuple(measure_configs(space, runner, space.sample_random(cfg.n_train, cfg.seed))))
+    n_valid = len(stage1.valid_samples())
+    if n_valid < cfg.k_bag:
+        raise errors.active["InsufficientDataError"](
+            f"stage 1 produced {n_valid} valid samples, need at least {cfg.k_bag}")
+    ens = train_ensemble(stage1, space, k=cfg.k_bag, cfg=cfg.resolved_train_cfg(), jobs=jobs)
+    sweep = sweep or top_m_predicted
+    cands = sweep(ens, space, cfg.m_candidates, cfg.max_prediction_sweep, cfg.seed)
+    predicted = {space.index_of(c): p for c, p in cands}
+    stage2 = SampleSet(space, rid, tuple(measure_configs(space, runner, [c for c, _ in cands])))
+    best, invalid = None, 0
+    for s in stage2.samples:
+        if not s.outcome.is_valid:
+            invalid += 1
+            continue
+        key = (s.outcome.time, space.index_of(s.config))
+        if best is None or key < best:
+            best = key
+    if best is None:
+        partial = TuningReport(space.name, rid, cfg, stage1, stage2, invalid)
+        raise errors.active["AllCandidatesInvalidError"](
+            f"all {len(stage2)} second-stage candidates were invalid", report=partial)
+    t, i = best
+    return TuningReport(space.name, rid, cfg, stage1, stage2, invalid, best_config=space.config_at(i),
+                        best_index=i, best_time=t, predicted_best_time=predicted[i])
+
+
+def exhaustive_search(space, runner):
+    """Measure every statically valid configuration once; return the fastest
+    (tuner.py:191-224). Vectorised through `runner.measured_times` when present."""
+    card = space.cardinality()
+    best = None
+    if hasattr(runner, "measured_times"):
+        reps = getattr(runner, "default_repetitions", 1)
+        for s in range(0, card, SWEEP_CHUNK):
+            idx = np.arange(s, min(s + SWEEP_CHUNK, card), dtype=np.int64)
+            if getattr(space, "rules", ()):
+                idx = idx[space.valid_mask_indices(idx)] if hasattr(space, "valid_mask_indices") else \
+                    idx[space.static_valid_mask(space.decode_indices(idx))]
+            if idx.size == 0:
+                continue
+            times, ok = runner.measured_times(idx, reps)
+            if not ok.any():
+                continue
+            pos = int(np.nanargmin(np.where(ok, times, np.nan)))
+            key = (float(times[pos]), int(idx[pos]))
+            if best is None or key < best:
+                best = key
+    else:
+        for i in range(card):
+            c = space.config_at(i)
+            if not space.is_statically_valid(c):
+                continue
+            smp = runner.measure(c)
+            if smp.outcome.is_valid and (best is None or (smp.outcome.time, i) < best):
+                best = (smp.outcome.time, i)
+    if best is None:
+        raise errors.active["EmptySpaceError"](f"space {space.name!r} has no valid configuration")
+    return space.config_at(best[1]), best[0]

@@ -1,0 +1,377 @@
+"""Parity of the sm_100a path (through the C ABI) against the reference's own
+outputs (golden fixtures written by tests/golden/make_golden.py from the real
+`mltune`) and against the oracle on seeded inputs.
+
+Bars (BASELINE.json north star): top-M index sets bit-exact; predictions
+within 1e-12 relative of the reference fp64 (the spec allows 1e-4 on log time;
+we hold the fp64 paths to summation-order noise); decode/mask/encode
+bit-exact; trained weights within 1e-8 relative of the reference trainer.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import (CASE_SPACE, golden, oracle_ensemble, oracle_space, product_ensemble, product_space,
+                      surrogates_doc)
+
+pytestmark = pytest.mark.gpu
+
+PRED_RTOL = 1e-12
+
+
+def _lib():
+    from paper_1506_00842_b200 import _native as N
+    return N
+
+
+@pytest.fixture(autouse=True)
+def _defaults(gpu_ok):
+    N = _lib()
+    c = N.ctx(0)
+    yield
+    for key in (N.MLT_OPT_PATH, N.MLT_OPT_GROUP, N.MLT_OPT_CAND_CAP):
+        N.lib().mlt_ctx_set_option(c, key, -1)
+
+
+def set_opt(key, value):
+    N = _lib()
+    N.check(N.lib().mlt_ctx_set_option(N.ctx(0), key, value))
+
+
+# ---- A1-A3: decode / mask / encode -------------------------------------------
+
+@pytest.mark.parametrize("name", ["convolution", "raycasting", "stereo", "synthetic-1e8", "conv-rules",
+                                  "bench512", "tiny"])
+def test_decode_mask_encode_match_reference(name):
+    from paper_1506_00842_b200.model import Encoder
+    g = golden(f"probe_{name}.npz")
+    sp = product_space(name)
+    assert np.array_equal(sp.decode_indices(g["idx"]), g["values"])
+    assert np.array_equal(sp.valid_mask_indices(g["idx"]), g["mask"])
+    assert np.array_equal(sp.static_valid_mask(g["values"]), g["mask"])
+    feat = Encoder.from_space(sp).encode_indices(g["idx"])
+    assert np.array_equal(feat, g["feat"])          # IEEE division: bit-exact
+
+
+# ---- A4-A6: fp64 prediction ----------------------------------------------------
+
+@pytest.mark.parametrize("case", list(CASE_SPACE))
+def test_predict_indices_match_reference(case):
+    g = golden(f"pred_{case}.npz")
+    ens = product_ensemble(case)
+    pred = ens.predict_indices(g["idx"])
+    np.testing.assert_allclose(pred, g["pred"], rtol=PRED_RTOL, atol=0)
+
+
+def test_predict_features_and_member_outputs():
+    ens = product_ensemble("conv_k11")
+    oens = oracle_ensemble("conv_k11")
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-0.5, 1.5, (5000, 9))
+    np.testing.assert_allclose(ens.predict_features(X), oens.predict_features(X), rtol=PRED_RTOL)
+    from oracle.model import net_out
+    for m, om in zip(ens.members[:3], oens.nets[:3]):
+        np.testing.assert_allclose(m.forward_batch(X), net_out(om, X), rtol=1e-12, atol=1e-13)
+
+
+def test_forward_closed_forms():
+    from paper_1506_00842_b200.model import Network, forward
+    assert forward(Network(np.zeros((30, 4)), np.zeros(30), np.zeros(30), 0.0), np.zeros(4)) == 0.0
+    assert forward(Network(np.zeros((30, 4)), np.zeros(30), np.ones(30), 0.0), np.ones(4)) == pytest.approx(15.0)
+    rng = np.random.default_rng(5)
+    W1, b1, w2, b2, x = rng.normal(size=(6, 3)), rng.normal(size=6), rng.normal(size=6), float(rng.normal()), \
+        rng.normal(size=3)
+    by_hand = b2 + sum(w2[j] / (1 + math.exp(-(W1[j] @ x + b1[j]))) for j in range(6))
+    assert abs(forward(Network(W1, b1, w2, b2), x) - by_hand) <= 1e-12
+
+
+# ---- A7: full-space top-M ------------------------------------------------------
+
+TOPM_CASES = [("conv_k1", 10), ("conv_k1", 200), ("conv_k11", 1), ("conv_k11", 10), ("conv_k11", 200),
+              ("conv_k11", 1000), ("raycast_k11", 10), ("raycast_k11", 200), ("stereo_k8", 10),
+              ("stereo_k8", 200), ("b512_k3", 1), ("b512_k3", 7), ("b512_k3", 512), ("b512_k3", 600)]
+
+
+@pytest.mark.parametrize("case,m", TOPM_CASES)
+@pytest.mark.parametrize("path", ["auto", "band", "full"])
+def test_top_m_matches_reference(case, m, path):
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    if path == "band":
+        set_opt(N.MLT_OPT_PATH, 0)
+    elif path == "full":
+        set_opt(N.MLT_OPT_PATH, 1)
+    g = golden(f"topm_{case}.npz")
+    idx, pred, st = top_m_arrays(product_ensemble(case), product_space(CASE_SPACE[case]), m, with_stats=True)
+    assert np.array_equal(idx, g[f"m{m}_i"]), (st, idx[:10], g[f"m{m}_i"][:10])
+    np.testing.assert_allclose(pred, g[f"m{m}_p"], rtol=PRED_RTOL)
+    if path == "band" and m <= 1024:
+        assert st["path"] == 0
+
+
+def test_top_m_synthetic_full_space_1e8():
+    """The north-star space: 100,663,296 configurations, k=16, m=200, against the
+    reference's own 11.6-minute CPU sweep (tests/golden/topm_synth_k16.npz)."""
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    g = golden("topm_synth_k16.npz")
+    if "m200_i" not in g:
+        pytest.skip("golden full-space sweep not generated (make_golden.py --synth)")
+    idx, pred, st = top_m_arrays(product_ensemble("synth_k16"), product_space("synthetic-1e8"), 200,
+                                 with_stats=True)
+    assert st["path"] == 0
+    assert np.array_equal(idx, g["m200_i"])
+    np.testing.assert_allclose(pred, g["m200_p"], rtol=PRED_RTOL)
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 1 << 21), (98566144, 100663296), (37000000, 37000000 + (1 << 21))])
+def test_top_m_synthetic_slices(lo, hi):
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    g = golden("topm_synth_k16.npz")
+    idx, pred = top_m_arrays(product_ensemble("synth_k16"), product_space("synthetic-1e8"), 200, begin=lo, end=hi)
+    assert np.array_equal(idx, g[f"slice_{lo}_{hi}_i"])
+    np.testing.assert_allclose(pred, g[f"slice_{lo}_{hi}_p"], rtol=PRED_RTOL)
+
+
+@pytest.mark.parametrize("case", ["conv_k11", "raycast_k11", "stereo_k8"])
+def test_sweep_cap_subset(case):
+    import paper_1506_00842_b200 as b
+    g = golden(f"topm_{case}.npz")
+    sp = product_space(CASE_SPACE[case])
+    res = b.top_m_predicted(product_ensemble(case), sp, 10, sweep_cap=50_000, seed=3)
+    assert [sp.index_of(c) for c, _ in res] == g["cap_i"].tolist()
+    np.testing.assert_allclose([p for _, p in res], g["cap_p"], rtol=PRED_RTOL)
+
+
+@pytest.mark.parametrize("m", [10, 200])
+def test_top_m_with_every_rule_kind(m):
+    """conv-rules: max-product, max-weighted-sum with a negative coefficient,
+    forbidden-combination, and an int64-wrapping product (paramspace.py:92-107)."""
+    from paper_1506_00842_b200.model import model_from_json
+    from conftest import model_doc
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    doc = dict(model_doc("conv_k11"))
+    doc["space_name"] = "conv-rules"
+    g = golden("topm_conv-rules_k11.npz")
+    for path in (0, 1):
+        set_opt(_lib().MLT_OPT_PATH, path)
+        idx, pred = top_m_arrays(model_from_json(doc), product_space("conv-rules"), m)
+        assert np.array_equal(idx, g[f"m{m}_i"])
+        np.testing.assert_allclose(pred, g[f"m{m}_p"], rtol=PRED_RTOL)
+
+
+@pytest.mark.parametrize("group", [1, 2, 3])
+def test_every_reciprocal_grouping_is_exact(group):
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    set_opt(_lib().MLT_OPT_GROUP, group)
+    g = golden("topm_stereo_k8.npz")
+    idx, pred, st = top_m_arrays(product_ensemble("stereo_k8"), product_space("stereo"), 200, with_stats=True)
+    assert st["group"] == group and st["path"] == 0
+    assert np.array_equal(idx, g["m200_i"])
+
+
+def test_constant_ensemble_ties_break_by_index():
+    """all predictions equal -> the m lowest valid indices."""
+    from paper_1506_00842_b200.model import Encoder, Ensemble, Network
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    sp = product_space("convolution")
+    net = Network(np.zeros((30, 9)), np.zeros(30), np.zeros(30), math.log(2.0))
+    ens = Ensemble([net, net], Encoder.from_space(sp), sp.name)
+    for path in (-1, 0, 1):
+        set_opt(_lib().MLT_OPT_PATH, path)
+        idx, pred = top_m_arrays(ens, sp, 5)
+        assert idx.tolist() == [0, 1, 2, 3, 4]
+        np.testing.assert_allclose(pred, 2.0, rtol=1e-15)
+
+
+def test_crowded_band_overflow_falls_back_exactly():
+    """A 16-entry candidate buffer forces the exact materialising fallback."""
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    set_opt(_lib().MLT_OPT_CAND_CAP, 16)
+    g = golden("topm_conv_k11.npz")
+    idx, _, st = top_m_arrays(product_ensemble("conv_k11"), product_space("convolution"), 200, with_stats=True)
+    assert st["path"] == 1
+    assert np.array_equal(idx, g["m200_i"])
+
+
+def test_fewer_valid_than_m_and_bad_m():
+    from paper_1506_00842_b200.space import ParamDef, ParamSpace, ValidityRule
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    import paper_1506_00842_b200 as b
+    sp = ParamSpace("few", (ParamDef("a", (1, 2, 4)), ParamDef("b", (0, 1)), ParamDef("c", (10, 20, 30, 40))),
+                    (ValidityRule("max-product", ("a", "c"), bound=40),))
+    ens = b.Ensemble([b.Network(np.random.default_rng(1).normal(size=(30, 3)), np.zeros(30),
+                                np.random.default_rng(2).normal(size=30), 0.1)], b.Encoder.from_space(sp), "few")
+    osp, oens = _oracle_from(sp, ens)
+    from oracle.tuner import top_m as otop
+    for m in (1, 5, 24, 100):
+        idx, pred = top_m_arrays(ens, sp, m)
+        oi, op = otop(oens, osp, m)
+        assert np.array_equal(idx, oi)
+        np.testing.assert_allclose(pred, op, rtol=PRED_RTOL)
+    with pytest.raises(ValueError):
+        b.top_m_predicted(ens, sp, 0)
+    assert len(b.top_m_predicted(ens, sp, 100)) == int(oi.size)
+
+
+def _oracle_from(sp, ens):
+    from oracle.model import ONet, OEnsemble
+    from oracle.space import space_from_doc
+    from paper_1506_00842_b200.space import space_to_json
+    osp = space_from_doc(space_to_json(sp))
+    nets = [ONet(m.weights_hidden, m.biases_hidden, m.weights_out, m.bias_out, m.target_mean, m.target_std)
+            for m in ens.members]
+    return osp, OEnsemble(nets, [len(v) for _, v in ens.encoder.params])
+
+
+def test_random_ensembles_against_oracle():
+    """Seeded random ensembles (random-init weights, several widths) on a
+    reduced space: band and full paths both equal the oracle's lexsort."""
+    import paper_1506_00842_b200 as b
+    from oracle.tuner import top_m as otop
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    sp = product_space("stereo")
+    rng = np.random.default_rng(11)
+    for trial in range(3):
+        k = int(rng.integers(1, 6))
+        scale = [0.5, 3.0, 8.0][trial]
+        nets = [b.Network(rng.normal(size=(30, 11)) * scale, rng.normal(size=30) * scale,
+                          rng.normal(size=30), float(rng.normal()), float(rng.normal()), float(rng.uniform(0.2, 2)))
+                for _ in range(k)]
+        ens = b.Ensemble(nets, b.Encoder.from_space(sp), sp.name)
+        osp, oens = _oracle_from(sp, ens)
+        oi, op = otop(oens, osp, 50, begin=0, end=1 << 20)
+        for path in (0, 1):
+            set_opt(_lib().MLT_OPT_PATH, path)
+            idx, pred = top_m_arrays(ens, sp, 50, begin=0, end=1 << 20)
+            assert np.array_equal(idx, oi), (trial, path)
+            np.testing.assert_allclose(pred, op, rtol=PRED_RTOL)
+
+
+def test_shard_merge_equals_single_sweep():
+    """The multi-GPU decomposition on one device: per-slice top-m then the
+    device merge equals the whole-space sweep."""
+    import torch
+    from paper_1506_00842_b200.distributed import _device_merge, shard_bounds
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    ens, sp = product_ensemble("stereo_k8"), product_space("stereo")
+    full_i, full_p = top_m_arrays(ens, sp, 200)
+    parts_i, parts_p = [], []
+    for r in range(8):
+        lo, hi = shard_bounds(sp.cardinality(), r, 8)
+        i, p = top_m_arrays(ens, sp, 200, begin=lo, end=hi)
+        parts_i.append(np.pad(i, (0, 200 - len(i)), constant_values=-1))
+        parts_p.append(np.pad(p, (0, 200 - len(p)), constant_values=np.inf))
+    gi = torch.from_numpy(np.concatenate(parts_i)).cuda()
+    gp = torch.from_numpy(np.concatenate(parts_p)).cuda()
+    mi, mp = _device_merge(gi, gp, 200)
+    assert np.array_equal(mi, full_i)
+    np.testing.assert_array_equal(mp, full_p)
+
+
+# ---- A9-A10: device training ---------------------------------------------------
+
+def _small_case(tag):
+    import paper_1506_00842_b200 as b
+    g = golden("train_small.npz")
+    sp = product_space("bench512")
+    cfgv = g[f"{tag}_cfg"]
+    cfg = b.TrainConfig(epochs=int(cfgv[0]), learning_rate=float(cfgv[1]), batch_size=int(cfgv[2]),
+                        momentum=float(cfgv[3]), weight_init_scale=float(cfgv[4]), seed=int(cfgv[5]))
+    samples = b.SampleSet(sp, "r", tuple(b.Sample(sp.config_at(int(i)), b.Outcome.valid(float(t)))
+                                         for i, t in zip(g[f"{tag}_idx"], g[f"{tag}_time"])))
+    return g, sp, cfg, int(cfgv[6]), samples
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c", "d"])
+def test_training_matches_reference_trainer(tag):
+    import paper_1506_00842_b200 as b
+    g, sp, cfg, k, samples = _small_case(tag)
+    ens = b.train_ensemble(samples, sp, k=k, cfg=cfg)
+    for i, mem in enumerate(ens.members):
+        np.testing.assert_allclose(mem.weights_hidden, g[f"{tag}_{i}_W1"], rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(mem.biases_hidden, g[f"{tag}_{i}_b1"], rtol=1e-8, atol=1e-10)
+        np.testing.assert_allclose(mem.weights_out, g[f"{tag}_{i}_w2"], rtol=1e-8, atol=1e-10)
+        misc = g[f"{tag}_{i}_misc"]
+        assert mem.bias_out == pytest.approx(misc[0], rel=1e-8, abs=1e-10)
+        assert (mem.target_mean, mem.target_std) == (misc[1], misc[2])     # host standardisation: exact
+        assert mem.first_epoch_loss == pytest.approx(misc[3], rel=1e-9)
+        assert mem.final_epoch_loss == pytest.approx(misc[4], rel=1e-8)
+
+
+@pytest.mark.parametrize("case", ["conv_k1", "conv_k11", "stereo_k8"])
+def test_full_training_matches_reference_predictions(case):
+    """2000 gpu-a surrogate samples, 500 epochs: the device-trained ensemble
+    predicts like the reference-trained one (survey measured 4.9e-15 for an
+    fp64 trainer with a different summation order)."""
+    import paper_1506_00842_b200 as b
+    sname = CASE_SPACE[case]
+    st = golden(f"stage1_{sname}.npz")
+    sp = product_space(sname)
+    samples = b.SampleSet(sp, "golden", tuple(
+        b.Sample(sp.config_at(int(i)), b.Outcome.valid(float(t)) if ok else b.Outcome.invalid("invalid-launch"))
+        for i, ok, t in zip(st["idx"], st["ok"], st["time"])))
+    k = product_ensemble(case).k
+    ens = b.train_ensemble(samples, sp, k=k, cfg=b.TrainConfig(seed=0))
+    gp = golden(f"pred_{case}.npz")
+    np.testing.assert_allclose(ens.predict_indices(gp["idx"]), gp["pred"], rtol=1e-9)
+    np.testing.assert_allclose([m.final_epoch_loss for m in ens.members], gp["final_loss"], rtol=1e-7)
+    gt = golden(f"topm_{case}.npz")
+    idx, _ = b.top_m_arrays(ens, sp, 10)
+    assert np.array_equal(idx, gt["m10_i"])
+
+
+def test_divergence_reports_epoch():
+    import paper_1506_00842_b200 as b
+    g = golden("train_small.npz")
+    sp = product_space("bench512")
+    samples = b.SampleSet(sp, "r", tuple(b.Sample(sp.config_at(int(i)), b.Outcome.valid(float(t)))
+                                         for i, t in zip(g["div_idx"], g["div_time"])))
+    with pytest.raises(b.DivergenceError) as err:
+        b.train_network(samples, sp, b.TrainConfig(seed=1, learning_rate=1e9, momentum=0.0))
+    assert err.value.epoch == int(g["div_epoch"])
+
+
+def test_insufficient_data():
+    import paper_1506_00842_b200 as b
+    sp = product_space("tiny")
+    samples = b.SampleSet(sp, "r", (b.Sample(sp.config_at(0), b.Outcome.invalid("invalid-launch")),))
+    with pytest.raises(b.InsufficientDataError):
+        b.train_ensemble(samples, sp, k=1)
+    two = b.SampleSet(sp, "r", tuple(b.Sample(sp.config_at(i), b.Outcome.valid(1.0 + i)) for i in range(3)))
+    with pytest.raises(b.InsufficientDataError):
+        b.train_ensemble(two, sp, k=11)
+
+
+def test_autotune_end_to_end_on_surrogate():
+    """sample -> measure (oracle surrogate as the device under test) -> device
+    train -> device sweep -> re-measure: finds the exhaustive optimum of the
+    gpu-a convolution surrogate (index 88599)."""
+    import paper_1506_00842_b200 as b
+    from oracle.surrogate import OSurrogate
+
+    class Runner:
+        runner_id = "surrogate"
+        default_repetitions = 1
+
+        def __init__(self, sp):
+            self.sp = sp
+            self.s = OSurrogate(surrogates_doc()["convolution"], oracle_space("convolution"))
+
+        def measure(self, config, repetitions=None):
+            t, ok = self.s.measured_times(np.array([self.sp.index_of(config)]), repetitions or 1)
+            return b.Sample(config, b.Outcome.valid(float(t[0])) if ok[0] else b.Outcome.invalid("invalid-launch"),
+                            repetitions or 1)
+
+        def measured_times(self, idx, reps=1):
+            return self.s.measured_times(idx, reps)
+
+    sp = product_space("convolution")
+    runner = Runner(sp)
+    rep = b.autotune(sp, runner, b.TunerConfig(n_train=2000, m_candidates=200, k_bag=11, seed=0))
+    best_cfg, best_t = b.exhaustive_search(sp, runner)
+    assert rep.best_time <= best_t * 1.10
+    assert rep.measurements_total == 2200
