@@ -68,7 +68,7 @@ namespace {
 
 enum Slot {
   S_SPACE_VALUES, S_SPACE_RPOS, S_SPACE_RCOEFF, S_ENS, S_IDX, S_OUT_A, S_OUT_B, S_OUT_C, S_OUT_D,
-  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT
+  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT, S_TOPI, S_TOPP
 };
 
 int ws(mlt_ctx* c, int slot, size_t bytes, void** out) {
@@ -339,7 +339,7 @@ struct mlt_plan {
   bool band_ok = false;
   std::string band_why;
   int split = 0, G = 3, dummies = 0;
-  int64_t c_in = 1, c_in_pad = kThreads;
+  int64_t c_in = 1, c_in_pad = kInnerBlock;
   double delta = 0, cst = 0;
 };
 
@@ -364,7 +364,7 @@ int plan_setup_band(mlt_plan* p) {
     for (int sp = s.P - 1; sp >= 0; --sp) {
       cin *= s.radix[sp];
       if (cin > 16384) break;
-      const int64_t pad = (cin + kThreads - 1) / kThreads * kThreads;
+      const int64_t pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
       if ((double)cin / pad >= 0.75) {
         best = sp;
         best_cin = cin;
@@ -379,7 +379,7 @@ int plan_setup_band(mlt_plan* p) {
   }
   p->split = best;
   p->c_in = best_cin;
-  p->c_in_pad = (best_cin + kThreads - 1) / kThreads * kThreads;
+  p->c_in_pad = (best_cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
 
   const int KH = e.k * kH;
   std::vector<double> cshift(KH, 0.0), wprime(KH, 0.0);
@@ -452,15 +452,26 @@ int plan_setup_band(mlt_plan* p) {
   for (int m = 0; m < e.k; ++m) cst += (e.b2()[m] * e.sd()[m] + e.mean()[m]) / e.k;
   cst -= dummies;
   p->cst = cst;
-  const double ngroups = (double)KH / G;
   const double uu = std::ldexp(1.0, -24);
-  // a-priori |fp32 - exact| bound on the mean log: group
-  // arithmetic <= 30u per unit magnitude, accumulation <= ngroups*u*S, final adds.
-  p->delta = 2.0 * uu * ((32.0 + ngroups) * S + 2.0 * std::fabs(cst) + 2.0) + 1e-12 * (1.0 + std::fabs(cst));
+  // A-priori |fp32 - exact| bound on the mean log:
+  //  * each unit term 1/d' = w' sigma carries <= 4u relative error from the
+  //    rounded tables and the FMA; the G-unit rational combination and the
+  //    approximate reciprocal add <= cg*u relative to the group's sum of |terms|;
+  //  * the running accumulator is rounded once per group, each time by at most
+  //    u * |partial sum| <= u * (prefix sum of |w'| up to that group);
+  //  * + cst (rounded) and the final add.
+  const double cg = G == 3 ? 30.0 : (G == 2 ? 16.0 : 8.0);
+  double prefix = 0.0, acc_bound = 0.0;
+  for (int q = 0; q < KH; q += G) {
+    for (int x = 0; x < G; ++x) prefix += wprime[q + x] != 0.0 ? std::fabs(wprime[q + x]) : 1.0;
+    acc_bound += prefix;
+  }
+  p->delta = 1.5 * uu * (cg * S + acc_bound + S + 3.0 * std::fabs(cst)) + 1e-12 * (1.0 + std::fabs(cst));
 
-  std::vector<double> tab(2 * (size_t)KH);
+  std::vector<double> tab(3 * (size_t)KH, 0.0);
   std::copy(cshift.begin(), cshift.end(), tab.begin());
   std::copy(wprime.begin(), wprime.end(), tab.begin() + KH);
+  for (int q = 0; q < KH; ++q) tab[2 * (size_t)KH + q] = wprime[q] != 0.0 ? 1.0 / wprime[q] : 0.0;
   mlt_ctx* c = p->ctx;
   CU(cudaMalloc(&p->d_tab, tab.size() * 8));
   CU(cudaMalloc(&p->d_u, (size_t)KH * 4));
@@ -839,13 +850,13 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     const int64_t o_lo = begin / p->c_in;
     const int64_t o_hi = (end - 1) / p->c_in + 1;
     const int n_ob = (int)((o_hi - o_lo + kOB - 1) / kOB);
-    const int n_ib = (int)(p->c_in_pad / kThreads);
+    const int n_ib = (int)(p->c_in_pad / kInnerBlock);
     float *ea, *ebp, *cval;
     int64_t* cidx;
     uint32_t* gs;
     TRY(ws_t(c, S_EA, (size_t)n_ob * KH * kOB, &ea));
     TRY(ws_t(c, S_EBP, (size_t)KH * p->c_in_pad, &ebp));
-    TRY(ws_t(c, S_GSCAL, 4, &gs));
+    TRY(ws_t(c, S_GSCAL, 8, &gs));
     TRY(ws_t(c, S_CIDX, (size_t)c->cand_cap, &cidx));
     TRY(ws_t(c, S_CVAL, (size_t)c->cand_cap, &cval));
     TableArgs ta;
@@ -859,6 +870,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.b1 = p->de.b1;
     ta.cshift = p->d_tab;
     ta.wprime = p->d_tab + KH;
+    ta.winv = p->d_tab + 2 * KH;
     ta.o_lo = o_lo;
     ta.c_in = p->c_in;
     ta.c_in_pad = p->c_in_pad;
@@ -869,9 +881,9 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     hs[0] = 0xFF800000u;   // fkey(+inf)
     hs[1] = 0u;
     CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
-    k_table_outer<<<grid_for(c, (int64_t)n_ob * KH * kOB, 256), 256, 0, c->stream>>>(ta);
+    k_table_outer<<<grid_for(c, (int64_t)n_ob * p->he.k * kOB, 128), 128, 0, c->stream>>>(ta);
     TRY(check_launch(c));
-    k_table_inner<<<grid_for(c, (int64_t)KH * p->c_in_pad, 256), 256, 0, c->stream>>>(ta);
+    k_table_inner<<<grid_for(c, (int64_t)p->he.k * p->c_in_pad, 128), 128, 0, c->stream>>>(ta);
     TRY(check_launch(c));
 
     SweepArgs sa;
@@ -923,17 +935,45 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       uint32_t b = (theta_key & 0x80000000u) ? (theta_key & 0x7fffffffu) : ~theta_key;
       float theta;
       std::memcpy(&theta, &b, 4);
-      double *pa, *pb;
-      int64_t *ia, *ib;
-      TRY(ws_t(c, S_OUT_A, std::max<uint32_t>(count, 1), &pa));
-      TRY(ws_t(c, S_OUT_B, std::max<uint32_t>(count, 1), &pb));
-      TRY(ws_t(c, S_OUT_C, std::max<uint32_t>(count, 1), &ia));
-      TRY(ws_t(c, S_OUT_D, std::max<uint32_t>(count, 1), &ib));
-      TRY(launch_predict64(c, p->de, p->ds, 0, 0, cidx, nullptr, count, pa, ia, cval, theta));
-      double* pcur = pa;
-      int64_t* icur = ia;
-      TRY(sort_pairs(c, &pcur, &icur, pb, ib, count, true));
-      TRY(emit_top(c, pcur, icur, count, m, out_idx, out_pred, out_n));
+      (void)theta;
+      const uint32_t cnt1 = std::max<uint32_t>(count, 1);
+      double *pa, *pb, *tp;
+      int64_t *ia, *ib, *ti;
+      float* fv;
+      TRY(ws_t(c, S_OUT_A, cnt1, &pa));
+      TRY(ws_t(c, S_OUT_B, cnt1, &pb));
+      TRY(ws_t(c, S_OUT_C, cnt1, &ia));
+      TRY(ws_t(c, S_OUT_D, cnt1, &ib));
+      TRY(ws_t(c, S_FEAT, cnt1, &fv));
+      TRY(ws_t(c, S_TOPI, (size_t)m, &ti));
+      TRY(ws_t(c, S_TOPP, (size_t)m, &tp));
+      // 1) exact global tau_m over the candidates, keep f32 <= tau_m + 2*delta
+      k_band_filter<<<1, 1024, 0, c->stream>>>(cidx, cval, count, (int)m, sa.band, ia, fv, gs + 2);
+      TRY(check_launch(c));
+      // 2) fp64 rescoring of the survivors, one warp each
+      const size_t smem64 = predict64_smem(p->de);
+      if (smem64 > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem64);
+      CU(cudaFuncSetAttribute(k_rescore_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
+      const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)count + 7) / 8, (int64_t)c->sms * 4));
+      k_rescore_warp<<<rgrid, 256, smem64, c->stream>>>(p->de, ia, gs + 2, pa);
+      TRY(check_launch(c));
+      // 3) sort by (prediction, index) in one CTA when small
+      const int ssmem = 16 * kSmallSort;
+      CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+      k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3);
+      TRY(check_launch(c));
+      CU(cudaMemcpyAsync(hs, gs, 32, cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      const uint32_t n2 = hs[2], big = hs[3], take = hs[4];
+      local.candidates = n2;
+      if (!big) {
+        TRY(emit_top(c, tp, ti, take, m, out_idx, out_pred, out_n));
+      } else {
+        double* pcur = pa;
+        int64_t* icur = ia;
+        TRY(sort_pairs(c, &pcur, &icur, pb, ib, n2, true));
+        TRY(emit_top(c, pcur, icur, n2, m, out_idx, out_pred, out_n));
+      }
     }
     if (c->prof) {
       float ms = 0;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "select.cuh"
 
 namespace mlt {
 
@@ -15,10 +16,20 @@ __global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, co
                             const float* band_v, float band_theta);
 __global__ void k_member_out64(DEns e, const double* feat, int64_t n, double* out);
 size_t predict64_smem(const DEns& e);
+__global__ void k_rescore_warp(DEns e, const int64_t* idx, const uint32_t* n_ptr, double* pred);
+
+// ---- final guard-band stage (select.cu) ------------------------------------
+constexpr int kSmallSort = 4096;  // survivors sorted in one CTA's shared memory
+__global__ void k_band_filter(const int64_t* cidx, const float* cval, uint32_t count, int m, float band,
+                              int64_t* out_idx, float* out_val, uint32_t* out_n);
+__global__ void k_sort_small(const double* pred, const int64_t* idx, const uint32_t* n_ptr, int m, double* out_pred,
+                             int64_t* out_idx, uint32_t* status);
 
 // ---- fp32 factored sweep (sweep.cu) ---------------------------------------
-constexpr int kThreads = 128;   // inner configurations per work item (one per thread)
-constexpr int kOB = 32;         // outer configurations per work item (per thread)
+constexpr int kThreads = 256;   // threads per sweep CTA
+constexpr int kInner = 2;       // inner configurations per thread (share every exp(-A') load)
+constexpr int kInnerBlock = kThreads * kInner;   // inner configurations per work item
+constexpr int kOB = 16;         // outer configurations per work item (per thread)
 constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
 constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
 constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
@@ -52,6 +63,7 @@ struct TableArgs {
   const double* b1;             // [k][h]
   const double* cshift;         // [k*kH] centring constant c
   const double* wprime;         // [k*kH] w2*std/k (0 for dummy units)
+  const double* winv;           // [k*kH] 1/w' (0 for dummy units)
   int64_t o_lo, c_in, c_in_pad;
   int n_ob;
   float* ea;

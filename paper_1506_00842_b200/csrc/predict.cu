@@ -157,3 +157,61 @@ size_t predict64_smem(const DEns& e) {
 }
 
 }  // namespace mlt
+
+namespace mlt {
+
+// Guard-band rescoring: one warp per candidate; lane j evaluates hidden unit j
+// of every member, the member output is a warp reduction. Same per-member
+// rounding sequence as k_predict64 (out*std + mean, member order, /k, exp).
+__global__ void __launch_bounds__(256) k_rescore_warp(DEns e, const int64_t* __restrict__ idx,
+                                                      const uint32_t* __restrict__ n_ptr, double* __restrict__ pred) {
+  extern __shared__ double sm[];
+  stage_weights(e, sm);
+  __syncthreads();
+  const uint32_t n = *n_ptr;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int nw = e.k * e.h * e.d, nh = e.k * e.h;
+  const double* W1 = sm;
+  const double* B1 = sm + nw;
+  const double* W2 = sm + nw + nh;
+  const double* B2 = sm + nw + 2 * nh;
+  const double* MU = B2 + e.k;
+  const double* SD = MU + e.k;
+  for (uint32_t t = blockIdx.x * wpb + (threadIdx.x >> 5); t < n; t += gridDim.x * wpb) {
+    uint64_t r = (uint64_t)idx[t];
+    double x[kMaxP];
+#pragma unroll
+    for (int p = kMaxP - 1; p >= 0; --p) {
+      if (p < e.d) {
+        const uint64_t c = (uint64_t)e.counts[p];
+        const uint64_t q = r / c;
+        x[p] = (double)(r - q * c) / (double)(e.counts[p] > 1 ? e.counts[p] - 1 : 1);
+        r = q;
+      } else {
+        x[p] = 0.0;
+      }
+    }
+    double acc = 0.0;
+    for (int m = 0; m < e.k; ++m) {
+      double part = 0.0;
+      for (int j = lane; j < e.h; j += 32) {
+        const double* w = W1 + (m * e.h + j) * e.d;
+        double z = 0.0;
+#pragma unroll
+        for (int p = 0; p < kMaxP; ++p)
+          if (p < e.d) z = fma(x[p], w[p], z);
+        z = __dadd_rn(z, B1[m * e.h + j]);
+        part = fma(1.0 / (1.0 + exp(-z)), W2[m * e.h + j], part);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const double out = __dadd_rn(part, B2[m]);
+      const double lg = __dadd_rn(__dmul_rn(out, SD[m]), MU[m]);
+      acc = (m == 0) ? lg : __dadd_rn(acc, lg);
+    }
+    if (lane == 0) pred[t] = exp(__ddiv_rn(acc, (double)e.k));
+  }
+}
+
+}  // namespace mlt

@@ -1,0 +1,95 @@
+// select.cu — the final stage of the guard-band top-m (reference: the
+// global lexsort of tuner.py:128-131).
+//
+//   k_band_filter  one CTA: the exact m-th smallest fp32 mean log tau_m over all
+//                  candidates (radix select), then keep f32 <= tau_m + 2*delta.
+//                  Every configuration of the true top-m passes.
+//   k_rescore_warp (predict.cu) fp64 prediction of the survivors, one warp each.
+//   k_sort_small   one CTA: bitonic sort of <= kSmallSort (prediction, index)
+//                  pairs in shared memory and the first m written out; larger
+//                  survivor sets are sorted by the caller with CUB.
+#include "kernels.cuh"
+
+namespace mlt {
+
+__global__ void __launch_bounds__(1024) k_band_filter(const int64_t* __restrict__ cidx, const float* __restrict__ cval,
+                                                      uint32_t count, int m, float band, int64_t* __restrict__ out_idx,
+                                                      float* __restrict__ out_val, uint32_t* __restrict__ out_n) {
+  __shared__ uint32_t s_hist[256], s_sel[2], s_n;
+  const int tid = threadIdx.x;
+  float theta = __int_as_float(0x7f800000);   // +inf: keep everything when count < m
+  if (count >= (uint32_t)m) {
+    const uint32_t key = block_select(
+        [&](auto&& f) {
+          for (uint32_t e = tid; e < count; e += blockDim.x) f(fkey(cval[e]));
+        },
+        m, s_hist, s_sel);
+    theta = __fadd_ru(fkey_inv(key), band);
+  }
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  for (uint32_t e = tid; e < count; e += blockDim.x) {
+    const float v = cval[e];
+    if (!(v > theta)) {
+      const uint32_t slot = atomicAdd(&s_n, 1u);
+      out_idx[slot] = cidx[e];
+      out_val[slot] = v;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *out_n = s_n;
+}
+
+__global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ pred, const int64_t* __restrict__ idx,
+                                                     const uint32_t* __restrict__ n_ptr, int m,
+                                                     double* __restrict__ out_pred, int64_t* __restrict__ out_idx,
+                                                     uint32_t* __restrict__ status) {
+  extern __shared__ unsigned long long sk[];     // [N] prediction bits, then [N] indices
+  const uint32_t n = *n_ptr;
+  const int tid = threadIdx.x;
+  if (n > (uint32_t)kSmallSort) {
+    if (tid == 0) status[0] = 1;                 // caller sorts with CUB
+    return;
+  }
+  uint32_t N = 1;
+  while (N < n) N <<= 1;
+  unsigned long long* key = sk;
+  long long* ix = reinterpret_cast<long long*>(sk + kSmallSort);
+  for (uint32_t e = tid; e < N; e += blockDim.x) {
+    key[e] = e < n ? (unsigned long long)__double_as_longlong(pred[e]) : 0x7ff0000000000000ull;
+    ix[e] = e < n ? idx[e] : INT64_MAX;
+  }
+  __syncthreads();
+  // predictions are positive doubles: their bit patterns order like the values
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t e = tid; e < N; e += blockDim.x) {
+        const uint32_t p = e ^ j;
+        if (p > e) {
+          const bool up = (e & k) == 0;
+          const bool gt = key[e] > key[p] || (key[e] == key[p] && ix[e] > ix[p]);
+          if (gt == up) {
+            const unsigned long long tk = key[e];
+            key[e] = key[p];
+            key[p] = tk;
+            const long long ti = ix[e];
+            ix[e] = ix[p];
+            ix[p] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t take = min((uint32_t)m, n);
+  for (uint32_t e = tid; e < take; e += blockDim.x) {
+    out_pred[e] = __longlong_as_double((long long)key[e]);
+    out_idx[e] = ix[e];
+  }
+  if (tid == 0) {
+    status[0] = 0;
+    status[1] = take;
+  }
+}
+
+}  // namespace mlt

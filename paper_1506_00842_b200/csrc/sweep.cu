@@ -23,60 +23,81 @@
 namespace mlt {
 
 // ---------------------------------------------------------------------------
-// Tables
+// Tables (fp64 arithmetic, rounded once to fp32). One thread per
+// (configuration, member): digits are decoded once, then the member's 30
+// units are written; W1 reads are warp-uniform broadcasts.
 // ---------------------------------------------------------------------------
+
+// digit features x_p = digit / max(count-1, 1) of params [p_lo, p_hi) of `id`,
+// where `id` indexes that sub-space (last parameter fastest).
+__device__ __forceinline__ void sub_features(const TableArgs& t, uint64_t id, int p_lo, int p_hi,
+                                             double (&x)[kMaxP]) {
+#pragma unroll
+  for (int p = kMaxP - 1; p >= 0; --p) {
+    if (p >= p_lo && p < p_hi) {
+      const uint32_t c = (uint32_t)t.radix[p];
+      uint32_t dig;
+      if (id <= 0xffffffffull) {
+        const uint32_t r = (uint32_t)id;
+        dig = r % c;
+        id = r / c;
+      } else {
+        dig = (uint32_t)(id % c);
+        id /= c;
+      }
+      x[p] = (double)dig / (double)(c > 1 ? c - 1 : 1);
+    } else {
+      x[p] = 0.0;
+    }
+  }
+}
 
 __global__ void k_table_outer(TableArgs t) {
   const int KH = t.k * kH;
-  const int64_t total = (int64_t)t.n_ob * KH * kOB;
+  const int64_t total = (int64_t)t.n_ob * t.k * kOB;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(q % kOB);
-    const int mj = (int)((q / kOB) % KH);
-    const int64_t ob = q / ((int64_t)kOB * KH);
-    const int m = mj / kH, j = mj % kH;
-    float out = 1.0f;
-    if (j < t.h && t.wprime[mj] != 0.0) {
-      uint64_t o = (uint64_t)(t.o_lo + ob * kOB + r);
-      const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
-      double acc = 0.0;
-      for (int p = t.split - 1; p >= 0; --p) {
-        const uint64_t c = (uint64_t)t.radix[p];
-        const uint64_t qq = o / c;
-        const int dig = (int)(o - qq * c);
-        o = qq;
-        const double x = (double)dig / (double)(t.radix[p] > 1 ? t.radix[p] - 1 : 1);
-        acc = fma(x, w[p], acc);
+    const int m = (int)((q / kOB) % t.k);
+    const int64_t ob = q / ((int64_t)kOB * t.k);
+    double x[kMaxP];
+    sub_features(t, (uint64_t)(t.o_lo + ob * kOB + r), 0, t.split, x);
+    float* dst = t.ea + ((size_t)ob * KH + (size_t)m * kH) * kOB + r;
+    for (int j = 0; j < kH; ++j) {
+      const int mj = m * kH + j;
+      float out = 1.0f;
+      if (j < t.h && t.wprime[mj] != 0.0) {
+        const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < kMaxP; ++p)
+          if (p < t.split) acc = fma(x[p], w[p], acc);
+        out = (float)exp(-(acc + t.b1[(size_t)m * t.h + j] - t.cshift[mj]));
       }
-      const double a = acc + t.b1[(size_t)m * t.h + j] - t.cshift[mj];
-      out = (float)exp(-a);
+      dst[(size_t)j * kOB] = out;
     }
-    t.ea[q] = out;
   }
 }
 
 __global__ void k_table_inner(TableArgs t) {
-  const int KH = t.k * kH;
-  const int64_t total = (int64_t)KH * t.c_in_pad;
+  const int64_t total = (int64_t)t.k * t.c_in_pad;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = q % t.c_in_pad;
-    const int mj = (int)(q / t.c_in_pad);
-    const int m = mj / kH, j = mj % kH;
-    float out = 0.0f;
-    if (i < t.c_in && j < t.h && t.wprime[mj] != 0.0) {
-      uint64_t r = (uint64_t)i;
-      const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
-      double acc = 0.0;
-      for (int p = t.d - 1; p >= t.split; --p) {
-        const uint64_t c = (uint64_t)t.radix[p];
-        const uint64_t qq = r / c;
-        const int dig = (int)(r - qq * c);
-        r = qq;
-        const double x = (double)dig / (double)(t.radix[p] > 1 ? t.radix[p] - 1 : 1);
-        acc = fma(x, w[p], acc);
+    const int m = (int)(q / t.c_in_pad);
+    double x[kMaxP];
+    sub_features(t, (uint64_t)i, t.split, t.d, x);
+    for (int j = 0; j < kH; ++j) {
+      const int mj = m * kH + j;
+      float out = 0.0f;
+      if (i < t.c_in && j < t.h && t.wprime[mj] != 0.0) {
+        const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < kMaxP; ++p)
+          if (p >= t.split && p < t.d) acc = fma(x[p], w[p], acc);
+        out = (float)(exp(-(acc + t.cshift[mj])) * t.winv[mj]);
       }
-      out = (float)(exp(-(acc + t.cshift[mj])) / t.wprime[mj]);
+      t.ebp[(size_t)mj * t.c_in_pad + i] = out;
     }
-    t.ebp[q] = out;
   }
 }
 
@@ -135,61 +156,50 @@ __device__ __forceinline__ void combine<3>(const f2 (&d)[3], f2& num, f2& den) {
   den = fmul2(p, d[2]);
 }
 
-// ---------------------------------------------------------------------------
-// block-wide radix select: the exact m-th smallest ordered key (1-based)
-// among keys visited by `visit` (each thread visits its own keys).
-// ---------------------------------------------------------------------------
-template <typename V>
-__device__ __forceinline__ uint32_t block_select(V visit, int m, uint32_t* s_hist, uint32_t* s_sel) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t prefix = 0;
-  uint32_t want = (uint32_t)m;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    for (int b = tid; b < 256; b += blockDim.x) s_hist[b] = 0u;
-    __syncthreads();
-    visit([&](uint32_t key) {
-      if (pass == 0 || (key >> (shift + 8)) == prefix) {
-        const uint32_t bin = (key >> shift) & 255u;
-        const uint32_t peers = __match_any_sync(__activemask(), bin);
-        if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[bin], (uint32_t)__popc(peers));
-      }
-    });
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t c[8], tot = 0;
+// Per-thread factors of one group of G units: exp(-B')/w' for both inners
+// (global, L2-resident, coalesced) and 1/w' (shared, broadcast).
+template <int G>
+__device__ __forceinline__ void load_group(const float* pe, int64_t c_in_pad, const float* pu,
+                                           float (&eb)[kInner][G], float (&uu)[G]) {
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        c[b] = s_hist[lane * 8 + b];
-        tot += c[b];
-      }
-      uint32_t incl = tot;
+  for (int x = 0; x < G; ++x) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t excl = incl - tot;
-      if (excl < want && want <= incl) {
-        uint32_t run = excl;
-        int bin = lane * 8 + 7;
+    for (int s = 0; s < kInner; ++s) eb[s][x] = __ldg(pe + (size_t)x * c_in_pad + s * kThreads);
+    uu[x] = pu[x];
+  }
+}
+
+// One group of G units for all kInner x kOB configurations of the thread:
+// d' = exp(-A')*(exp(-B')/w') + 1/w' (FFMA2 over an outer pair), the G-term
+// rational combination, two reciprocals, one accumulate.
+template <int G>
+__device__ __forceinline__ void group_step(f2 (&acc)[kInner][kOB / 2], const float* E,
+                                           const float (&eb)[kInner][G], const float (&uu)[G]) {
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (run + c[b] >= want) {
-            bin = lane * 8 + b;
-            break;
-          }
-          run += c[b];
+  for (int q = 0; q < kOB / 4; ++q) {
+    float4 ea[G];
+#pragma unroll
+    for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * kOB + 4 * q);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+      for (int s = 0; s < kInner; ++s) {
+        f2 d[G];
+#pragma unroll
+        for (int x = 0; x < G; ++x) {
+          const f2 A = half ? pk(ea[x].z, ea[x].w) : pk(ea[x].x, ea[x].y);
+          d[x] = ffma2(A, pk(eb[s][x], eb[s][x]), pk(uu[x], uu[x]));
         }
-        s_sel[0] = (prefix << 8) | (uint32_t)bin;
-        s_sel[1] = want - run;
+        f2 num, den;
+        combine<G>(d, num, den);
+        float dl, dh;
+        upk(den, dl, dh);
+        const f2 r = pk(rcpa(dl), rcpa(dh));
+        f2& ac = acc[s][2 * q + half];
+        ac = (G == 1) ? fadd2(ac, r) : ffma2(num, r, ac);
       }
     }
-    __syncthreads();
-    prefix = s_sel[0];
-    want = s_sel[1];
   }
-  return prefix;
 }
 
 __device__ __forceinline__ void gappend(const SweepArgs& a, int64_t idx, float v) {
@@ -213,12 +223,17 @@ size_t sweep_smem(int k) {
   const size_t KH = (size_t)k * kH;
   return KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4;
 }
-
 // ---------------------------------------------------------------------------
 // the sweep
+//
+// CTA = 256 threads; a work item is kOB = 16 outer x kInnerBlock = 512 inner
+// configurations. Thread t owns inners {t, t + 256} of the block and all 16
+// outers, so every broadcast LDS.128 of exp(-A') feeds 2 x 4 configurations
+// and every per-thread exp(-B')/w' register feeds 16. acc[s][q] holds the
+// f32x2 pair of outers (2q, 2q+1) for inner s.
 // ---------------------------------------------------------------------------
 template <int G>
-__global__ void __launch_bounds__(kThreads) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int KH = a.k * kH;
   float* s_ea = reinterpret_cast<float*>(smraw);                 // [KH][kOB]
@@ -237,6 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep(SweepArgs a) {
   }
   const int ngroups = KH / G;
   const int n_items = a.n_ob * a.n_ib;
+  constexpr int kV = kInner * kOB;   // configurations per thread per work item (32)
 
   for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
     const int ob = w / a.n_ib, ib = w - ob * a.n_ib;
@@ -253,85 +269,68 @@ __global__ void __launch_bounds__(kThreads) k_sweep(SweepArgs a) {
     }
     __syncthreads();
 
-    const int64_t i = (int64_t)ib * kThreads + tid;
-    const float* ebcol = a.ebp + i;
-    f2 acc[kOB / 2];
+    const int64_t ibase = (int64_t)ib * kInnerBlock + tid;     // inner s is ibase + s*kThreads
+    const float* ebcol = a.ebp + ibase;
+    f2 acc[kInner][kOB / 2];
 #pragma unroll
-    for (int q = 0; q < kOB / 2; ++q) acc[q] = 0ull;
+    for (int s = 0; s < kInner; ++s)
+#pragma unroll
+      for (int q = 0; q < kOB / 2; ++q) acc[s][q] = 0ull;
 
-    float eb[G], uu[G];
-#pragma unroll
-    for (int x = 0; x < G; ++x) {
-      eb[x] = __ldg(ebcol + (size_t)x * a.c_in_pad);
-      uu[x] = s_u[x];
-    }
+    // Two register sets (A, B) ping-pong so the next group's per-thread factors
+    // are in flight from L2 while the current group computes, with no copies.
+    const size_t gstride = (size_t)G * a.c_in_pad;
+    const float* pe = ebcol;                 // per-thread exp(-B')/w' of the current group
+    const float* pu = s_u;                   // 1/w' of the current group
+    const float* E = s_ea;                   // exp(-A') rows of the current group
+    float ebA[kInner][G], uA[G], ebB[kInner][G], uB[G];
+    load_group<G>(pe, a.c_in_pad, pu, ebA, uA);
 #pragma unroll 1
-    for (int gi = 0; gi < ngroups; ++gi) {
-      const int mj0 = gi * G;
-      // prefetch the next group's per-thread factors (global/L2 latency)
-      float ebn[G], un[G];
-      const int mjn = (gi + 1 < ngroups) ? mj0 + G : mj0;
-#pragma unroll
-      for (int x = 0; x < G; ++x) {
-        ebn[x] = __ldg(ebcol + (size_t)(mjn + x) * a.c_in_pad);
-        un[x] = s_u[mjn + x];
-      }
-      const float* E = s_ea + (size_t)mj0 * kOB;
-#pragma unroll
-      for (int q = 0; q < kOB / 4; ++q) {
-        float4 ea[G];
-#pragma unroll
-        for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * kOB + 4 * q);
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          f2 d[G];
-#pragma unroll
-          for (int x = 0; x < G; ++x) {
-            const f2 A = half ? pk(ea[x].z, ea[x].w) : pk(ea[x].x, ea[x].y);
-            d[x] = ffma2(A, pk(eb[x], eb[x]), pk(uu[x], uu[x]));
-          }
-          f2 num, den;
-          combine<G>(d, num, den);
-          float dl, dh;
-          upk(den, dl, dh);
-          const f2 r = pk(rcpa(dl), rcpa(dh));
-          acc[2 * q + half] = (G == 1) ? fadd2(acc[2 * q + half], r) : ffma2(num, r, acc[2 * q + half]);
-        }
-      }
-#pragma unroll
-      for (int x = 0; x < G; ++x) {
-        eb[x] = ebn[x];
-        uu[x] = un[x];
-      }
+    for (int gi = 0; gi < ngroups; gi += 2) {
+      const bool has_b = gi + 1 < ngroups;
+      load_group<G>(has_b ? pe + gstride : pe, a.c_in_pad, has_b ? pu + G : pu, ebB, uB);
+      group_step<G>(acc, E, ebA, uA);
+      if (!has_b) break;
+      const bool has_c = gi + 2 < ngroups;
+      load_group<G>(has_c ? pe + 2 * gstride : pe, a.c_in_pad, has_c ? pu + 2 * G : pu, ebA, uA);
+      group_step<G>(acc, E + G * kOB, ebB, uB);
+      pe += 2 * gstride;
+      pu += 2 * G;
+      E += 2 * G * kOB;
     }
 
-    // ---- candidates ---------------------------------------------------------
-    float v[kOB];
+    // ---- candidates: bit (s*kOB + r) <-> inner s, outer r -----------------------
+    float v[kV];
 #pragma unroll
-    for (int q = 0; q < kOB / 2; ++q) {
-      upk(acc[q], v[2 * q], v[2 * q + 1]);
-      v[2 * q] += a.cst;
-      v[2 * q + 1] += a.cst;
-    }
+    for (int s = 0; s < kInner; ++s)
+#pragma unroll
+      for (int q = 0; q < kOB / 2; ++q) {
+        upk(acc[s][q], v[s * kOB + 2 * q], v[s * kOB + 2 * q + 1]);
+        v[s * kOB + 2 * q] += a.cst;
+        v[s * kOB + 2 * q + 1] += a.cst;
+      }
     const int64_t obase = a.o_lo + (int64_t)ob * kOB;
-    const bool ival = i < a.c_in;
+    auto cfg_index = [&](int b) -> int64_t {
+      return (obase + (b % kOB)) * a.c_in + ibase + (b / kOB) * kThreads;
+    };
     uint32_t mask = 0;
     {
       const float thf = fkey_inv(s_th);
 #pragma unroll
-      for (int r = 0; r < kOB; ++r) {
-        const int64_t idx = (obase + r) * a.c_in + i;
-        const bool in = ival && idx >= a.begin && idx < a.end;
-        if (in && !(v[r] > thf)) mask |= 1u << r;   // NaN passes (never silently dropped)
+      for (int b = 0; b < kV; ++b) {
+        const int64_t i = ibase + (b / kOB) * kThreads;
+        const int64_t idx = cfg_index(b);
+        const bool in = i < a.c_in && idx >= a.begin && idx < a.end;
+        if (in && !(v[b] > thf)) mask |= 1u << b;   // NaN passes (never silently dropped)
       }
     }
     if (a.check_rules && mask) {
 #pragma unroll 1
-      for (int r = 0; r < kOB; ++r) {
-        if (mask & (1u << r)) {
+      for (int b = 0; b < kV; ++b) {
+        if (mask & (1u << b)) {
           int dig[kMaxP];
-          decode_digits(a.sp, (uint64_t)((obase + r) * a.c_in + i), dig);
-          if (!rules_ok(a.sp, dig)) mask &= ~(1u << r);
+          decode_digits(a.sp, (uint64_t)cfg_index(b), dig);
+          if (!rules_ok(a.sp, dig)) mask &= ~(1u << b);
         }
       }
     }
@@ -347,16 +346,16 @@ __global__ void __launch_bounds__(kThreads) k_sweep(SweepArgs a) {
       const uint32_t key = block_select(
           [&](auto&& f) {
 #pragma unroll
-            for (int r = 0; r < kOB; ++r)
-              if (mask & (1u << r)) f(fkey(v[r]));
+            for (int b = 0; b < kV; ++b)
+              if (mask & (1u << b)) f(fkey(v[b]));
           },
           a.m, s_hist, s_sel);
       lower_threshold(a, &s_th, key);
       __syncthreads();
       const float thf = fkey_inv(s_th);
 #pragma unroll
-      for (int r = 0; r < kOB; ++r)
-        if (v[r] > thf) mask &= ~(1u << r);
+      for (int b = 0; b < kV; ++b)
+        if (v[b] > thf) mask &= ~(1u << b);
     }
     {  // append: warp-aggregated slot reservation
       const int c = __popc(mask);
@@ -370,14 +369,14 @@ __global__ void __launch_bounds__(kThreads) k_sweep(SweepArgs a) {
       if (lane == 31 && incl) base = atomicAdd(&s_n, incl);
       base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
 #pragma unroll
-      for (int r = 0; r < kOB; ++r) {
-        if (mask & (1u << r)) {
-          const int64_t idx = (obase + r) * a.c_in + i;
+      for (int b = 0; b < kV; ++b) {
+        if (mask & (1u << b)) {
+          const int64_t idx = cfg_index(b);
           if (base < kSB) {
             s_bidx[base] = idx;
-            s_bval[base] = v[r];
+            s_bval[base] = v[b];
           } else {
-            gappend(a, idx, v[r]);
+            gappend(a, idx, v[b]);
           }
           ++base;
         }

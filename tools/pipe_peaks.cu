@@ -39,7 +39,10 @@ __global__ void k_rcp(float* out, float s) {
   for (int c = 0; c < NCHAIN; ++c) a[c] = 1.0f + threadIdx.x * 1e-3f + c;
   for (int i = 0; i < ITERS; ++i) {
 #pragma unroll
-    for (int c = 0; c < NCHAIN; ++c) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[c]));
+    for (int c = 0; c < NCHAIN; ++c) {
+      asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[c]));
+      asm volatile("add.f32 %0, %0, 0f3F800000;" : "+f"(a[c]));   // defeats rcp(rcp(x)) folding
+    }
   }
   float r = 0; for (int c = 0; c < NCHAIN; ++c) r += a[c];
   if (r == 1234.5f) out[0] = r;
