@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -320,8 +321,22 @@ __global__ void k_merge_prep(const int64_t* idx, const double* pred, int64_t n, 
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// plan: resident descriptors + the fp32-sweep setup
+// plan: resident descriptors + the fp32-sweep setups
 // ---------------------------------------------------------------------------
+namespace {
+// Everything the factored sweep needs for one split point (outer params
+// [0, split), inner params [split, P)); computed once per split and cached.
+struct BandSetup {
+  bool ok = false;
+  std::string why;
+  int split = 0, G = 3, dummies = 0;
+  int64_t c_in = 1, c_in_pad = kInnerBlock;
+  double delta = 0, cst = 0;
+  double* d_tab = nullptr;      // [ca | cb | wprime] (k*kH each)
+  float* d_u = nullptr;         // [k*kH] 1/w'
+};
+}  // namespace
+
 struct mlt_plan {
   mlt_ctx* ctx = nullptr;
   HostSpace hs;
@@ -331,77 +346,77 @@ struct mlt_plan {
   int* d_rpos = nullptr;
   int64_t* d_rcoeff = nullptr;
   double* d_ens = nullptr;
-  double* d_tab = nullptr;      // [cshift | wprime] (k*kH each)
-  float* d_u = nullptr;         // [k*kH]
+  double* d_F = nullptr;        // per-parameter exp factors [k*kH][sum radix]
+  int foff[kMaxP + 1] = {0};
   DSpace ds{};
   DEns de{};
-  // sweep setup
-  bool band_ok = false;
-  std::string band_why;
-  int split = 0, G = 3, dummies = 0;
-  int64_t c_in = 1, c_in_pad = kInnerBlock;
-  double delta = 0, cst = 0;
+  bool factors_ok = false;
+  std::map<int, BandSetup> setups;
 };
 
 namespace {
 
-int plan_setup_band(mlt_plan* p) {
+// Inner/outer split for a sweep over n configurations: the inner factor must
+// fit a 512-thread-pair work item well (padding waste) and stay small enough
+// for the L2-resident table; table entries cost ~10 configuration-units each.
+int choose_split(const mlt_plan* p, int64_t n) {
+  const HostSpace& s = p->hs;
+  int best = s.P;
+  double best_cost = 1e300;
+  int64_t cin = 1;
+  for (int sp = s.P - 1; sp >= 0; --sp) {
+    cin *= s.radix[sp];
+    if (cin > 16384) break;
+    const int64_t pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
+    const double rows = std::ceil((double)n / cin) + 1.0;
+    const double waste = (double)n * ((double)pad / cin - 1.0);
+    const double cost = waste + 10.0 * ((double)pad + std::ceil(rows / kOB) * kOB);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best == s.P ? s.P - 1 : best;
+}
+
+int band_setup(mlt_plan* p, int split, BandSetup& b) {
   const HostEns& e = p->he;
   const HostSpace& s = p->hs;
-  p->band_ok = false;
-  if (e.h > kH) {
-    p->band_why = "hidden size > 30";
+  b = BandSetup();
+  b.split = split;
+  if (e.h > kH || !p->factors_ok) {
+    b.why = e.h > kH ? "hidden size > 30" : "first-layer weights too large for the factored tables";
     return MLT_OK;
   }
-  // split: inner = params [split, P); choose the largest inner cardinality
-  // <= 16384 that pads well to the 128-thread CTA.
-  int best = s.P;
-  int64_t best_cin = 1;
-  {
-    int64_t cin = 1;
-    int fallback = s.P;
-    int64_t fb_cin = 1;
-    for (int sp = s.P - 1; sp >= 0; --sp) {
-      cin *= s.radix[sp];
-      if (cin > 16384) break;
-      const int64_t pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
-      if ((double)cin / pad >= 0.75) {
-        best = sp;
-        best_cin = cin;
-      }
-      fallback = sp;
-      fb_cin = cin;
-    }
-    if (best == s.P) {
-      best = fallback;
-      best_cin = fb_cin;
-    }
-  }
-  p->split = best;
-  p->c_in = best_cin;
-  p->c_in_pad = (best_cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
+  int64_t cin = 1;
+  for (int q = split; q < s.P; ++q) cin *= s.radix[q];
+  b.c_in = cin;
+  b.c_in_pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
 
   const int KH = e.k * kH;
-  std::vector<double> cshift(KH, 0.0), wprime(KH, 0.0);
+  std::vector<double> tab(3 * (size_t)KH, 0.0);
+  double* ca = tab.data();
+  double* cb = ca + KH;
+  double* wpv = cb + KH;
   std::vector<float> u(KH, 1.0f);
   double S = 0, log2dmax = -1e300, log2dmin = 1e300;
   int dummies = 0;
-  bool ok = true;
-  std::string why;
-  for (int m = 0; m < e.k && ok; ++m) {
+  for (int m = 0; m < e.k; ++m) {
     for (int j = 0; j < kH; ++j) {
       const int mj = m * kH + j;
       const double wp = (j < e.h) ? e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k : 0.0;
       if (wp == 0.0) {
-        ++dummies;                // contributes exactly 1/d' = 1/(0*Eb' + 1) = 1
+        ++dummies;                // contributes exactly 1/d' = 1/(Ea*0 + 1) = 1
+        ca[mj] = 1.0;
         continue;
       }
-      double amin = e.b1()[(size_t)m * e.h + j], amax = amin, bmin = 0, bmax = 0;
+      const double b1 = e.b1()[(size_t)m * e.h + j];
+      double amin = b1, amax = b1, bmin = 0, bmax = 0;
       const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
       for (int q = 0; q < s.P; ++q) {
         if (s.radix[q] < 2) continue;
         const double lo = std::min(0.0, w[q]), hi = std::max(0.0, w[q]);
-        if (q < p->split) {
+        if (q < split) {
           amin += lo;
           amax += hi;
         } else {
@@ -409,29 +424,25 @@ int plan_setup_band(mlt_plan* p) {
           bmax += hi;
         }
       }
-      const double c = 0.5 * (amin - bmin);
+      const double c = 0.5 * (amin - bmin);   // centring: both tables span zmin/2 at their low end
       const double zmin = amin + bmin;
       const double lw = std::log(std::fabs(wp));
       const double lim = 80.0;
       // exp(-A'), exp(-B')/w' and 1/w' must be normal fp32 numbers
       if (!(amax - c <= lim && -(amin - c) <= lim && (bmax + c) + lw <= lim && -(bmin + c) - lw <= lim &&
             std::fabs(lw) <= lim)) {
-        ok = false;
-        why = "first-layer range too wide for fp32 tables";
-        break;
+        b.why = "first-layer range too wide for fp32 tables";
+        return MLT_OK;
       }
-      cshift[mj] = c;
-      wprime[mj] = wp;
+      ca[mj] = std::exp(-(b1 - c));
+      cb[mj] = std::exp(-c) / wp;
+      wpv[mj] = wp;
       u[mj] = (float)(1.0 / wp);
       S += std::fabs(wp);
       const double l2max = (std::log1p(std::exp(std::min(-zmin, 700.0))) - lw) / std::log(2.0);
       log2dmax = std::max(log2dmax, l2max);
       log2dmin = std::min(log2dmin, -lw / std::log(2.0));
     }
-  }
-  if (!ok) {
-    p->band_why = why;
-    return MLT_OK;
   }
   int G = 0;
   for (int g = 3; g >= 1; --g) {
@@ -442,16 +453,16 @@ int plan_setup_band(mlt_plan* p) {
   }
   if (p->ctx->opt_group >= 1 && p->ctx->opt_group <= 3) G = std::min(G, p->ctx->opt_group);
   if (G == 0) {
-    p->band_why = "reciprocal products would overflow fp32";
+    b.why = "reciprocal products would overflow fp32";
     return MLT_OK;
   }
-  p->G = G;
-  p->dummies = dummies;
+  b.G = G;
+  b.dummies = dummies;
   S += dummies;
   double cst = 0;
   for (int m = 0; m < e.k; ++m) cst += (e.b2()[m] * e.sd()[m] + e.mean()[m]) / e.k;
   cst -= dummies;
-  p->cst = cst;
+  b.cst = cst;
   const double uu = std::ldexp(1.0, -24);
   // A-priori |fp32 - exact| bound on the mean log:
   //  * each unit term 1/d' = w' sigma carries <= 4u relative error from the
@@ -463,22 +474,61 @@ int plan_setup_band(mlt_plan* p) {
   const double cg = G == 3 ? 30.0 : (G == 2 ? 16.0 : 8.0);
   double prefix = 0.0, acc_bound = 0.0;
   for (int q = 0; q < KH; q += G) {
-    for (int x = 0; x < G; ++x) prefix += wprime[q + x] != 0.0 ? std::fabs(wprime[q + x]) : 1.0;
+    for (int x = 0; x < G; ++x) prefix += wpv[q + x] != 0.0 ? std::fabs(wpv[q + x]) : 1.0;
     acc_bound += prefix;
   }
-  p->delta = 1.5 * uu * (cg * S + acc_bound + S + 3.0 * std::fabs(cst)) + 1e-12 * (1.0 + std::fabs(cst));
+  b.delta = 1.5 * uu * (cg * S + acc_bound + S + 3.0 * std::fabs(cst)) + 1e-12 * (1.0 + std::fabs(cst));
 
-  std::vector<double> tab(3 * (size_t)KH, 0.0);
-  std::copy(cshift.begin(), cshift.end(), tab.begin());
-  std::copy(wprime.begin(), wprime.end(), tab.begin() + KH);
-  for (int q = 0; q < KH; ++q) tab[2 * (size_t)KH + q] = wprime[q] != 0.0 ? 1.0 / wprime[q] : 0.0;
   mlt_ctx* c = p->ctx;
-  CU(cudaMalloc(&p->d_tab, tab.size() * 8));
-  CU(cudaMalloc(&p->d_u, (size_t)KH * 4));
-  CU(cudaMemcpyAsync(p->d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  CU(cudaMemcpyAsync(p->d_u, u.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  p->band_ok = true;
+  CU(cudaMalloc(&b.d_tab, tab.size() * 8));
+  CU(cudaMalloc(&b.d_u, (size_t)KH * 4));
+  CU(cudaMemcpyAsync(b.d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(b.d_u, u.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
+  b.ok = true;
+  return MLT_OK;
+}
+
+int get_setup(mlt_plan* p, int split, BandSetup** out) {
+  auto it = p->setups.find(split);
+  if (it == p->setups.end()) {
+    BandSetup b;
+    const int rc = band_setup(p, split, b);
+    if (rc != MLT_OK) {
+      cudaFree(b.d_tab);
+      cudaFree(b.d_u);
+      return rc;
+    }
+    it = p->setups.emplace(split, b).first;
+  }
+  *out = &it->second;
+  return MLT_OK;
+}
+
+// exp factors of every (unit, parameter, digit): computed once per plan.
+int plan_factors(mlt_plan* p) {
+  const HostEns& e = p->he;
+  const HostSpace& s = p->hs;
+  p->factors_ok = false;
+  double wmax = 0;
+  for (size_t q = 0; q < (size_t)e.k * e.h * e.d; ++q) wmax = std::max(wmax, std::fabs(e.w1()[q]));
+  if (wmax > 600.0) return MLT_OK;          // a single factor could overflow fp64
+  p->foff[0] = 0;
+  for (int q = 0; q < s.P; ++q) p->foff[q + 1] = p->foff[q] + s.radix[q];
+  const int KH = e.k * kH;
+  mlt_ctx* c = p->ctx;
+  CU(cudaMalloc(&p->d_F, (size_t)KH * p->foff[s.P] * 8));
+  TableArgs ta;
+  std::memset(&ta, 0, sizeof ta);
+  ta.k = e.k;
+  ta.d = e.d;
+  ta.h = e.h;
+  for (int q = 0; q < s.P; ++q) ta.radix[q] = s.radix[q];
+  for (int q = 0; q <= s.P; ++q) ta.foff[q] = p->foff[q];
+  ta.w1 = p->de.w1;
+  ta.F = p->d_F;
+  k_table_factors<<<grid_for(c, (int64_t)KH * p->foff[s.P], 256), 256, 0, c->stream>>>(ta);
+  TRY(check_launch(c));
+  p->factors_ok = true;
   return MLT_OK;
 }
 
@@ -536,8 +586,12 @@ void plan_free(mlt_plan* p) {
   cudaFree(p->d_rpos);
   cudaFree(p->d_rcoeff);
   cudaFree(p->d_ens);
-  cudaFree(p->d_tab);
-  cudaFree(p->d_u);
+  cudaFree(p->d_F);
+  for (auto& kv : p->setups) {
+    cudaFree(kv.second.d_tab);
+    cudaFree(kv.second.d_u);
+  }
+  p->setups.clear();
 }
 
 // fp64 materialise over a range or list, then sort: exact and general.
@@ -787,7 +841,7 @@ int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens,
       rc = fail(MLT_EMISMATCH, "encoder parameter %d has %d values, space has %d", q, p->he.counts[q],
                 p->hs.radix[q]);
   if (rc == MLT_OK) rc = plan_upload(p);
-  if (rc == MLT_OK) rc = plan_setup_band(p);
+  if (rc == MLT_OK) rc = plan_factors(p);
   if (rc != MLT_OK) {
     plan_free(p);
     delete p;
@@ -834,28 +888,29 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     n = end - begin;
   }
   local.configs = n;
-  local.split = p->hs.P - p->split;
   if (n == 0) {
     if (st) *st = local;
     return MLT_OK;
   }
   if (c->prof) CU(cudaEventRecord(c->ev[0], c->stream));
 
-  bool band = !idx_list && p->band_ok && m <= kMaxTopM && n >= 4096;
-  if (c->opt_path == 0 && !idx_list && p->band_ok && m <= kMaxTopM) band = true;
-  if (c->opt_path == 1) band = false;
+  BandSetup* bs = nullptr;
+  if (!idx_list && m <= kMaxTopM && c->opt_path != 1) TRY(get_setup(p, choose_split(p, n), &bs));
+  bool band = bs && bs->ok && (n >= 4096 || c->opt_path == 0);
 
   if (band) {
+    const BandSetup& B = *bs;
+    local.split = p->hs.P - B.split;
     const int KH = p->he.k * kH;
-    const int64_t o_lo = begin / p->c_in;
-    const int64_t o_hi = (end - 1) / p->c_in + 1;
+    const int64_t o_lo = begin / B.c_in;
+    const int64_t o_hi = (end - 1) / B.c_in + 1;
     const int n_ob = (int)((o_hi - o_lo + kOB - 1) / kOB);
-    const int n_ib = (int)(p->c_in_pad / kInnerBlock);
+    const int n_ib = (int)(B.c_in_pad / kInnerBlock);
     float *ea, *ebp, *cval;
     int64_t* cidx;
     uint32_t* gs;
     TRY(ws_t(c, S_EA, (size_t)n_ob * KH * kOB, &ea));
-    TRY(ws_t(c, S_EBP, (size_t)KH * p->c_in_pad, &ebp));
+    TRY(ws_t(c, S_EBP, (size_t)KH * B.c_in_pad, &ebp));
     TRY(ws_t(c, S_GSCAL, 8, &gs));
     TRY(ws_t(c, S_CIDX, (size_t)c->cand_cap, &cidx));
     TRY(ws_t(c, S_CVAL, (size_t)c->cand_cap, &cval));
@@ -864,16 +919,18 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.k = p->he.k;
     ta.d = p->he.d;
     ta.h = p->he.h;
-    ta.split = p->split;
+    ta.split = B.split;
     for (int q = 0; q < p->hs.P; ++q) ta.radix[q] = p->hs.radix[q];
+    for (int q = 0; q <= p->hs.P; ++q) ta.foff[q] = p->foff[q];
     ta.w1 = p->de.w1;
-    ta.b1 = p->de.b1;
-    ta.cshift = p->d_tab;
-    ta.wprime = p->d_tab + KH;
-    ta.winv = p->d_tab + 2 * KH;
+    ta.F = p->d_F;
+    ta.ca = B.d_tab;
+    ta.cb = B.d_tab + KH;
+    ta.wprime = B.d_tab + 2 * KH;
     ta.o_lo = o_lo;
-    ta.c_in = p->c_in;
-    ta.c_in_pad = p->c_in_pad;
+    ta.o_card = card / B.c_in;
+    ta.c_in = B.c_in;
+    ta.c_in_pad = B.c_in_pad;
     ta.n_ob = n_ob;
     ta.ea = ea;
     ta.ebp = ebp;
@@ -881,26 +938,34 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     hs[0] = 0xFF800000u;   // fkey(+inf)
     hs[1] = 0u;
     CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
-    k_table_outer<<<grid_for(c, (int64_t)n_ob * p->he.k * kOB, 128), 128, 0, c->stream>>>(ta);
-    TRY(check_launch(c));
-    k_table_inner<<<grid_for(c, (int64_t)p->he.k * p->c_in_pad, 128), 128, 0, c->stream>>>(ta);
-    TRY(check_launch(c));
+    {
+      const dim3 g_out((unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_ob * kOB + 127) / 128,
+                                                                        (int64_t)c->sms * 8 / p->he.k + 1)),
+                       (unsigned)p->he.k);
+      k_table_outer<<<g_out, 128, 0, c->stream>>>(ta);
+      TRY(check_launch(c));
+      const dim3 g_in((unsigned)std::max<int64_t>(1, std::min<int64_t>((B.c_in_pad + 127) / 128,
+                                                                       (int64_t)c->sms * 8 / p->he.k + 1)),
+                      (unsigned)p->he.k);
+      k_table_inner<<<g_in, 128, 0, c->stream>>>(ta);
+      TRY(check_launch(c));
+    }
 
     SweepArgs sa;
     std::memset(&sa, 0, sizeof sa);
     sa.k = p->he.k;
     sa.ea = ea;
     sa.ebp = ebp;
-    sa.u = p->d_u;
-    sa.c_in = p->c_in;
-    sa.c_in_pad = p->c_in_pad;
+    sa.u = B.d_u;
+    sa.c_in = B.c_in;
+    sa.c_in_pad = B.c_in_pad;
     sa.o_lo = o_lo;
     sa.n_ob = n_ob;
     sa.n_ib = n_ib;
     sa.begin = begin;
     sa.end = end;
-    sa.cst = (float)p->cst;
-    sa.band = (float)(2.0 * p->delta * (1.0 + 1e-6));
+    sa.cst = (float)B.cst;
+    sa.band = (float)(2.0 * B.delta * (1.0 + 1e-6));
     sa.m = (int)m;
     sa.g_theta = gs;
     sa.g_count = gs + 1;
@@ -911,7 +976,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     sa.sp = p->ds;
     const size_t smem = sweep_smem(p->he.k);
     if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);
-    void (*kern)(SweepArgs) = p->G == 3 ? k_sweep<3> : (p->G == 2 ? k_sweep<2> : k_sweep<1>);
+    void (*kern)(SweepArgs) = B.G == 3 ? k_sweep<3> : (B.G == 2 ? k_sweep<2> : k_sweep<1>);
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));
@@ -925,8 +990,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     CU(cudaMemcpyAsync(hs, gs, 8, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const uint32_t theta_key = hs[0], count = hs[1];
-    local.group = p->G;
-    local.delta = p->delta;
+    local.group = B.G;
+    local.delta = B.delta;
     if ((int64_t)count > c->cand_cap) {
       band = false;   // crowded guard band: fall back to the exact materialising path
     } else {
@@ -1047,6 +1112,22 @@ int mlt_merge_top_m(mlt_ctx* c, const int64_t* dev_idx, const double* dev_pred, 
   TRY(ws_t(c, S_OUT_D, n, &ib));
   k_merge_prep<<<grid_for(c, n, 256), 256, 0, c->stream>>>(dev_idx, dev_pred, n, ia, pa);
   TRY(check_launch(c));
+  if (n <= kSmallSort) {   // typical: P ranks x m entries -> one-CTA bitonic sort
+    uint32_t* gs;
+    double* tp;
+    int64_t* ti;
+    TRY(ws_t(c, S_GSCAL, 8, &gs));
+    TRY(ws_t(c, S_TOPI, (size_t)std::min(m, n), &ti));
+    TRY(ws_t(c, S_TOPP, (size_t)std::min(m, n), &tp));
+    uint32_t* hs = static_cast<uint32_t*>(c->pinned);
+    hs[2] = (uint32_t)n;
+    CU(cudaMemcpyAsync(gs + 2, hs + 2, 4, cudaMemcpyHostToDevice, c->stream));
+    const int ssmem = 16 * kSmallSort;
+    CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)std::min<int64_t>(m, n), tp, ti, gs + 3);
+    TRY(check_launch(c));
+    return emit_top(c, tp, ti, std::min(m, n), m, out_idx, out_pred, out_n);
+  }
   TRY(sort_pairs(c, &pa, &ia, pb, ib, n, true));
   return emit_top(c, pa, ia, n, m, out_idx, out_pred, out_n);
 }

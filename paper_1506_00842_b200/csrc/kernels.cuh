@@ -56,20 +56,27 @@ struct SweepArgs {
 };
 
 // Tables of the factored first layer (sweep.cu).
+// Tables of the factored first layer. exp(-z) factorises over parameters:
+//   F[mj][p][digit] = exp(-W1[mj][p] * x_p(digit))           (k_table_factors, once per plan)
+//   Ea(outer) = ca[mj] * prod_{p <  split} F[mj][p][digit_p]  ca = exp(-(b1 - c))
+//   Eb'(inner) = cb[mj] * prod_{p >= split} F[mj][p][digit_p] cb = exp(-c) / w'
+// so every table entry is a handful of fp64 multiplies (no exp), rounded once to fp32.
 struct TableArgs {
   int k, d, h, split;           // params [0, split) are outer, [split, d) inner
   int radix[kMaxP];
+  int foff[kMaxP + 1];          // offset of parameter p's digits in a row of F
   const double* w1;             // [k][h][d]
-  const double* b1;             // [k][h]
-  const double* cshift;         // [k*kH] centring constant c
-  const double* wprime;         // [k*kH] w2*std/k (0 for dummy units)
-  const double* winv;           // [k*kH] 1/w' (0 for dummy units)
-  int64_t o_lo, c_in, c_in_pad;
+  double* F;                    // [k*kH][foff[d]]
+  const double* ca;             // [k*kH]
+  const double* cb;             // [k*kH]  (0 for dummy units)
+  const double* wprime;         // [k*kH]  w2*std/k (0 for dummy units)
+  int64_t o_lo, o_card, c_in, c_in_pad;   // o_card = number of outer configurations
   int n_ob;
   float* ea;
   float* ebp;
 };
 
+__global__ void k_table_factors(TableArgs t);
 __global__ void k_table_outer(TableArgs t);
 __global__ void k_table_inner(TableArgs t);
 

@@ -23,78 +23,93 @@
 namespace mlt {
 
 // ---------------------------------------------------------------------------
-// Tables (fp64 arithmetic, rounded once to fp32). One thread per
-// (configuration, member): digits are decoded once, then the member's 30
-// units are written; W1 reads are warp-uniform broadcasts.
+// Tables (fp64 products, rounded once to fp32; see TableArgs in kernels.cuh)
 // ---------------------------------------------------------------------------
 
-// digit features x_p = digit / max(count-1, 1) of params [p_lo, p_hi) of `id`,
-// where `id` indexes that sub-space (last parameter fastest).
-__device__ __forceinline__ void sub_features(const TableArgs& t, uint64_t id, int p_lo, int p_hi,
-                                             double (&x)[kMaxP]) {
+__global__ void k_table_factors(TableArgs t) {
+  const int KH = t.k * kH;
+  const int fs = t.foff[t.d];
+  const int64_t total = (int64_t)KH * fs;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int mj = (int)(q / fs), r = (int)(q % fs);
+    const int m = mj / kH, j = mj % kH;
+    int p = 0;
+    while (t.foff[p + 1] <= r) ++p;
+    const int dig = r - t.foff[p];
+    double f = 1.0;
+    if (j < t.h) {
+      const double x = (double)dig / (double)(t.radix[p] > 1 ? t.radix[p] - 1 : 1);
+      f = exp(-(t.w1[((size_t)m * t.h + j) * t.d + p] * x));
+    }
+    t.F[q] = f;
+  }
+}
+
+// digits of the sub-index `id` over parameters [p_lo, p_hi) (last fastest)
+__device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int p_lo, int p_hi, int (&dig)[kMaxP]) {
 #pragma unroll
   for (int p = kMaxP - 1; p >= 0; --p) {
+    dig[p] = 0;
     if (p >= p_lo && p < p_hi) {
       const uint32_t c = (uint32_t)t.radix[p];
-      uint32_t dig;
       if (id <= 0xffffffffull) {
         const uint32_t r = (uint32_t)id;
-        dig = r % c;
+        dig[p] = (int)(r % c);
         id = r / c;
       } else {
-        dig = (uint32_t)(id % c);
+        dig[p] = (int)(id % c);
         id /= c;
       }
-      x[p] = (double)dig / (double)(c > 1 ? c - 1 : 1);
-    } else {
-      x[p] = 0.0;
     }
   }
 }
 
+// blockIdx.y = member; threads over (outer block, row): Ea[ob][m*30 + j][r]
 __global__ void k_table_outer(TableArgs t) {
   const int KH = t.k * kH;
-  const int64_t total = (int64_t)t.n_ob * t.k * kOB;
+  const int m = blockIdx.y;
+  const int fs = t.foff[t.d];
+  const int64_t total = (int64_t)t.n_ob * kOB;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(q % kOB);
-    const int m = (int)((q / kOB) % t.k);
-    const int64_t ob = q / ((int64_t)kOB * t.k);
-    double x[kMaxP];
-    sub_features(t, (uint64_t)(t.o_lo + ob * kOB + r), 0, t.split, x);
+    const int64_t ob = q / kOB;
+    int dig[kMaxP];
+    sub_digits(t, (uint64_t)(t.o_lo + q), 0, t.split, dig);
     float* dst = t.ea + ((size_t)ob * KH + (size_t)m * kH) * kOB + r;
     for (int j = 0; j < kH; ++j) {
       const int mj = m * kH + j;
       float out = 1.0f;
-      if (j < t.h && t.wprime[mj] != 0.0) {
-        const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
-        double acc = 0.0;
+      if (t.wprime[mj] != 0.0 && t.o_lo + q < t.o_card) {
+        const double* F = t.F + (size_t)mj * fs;
+        double e = t.ca[mj];
 #pragma unroll
         for (int p = 0; p < kMaxP; ++p)
-          if (p < t.split) acc = fma(x[p], w[p], acc);
-        out = (float)exp(-(acc + t.b1[(size_t)m * t.h + j] - t.cshift[mj]));
+          if (p < t.split) e *= F[t.foff[p] + dig[p]];
+        out = (float)e;
       }
       dst[(size_t)j * kOB] = out;
     }
   }
 }
 
+// blockIdx.y = member; threads over inner index: Eb'[m*30 + j][i]
 __global__ void k_table_inner(TableArgs t) {
-  const int64_t total = (int64_t)t.k * t.c_in_pad;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q % t.c_in_pad;
-    const int m = (int)(q / t.c_in_pad);
-    double x[kMaxP];
-    sub_features(t, (uint64_t)i, t.split, t.d, x);
+  const int m = blockIdx.y;
+  const int fs = t.foff[t.d];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < t.c_in_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int dig[kMaxP];
+    sub_digits(t, (uint64_t)i, t.split, t.d, dig);
     for (int j = 0; j < kH; ++j) {
       const int mj = m * kH + j;
       float out = 0.0f;
-      if (i < t.c_in && j < t.h && t.wprime[mj] != 0.0) {
-        const double* w = t.w1 + ((size_t)m * t.h + j) * t.d;
-        double acc = 0.0;
+      if (i < t.c_in && t.wprime[mj] != 0.0) {
+        const double* F = t.F + (size_t)mj * fs;
+        double e = t.cb[mj];
 #pragma unroll
         for (int p = 0; p < kMaxP; ++p)
-          if (p >= t.split && p < t.d) acc = fma(x[p], w[p], acc);
-        out = (float)(exp(-(acc + t.cshift[mj])) * t.winv[mj]);
+          if (p >= t.split && p < t.d) e *= F[t.foff[p] + dig[p]];
+        out = (float)e;
       }
       t.ebp[(size_t)mj * t.c_in_pad + i] = out;
     }
