@@ -18,7 +18,7 @@ import numpy as np
 
 from . import errors
 
-_LIB_PATH = Path(__file__).resolve().parent / "libmltune_b200.so"
+_LIB_PATH = Path(os.environ.get("MLTUNE_B200_LIB", Path(__file__).resolve().parent / "libmltune_b200.so"))
 
 MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
 MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP = 1, 2, 3

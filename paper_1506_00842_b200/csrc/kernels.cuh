@@ -26,10 +26,23 @@ __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint3
                              int64_t* out_idx, uint32_t* status);
 
 // ---- fp32 factored sweep (sweep.cu) ---------------------------------------
-constexpr int kThreads = 256;   // threads per sweep CTA
-constexpr int kInner = 2;       // inner configurations per thread (share every exp(-A') load)
+#ifndef MLT_THREADS
+#define MLT_THREADS 256
+#endif
+#ifndef MLT_INNER
+#define MLT_INNER 2
+#endif
+#ifndef MLT_OB
+#define MLT_OB 16
+#endif
+#ifndef MLT_MINB
+#define MLT_MINB 2
+#endif
+constexpr int kThreads = MLT_THREADS;   // threads per sweep CTA
+constexpr int kInner = MLT_INNER;   // inner configurations per thread (share every exp(-A') load)
 constexpr int kInnerBlock = kThreads * kInner;   // inner configurations per work item
-constexpr int kOB = 16;         // outer configurations per work item (per thread)
+constexpr int kOB = MLT_OB;         // outer configurations per work item (per thread)
+
 constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
 constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
 constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path

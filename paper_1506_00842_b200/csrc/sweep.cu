@@ -64,27 +64,46 @@ __device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int 
   }
 }
 
+// Stage member m's factor rows F[m*30 .. m*30+29][0, fs) in shared memory
+// (fs <= kMaxFactorCols) — the products below are then independent LDS reads.
+constexpr int kMaxFactorCols = 192;   // 30 x 192 x 8 B = 45 KB
+
+__device__ __forceinline__ const double* stage_factors(const TableArgs& t, int m, double* sF) {
+  const int fs = t.foff[t.d];
+  const double* src = t.F + (size_t)m * kH * fs;
+  if (fs > kMaxFactorCols) return src;
+  for (int q = threadIdx.x; q < kH * fs; q += blockDim.x) sF[q] = src[q];
+  __syncthreads();
+  return sF;
+}
+
 // blockIdx.y = member; threads over (outer block, row): Ea[ob][m*30 + j][r]
 __global__ void k_table_outer(TableArgs t) {
+  __shared__ double sF[kH * kMaxFactorCols];
   const int KH = t.k * kH;
   const int m = blockIdx.y;
   const int fs = t.foff[t.d];
+  const double* F = stage_factors(t, m, sF);
   const int64_t total = (int64_t)t.n_ob * kOB;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(q % kOB);
     const int64_t ob = q / kOB;
     int dig[kMaxP];
     sub_digits(t, (uint64_t)(t.o_lo + q), 0, t.split, dig);
+    int col[kMaxP];
+#pragma unroll
+    for (int p = 0; p < kMaxP; ++p) col[p] = t.foff[p] + dig[p];
+    const bool live = t.o_lo + q < t.o_card;
     float* dst = t.ea + ((size_t)ob * KH + (size_t)m * kH) * kOB + r;
     for (int j = 0; j < kH; ++j) {
       const int mj = m * kH + j;
       float out = 1.0f;
-      if (t.wprime[mj] != 0.0 && t.o_lo + q < t.o_card) {
-        const double* F = t.F + (size_t)mj * fs;
+      if (live && t.wprime[mj] != 0.0) {
+        const double* Fj = F + (size_t)j * fs;
         double e = t.ca[mj];
 #pragma unroll
         for (int p = 0; p < kMaxP; ++p)
-          if (p < t.split) e *= F[t.foff[p] + dig[p]];
+          if (p < t.split) e *= Fj[col[p]];
         out = (float)e;
       }
       dst[(size_t)j * kOB] = out;
@@ -94,21 +113,26 @@ __global__ void k_table_outer(TableArgs t) {
 
 // blockIdx.y = member; threads over inner index: Eb'[m*30 + j][i]
 __global__ void k_table_inner(TableArgs t) {
+  __shared__ double sF[kH * kMaxFactorCols];
   const int m = blockIdx.y;
   const int fs = t.foff[t.d];
+  const double* F = stage_factors(t, m, sF);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < t.c_in_pad;
        i += (int64_t)gridDim.x * blockDim.x) {
     int dig[kMaxP];
     sub_digits(t, (uint64_t)i, t.split, t.d, dig);
+    int col[kMaxP];
+#pragma unroll
+    for (int p = 0; p < kMaxP; ++p) col[p] = t.foff[p] + dig[p];
     for (int j = 0; j < kH; ++j) {
       const int mj = m * kH + j;
       float out = 0.0f;
       if (i < t.c_in && t.wprime[mj] != 0.0) {
-        const double* F = t.F + (size_t)mj * fs;
+        const double* Fj = F + (size_t)j * fs;
         double e = t.cb[mj];
 #pragma unroll
         for (int p = 0; p < kMaxP; ++p)
-          if (p >= t.split && p < t.d) e *= F[t.foff[p] + dig[p]];
+          if (p >= t.split && p < t.d) e *= Fj[col[p]];
         out = (float)e;
       }
       t.ebp[(size_t)mj * t.c_in_pad + i] = out;
@@ -248,7 +272,7 @@ size_t sweep_smem(int k) {
 // f32x2 pair of outers (2q, 2q+1) for inner s.
 // ---------------------------------------------------------------------------
 template <int G>
-__global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int KH = a.k * kH;
   float* s_ea = reinterpret_cast<float*>(smraw);                 // [KH][kOB]
