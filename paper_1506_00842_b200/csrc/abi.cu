@@ -910,7 +910,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     int64_t* cidx;
     uint32_t* gs;
     TRY(ws_t(c, S_EA, (size_t)n_ob * KH * kOB, &ea));
-    TRY(ws_t(c, S_EBP, (size_t)KH * B.c_in_pad, &ebp));
+    const int ebw = B.G == 3 ? ebw_of(3) : (B.G == 2 ? ebw_of(2) : ebw_of(1));
+    TRY(ws_t(c, S_EBP, (size_t)n_ib * (KH / B.G) * kThreads * ebw * 4, &ebp));
     TRY(ws_t(c, S_GSCAL, 8, &gs));
     TRY(ws_t(c, S_CIDX, (size_t)c->cand_cap, &cidx));
     TRY(ws_t(c, S_CVAL, (size_t)c->cand_cap, &cval));
@@ -920,6 +921,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.d = p->he.d;
     ta.h = p->he.h;
     ta.split = B.split;
+    ta.G = B.G;
     for (int q = 0; q < p->hs.P; ++q) ta.radix[q] = p->hs.radix[q];
     for (int q = 0; q <= p->hs.P; ++q) ta.foff[q] = p->foff[q];
     ta.w1 = p->de.w1;

@@ -43,6 +43,8 @@ constexpr int kInner = MLT_INNER;   // inner configurations per thread (share ev
 constexpr int kInnerBlock = kThreads * kInner;   // inner configurations per work item
 constexpr int kOB = MLT_OB;         // outer configurations per work item (per thread)
 
+// float4s per thread per group in the thread-contiguous exp(-B')/w' layout
+__host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
 constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
 constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
@@ -50,7 +52,7 @@ constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
 struct SweepArgs {
   int k;                        // members
   const float* ea;              // [n_ob][k*kH][kOB]  exp(-A') of outer configurations
-  const float* ebp;             // [k*kH][c_in_pad]   exp(-B') / w' of inner configurations
+  const float* ebp;             // [n_ib][group][thread][4*ebw] exp(-B') / w' of inner configurations
   const float* u;               // [k*kH]             1 / w'
   int64_t c_in, c_in_pad;       // inner cardinality (and padded to kThreads)
   int64_t o_lo;                 // outer index of ea block 0, row 0
@@ -76,6 +78,7 @@ struct SweepArgs {
 // so every table entry is a handful of fp64 multiplies (no exp), rounded once to fp32.
 struct TableArgs {
   int k, d, h, split;           // params [0, split) are outer, [split, d) inner
+  int G;                        // units per reciprocal group of the sweep (inner-table layout)
   int radix[kMaxP];
   int foff[kMaxP + 1];          // offset of parameter p's digits in a row of F
   const double* w1;             // [k][h][d]

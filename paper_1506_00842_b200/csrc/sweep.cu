@@ -111,12 +111,17 @@ __global__ void k_table_outer(TableArgs t) {
   }
 }
 
-// blockIdx.y = member; threads over inner index: Eb'[m*30 + j][i]
+// blockIdx.y = member; threads over inner index. Layout (thread-contiguous for
+// the sweep): ebp[ib][group][thread][ebw_of(G)*4] with unit x of the group and
+// inner slot s of the thread at x*kInner + s.
 __global__ void k_table_inner(TableArgs t) {
   __shared__ double sF[kH * kMaxFactorCols];
   const int m = blockIdx.y;
   const int fs = t.foff[t.d];
   const double* F = stage_factors(t, m, sF);
+  const int G = t.G;
+  const int ngroups = t.k * kH / G;
+  const int wf = 4 * (G == 3 ? ebw_of(3) : (G == 2 ? ebw_of(2) : ebw_of(1)));
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < t.c_in_pad;
        i += (int64_t)gridDim.x * blockDim.x) {
     int dig[kMaxP];
@@ -124,6 +129,8 @@ __global__ void k_table_inner(TableArgs t) {
     int col[kMaxP];
 #pragma unroll
     for (int p = 0; p < kMaxP; ++p) col[p] = t.foff[p] + dig[p];
+    const int64_t ib = i / kInnerBlock;
+    const int r = (int)(i % kInnerBlock), sl = r / kThreads, th = r % kThreads;
     for (int j = 0; j < kH; ++j) {
       const int mj = m * kH + j;
       float out = 0.0f;
@@ -135,7 +142,8 @@ __global__ void k_table_inner(TableArgs t) {
           if (p >= t.split && p < t.d) e *= Fj[col[p]];
         out = (float)e;
       }
-      t.ebp[(size_t)mj * t.c_in_pad + i] = out;
+      const int gi = mj / G, x = mj % G;
+      t.ebp[(((size_t)ib * ngroups + gi) * kThreads + th) * wf + x * kInner + sl] = out;
     }
   }
 }
@@ -195,15 +203,26 @@ __device__ __forceinline__ void combine<3>(const f2 (&d)[3], f2& num, f2& den) {
   den = fmul2(p, d[2]);
 }
 
-// Per-thread factors of one group of G units: exp(-B')/w' for both inners
-// (global, L2-resident, coalesced) and 1/w' (shared, broadcast).
+// Per-thread factors of one group of G units: exp(-B')/w' for the thread's
+// kInner inners, stored thread-contiguously (k_table_inner layout) so they
+// arrive in ebw_of(G) 16-byte loads; 1/w' is a shared-memory broadcast.
 template <int G>
-__device__ __forceinline__ void load_group(const float* pe, int64_t c_in_pad, const float* pu,
-                                           float (&eb)[kInner][G], float (&uu)[G]) {
+__device__ __forceinline__ void load_group(const float4* pe, const float* pu, float (&eb)[kInner][G],
+                                           float (&uu)[G]) {
+  constexpr int W = ebw_of(G);
+  float f[4 * W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const float4 v = __ldg(pe + w);
+    f[4 * w] = v.x;
+    f[4 * w + 1] = v.y;
+    f[4 * w + 2] = v.z;
+    f[4 * w + 3] = v.w;
+  }
 #pragma unroll
   for (int x = 0; x < G; ++x) {
 #pragma unroll
-    for (int s = 0; s < kInner; ++s) eb[s][x] = __ldg(pe + (size_t)x * c_in_pad + s * kThreads);
+    for (int s = 0; s < kInner; ++s) eb[s][x] = f[x * kInner + s];
     uu[x] = pu[x];
   }
 }
@@ -309,7 +328,6 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     __syncthreads();
 
     const int64_t ibase = (int64_t)ib * kInnerBlock + tid;     // inner s is ibase + s*kThreads
-    const float* ebcol = a.ebp + ibase;
     f2 acc[kInner][kOB / 2];
 #pragma unroll
     for (int s = 0; s < kInner; ++s)
@@ -318,20 +336,21 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
 
     // Two register sets (A, B) ping-pong so the next group's per-thread factors
     // are in flight from L2 while the current group computes, with no copies.
-    const size_t gstride = (size_t)G * a.c_in_pad;
-    const float* pe = ebcol;                 // per-thread exp(-B')/w' of the current group
+    constexpr int W = ebw_of(G);
+    const size_t gstride = (size_t)kThreads * W;   // float4s per group
+    const float4* pe = reinterpret_cast<const float4*>(a.ebp) + ((size_t)ib * ngroups * kThreads + tid) * W;
     const float* pu = s_u;                   // 1/w' of the current group
     const float* E = s_ea;                   // exp(-A') rows of the current group
     float ebA[kInner][G], uA[G], ebB[kInner][G], uB[G];
-    load_group<G>(pe, a.c_in_pad, pu, ebA, uA);
+    load_group<G>(pe, pu, ebA, uA);
 #pragma unroll 1
     for (int gi = 0; gi < ngroups; gi += 2) {
       const bool has_b = gi + 1 < ngroups;
-      load_group<G>(has_b ? pe + gstride : pe, a.c_in_pad, has_b ? pu + G : pu, ebB, uB);
+      load_group<G>(has_b ? pe + gstride : pe, has_b ? pu + G : pu, ebB, uB);
       group_step<G>(acc, E, ebA, uA);
       if (!has_b) break;
       const bool has_c = gi + 2 < ngroups;
-      load_group<G>(has_c ? pe + 2 * gstride : pe, a.c_in_pad, has_c ? pu + 2 * G : pu, ebA, uA);
+      load_group<G>(has_c ? pe + 2 * gstride : pe, has_c ? pu + 2 * G : pu, ebA, uA);
       group_step<G>(acc, E + G * kOB, ebB, uB);
       pe += 2 * gstride;
       pu += 2 * G;
