@@ -102,6 +102,7 @@ typedef struct mlt_sweep_stats {
   float total_ms;              /* device time of the whole call   (profiling on) */
   int32_t launches;            /* kernels launched by this call */
   int32_t split;               /* parameters in the inner (per-thread) factor */
+  int64_t raw_candidates;      /* configurations the streaming band kept before the exact filter */
 } mlt_sweep_stats;
 
 typedef struct mlt_ctx mlt_ctx;

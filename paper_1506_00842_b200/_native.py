@@ -44,7 +44,7 @@ class MltEnsemble(C.Structure):
 class MltSweepStats(C.Structure):
     _fields_ = [("configs", C.c_int64), ("candidates", C.c_int64), ("path", C.c_int32), ("group", C.c_int32),
                 ("delta", C.c_double), ("sweep_ms", C.c_float), ("total_ms", C.c_float),
-                ("launches", C.c_int32), ("split", C.c_int32)]
+                ("launches", C.c_int32), ("split", C.c_int32), ("raw_candidates", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

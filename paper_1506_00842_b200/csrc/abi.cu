@@ -69,7 +69,7 @@ namespace {
 
 enum Slot {
   S_SPACE_VALUES, S_SPACE_RPOS, S_SPACE_RCOEFF, S_ENS, S_IDX, S_OUT_A, S_OUT_B, S_OUT_C, S_OUT_D,
-  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT, S_TOPI, S_TOPP
+  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT, S_TOPI, S_TOPP, S_POH, S_POL, S_PIH, S_PIL
 };
 
 int ws(mlt_ctx* c, int slot, size_t bytes, void** out) {
@@ -366,7 +366,7 @@ int choose_split(const mlt_plan* p, int64_t n) {
   int64_t cin = 1;
   for (int sp = s.P - 1; sp >= 0; --sp) {
     cin *= s.radix[sp];
-    if (cin > 16384) break;
+    if (cin > 16384 || s.P - sp > 16) break;    // k_table_inner handles <= 16 inner params
     const int64_t pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
     const double rows = std::ceil((double)n / cin) + 1.0;
     const double waste = (double)n * ((double)pad / cin - 1.0);
@@ -941,15 +941,47 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     hs[1] = 0u;
     CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
     {
-      const dim3 g_out((unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n_ob * kOB + 127) / 128,
-                                                                        (int64_t)c->sms * 8 / p->he.k + 1)),
-                       (unsigned)p->he.k);
-      k_table_outer<<<g_out, 128, 0, c->stream>>>(ta);
+      // two-level split of each side: lo = trailing parameters with <= 64 combinations
+      auto lo_split = [&](int p_lo, int p_hi, int* sa, int64_t* nlo) {
+        int64_t n = 1;
+        int q = p_hi;
+        while (q > p_lo && n * p->hs.radix[q - 1] <= 64) n *= p->hs.radix[--q];
+        *sa = q;
+        *nlo = n;
+      };
+      int sa_o, sa_i;
+      int64_t nlo_o, nlo_i;
+      lo_split(0, B.split, &sa_o, &nlo_o);
+      lo_split(B.split, p->hs.P, &sa_i, &nlo_i);
+      const int64_t o_end = std::min<int64_t>(o_lo + (int64_t)n_ob * kOB, card / B.c_in);
+      const int64_t hb = o_lo / nlo_o, he = (std::max<int64_t>(o_end, o_lo + 1) - 1) / nlo_o + 1;
+      const int64_t nhi_i = B.c_in / nlo_i;
+      double *PoH, *PoL, *PiH, *PiL;
+      TRY(ws_t(c, S_POH, (size_t)KH * (he - hb), &PoH));
+      TRY(ws_t(c, S_POL, (size_t)KH * nlo_o, &PoL));
+      TRY(ws_t(c, S_PIH, (size_t)KH * nhi_i, &PiH));
+      TRY(ws_t(c, S_PIL, (size_t)KH * nlo_i, &PiL));
+      k_table_partial<<<grid_for(c, (int64_t)KH * (he - hb), 256), 256, 0, c->stream>>>(ta, 0, sa_o, hb, he - hb, PoH);
       TRY(check_launch(c));
-      const dim3 g_in((unsigned)std::max<int64_t>(1, std::min<int64_t>((B.c_in_pad + 127) / 128,
-                                                                       (int64_t)c->sms * 8 / p->he.k + 1)),
-                      (unsigned)p->he.k);
-      k_table_inner<<<g_in, 128, 0, c->stream>>>(ta);
+      k_table_partial<<<grid_for(c, (int64_t)KH * nlo_o, 256), 256, 0, c->stream>>>(ta, sa_o, B.split, 0, nlo_o, PoL);
+      TRY(check_launch(c));
+      k_table_partial<<<grid_for(c, (int64_t)KH * nhi_i, 256), 256, 0, c->stream>>>(ta, B.split, sa_i, 0, nhi_i, PiH);
+      TRY(check_launch(c));
+      k_table_partial<<<grid_for(c, (int64_t)KH * nlo_i, 256), 256, 0, c->stream>>>(ta, sa_i, p->hs.P, 0, nlo_i, PiL);
+      TRY(check_launch(c));
+      ta.PoH = PoH;
+      ta.PoL = PoL;
+      ta.PiH = PiH;
+      ta.PiL = PiL;
+      ta.o_nlo = nlo_o;
+      ta.o_nhi = he - hb;
+      ta.o_hi_base = hb;
+      ta.i_nlo = nlo_i;
+      ta.i_nhi = nhi_i;
+      k_table_outer<<<grid_for(c, (int64_t)n_ob * KH * kOB, 256), 256, 0, c->stream>>>(ta);
+      TRY(check_launch(c));
+      void (*tin)(TableArgs) = B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
+      tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads * 4 * ebw, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
     }
 
@@ -993,6 +1025,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     CU(cudaStreamSynchronize(c->stream));
     const uint32_t theta_key = hs[0], count = hs[1];
     local.group = B.G;
+    local.raw_candidates = count;
     local.delta = B.delta;
     if ((int64_t)count > c->cand_cap) {
       band = false;   // crowded guard band: fall back to the exact materialising path
@@ -1021,7 +1054,9 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       const size_t smem64 = predict64_smem(p->de);
       if (smem64 > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem64);
       CU(cudaFuncSetAttribute(k_rescore_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
-      const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)count + 7) / 8, (int64_t)c->sms * 4));
+      // survivors are few (~m); a fixed 32 x 8-warp grid avoids staging the
+      // weights into hundreds of idle CTAs (grid-stride over the device count)
+      const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)count + 7) / 8, 32));
       k_rescore_warp<<<rgrid, 256, smem64, c->stream>>>(p->de, ia, gs + 2, pa);
       TRY(check_launch(c));
       // 3) sort by (prediction, index) in one CTA when small

@@ -87,13 +87,18 @@ struct TableArgs {
   const double* cb;             // [k*kH]  (0 for dummy units)
   const double* wprime;         // [k*kH]  w2*std/k (0 for dummy units)
   int64_t o_lo, o_card, c_in, c_in_pad;   // o_card = number of outer configurations
+  // two-level split of each table: entry = const * P_hi[index / nlo] * P_lo[index % nlo]
+  const double *PoH, *PoL, *PiH, *PiL;    // [k*kH][n_hi] / [k*kH][n_lo]
+  int64_t o_nlo, o_nhi, o_hi_base, i_nlo, i_nhi;
   int n_ob;
   float* ea;
   float* ebp;
 };
 
 __global__ void k_table_factors(TableArgs t);
+__global__ void k_table_partial(TableArgs t, int p_lo, int p_hi, int64_t base, int64_t count, double* P);
 __global__ void k_table_outer(TableArgs t);
+template <int G>
 __global__ void k_table_inner(TableArgs t);
 
 template <int G>

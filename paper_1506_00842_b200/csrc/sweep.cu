@@ -64,87 +64,68 @@ __device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int 
   }
 }
 
-// Stage member m's factor rows F[m*30 .. m*30+29][0, fs) in shared memory
-// (fs <= kMaxFactorCols) — the products below are then independent LDS reads.
-constexpr int kMaxFactorCols = 192;   // 30 x 192 x 8 B = 45 KB
-
-__device__ __forceinline__ const double* stage_factors(const TableArgs& t, int m, double* sF) {
-  const int fs = t.foff[t.d];
-  const double* src = t.F + (size_t)m * kH * fs;
-  if (fs > kMaxFactorCols) return src;
-  for (int q = threadIdx.x; q < kH * fs; q += blockDim.x) sF[q] = src[q];
-  __syncthreads();
-  return sF;
-}
-
-// blockIdx.y = member; threads over (outer block, row): Ea[ob][m*30 + j][r]
-__global__ void k_table_outer(TableArgs t) {
-  __shared__ double sF[kH * kMaxFactorCols];
+// Partial products of the factor rows over a parameter range:
+//   P[mj][q] = prod_{p in [p_lo, p_hi)} F[mj][foff[p] + digit_p(base + q)]
+// where digits are those of the sub-index over [p_lo, p_hi) (last fastest).
+// Every table entry is then ca|cb * P_hi * P_lo: two fp64 multiplies.
+__global__ void k_table_partial(TableArgs t, int p_lo, int p_hi, int64_t base, int64_t count, double* __restrict__ P) {
   const int KH = t.k * kH;
-  const int m = blockIdx.y;
   const int fs = t.foff[t.d];
-  const double* F = stage_factors(t, m, sF);
-  const int64_t total = (int64_t)t.n_ob * kOB;
+  const int64_t total = (int64_t)KH * count;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(q % kOB);
-    const int64_t ob = q / kOB;
+    const int mj = (int)(q / count);
     int dig[kMaxP];
-    sub_digits(t, (uint64_t)(t.o_lo + q), 0, t.split, dig);
-    int col[kMaxP];
+    sub_digits(t, (uint64_t)(base + q % count), p_lo, p_hi, dig);
+    const double* Fj = t.F + (size_t)mj * fs;
+    double e = 1.0;
 #pragma unroll
-    for (int p = 0; p < kMaxP; ++p) col[p] = t.foff[p] + dig[p];
-    const bool live = t.o_lo + q < t.o_card;
-    float* dst = t.ea + ((size_t)ob * KH + (size_t)m * kH) * kOB + r;
-    for (int j = 0; j < kH; ++j) {
-      const int mj = m * kH + j;
-      float out = 1.0f;
-      if (live && t.wprime[mj] != 0.0) {
-        const double* Fj = F + (size_t)j * fs;
-        double e = t.ca[mj];
-#pragma unroll
-        for (int p = 0; p < kMaxP; ++p)
-          if (p < t.split) e *= Fj[col[p]];
-        out = (float)e;
-      }
-      dst[(size_t)j * kOB] = out;
-    }
+    for (int p = 0; p < kMaxP; ++p)
+      if (p >= p_lo && p < p_hi) e *= __ldg(Fj + t.foff[p] + dig[p]);
+    P[q] = e;
   }
 }
 
-// blockIdx.y = member; threads over inner index. Layout (thread-contiguous for
-// the sweep): ebp[ib][group][thread][ebw_of(G)*4] with unit x of the group and
-// inner slot s of the thread at x*kInner + s.
-__global__ void k_table_inner(TableArgs t) {
-  __shared__ double sF[kH * kMaxFactorCols];
-  const int m = blockIdx.y;
-  const int fs = t.foff[t.d];
-  const double* F = stage_factors(t, m, sF);
-  const int G = t.G;
-  const int ngroups = t.k * kH / G;
-  const int wf = 4 * (G == 3 ? ebw_of(3) : (G == 2 ? ebw_of(2) : ebw_of(1)));
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < t.c_in_pad;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int dig[kMaxP];
-    sub_digits(t, (uint64_t)i, t.split, t.d, dig);
-    int col[kMaxP];
-#pragma unroll
-    for (int p = 0; p < kMaxP; ++p) col[p] = t.foff[p] + dig[p];
-    const int64_t ib = i / kInnerBlock;
-    const int r = (int)(i % kInnerBlock), sl = r / kThreads, th = r % kThreads;
-    for (int j = 0; j < kH; ++j) {
-      const int mj = m * kH + j;
-      float out = 0.0f;
-      if (i < t.c_in && t.wprime[mj] != 0.0) {
-        const double* Fj = F + (size_t)j * fs;
-        double e = t.cb[mj];
-#pragma unroll
-        for (int p = 0; p < kMaxP; ++p)
-          if (p >= t.split && p < t.d) e *= Fj[col[p]];
-        out = (float)e;
-      }
-      const int gi = mj / G, x = mj % G;
-      t.ebp[(((size_t)ib * ngroups + gi) * kThreads + th) * wf + x * kInner + sl] = out;
+// Outer table Ea[ob][mj][r], one thread per element in output order.
+// Row o = o_lo + ob*kOB + r = (o / nlo) * nlo + o % nlo over the outer split.
+__global__ void k_table_outer(TableArgs t) {
+  const int KH = t.k * kH;
+  const int64_t total = (int64_t)t.n_ob * KH * kOB;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(q % kOB);
+    const int mj = (int)((q / kOB) % KH);
+    const int64_t o = t.o_lo + (q / ((int64_t)kOB * KH)) * kOB + r;
+    float out = 1.0f;
+    if (o < t.o_card && t.wprime[mj] != 0.0) {
+      const int64_t a = o / t.o_nlo - t.o_hi_base, b = o % t.o_nlo;
+      out = (float)(t.ca[mj] * __ldg(t.PoH + (size_t)mj * t.o_nhi + a) * __ldg(t.PoL + (size_t)mj * t.o_nlo + b));
     }
+    t.ea[q] = out;
+  }
+}
+
+// Inner table in the sweep's thread-contiguous layout ebp[ib][group][thread][4*ebw]
+// (slot x*kInner + s = unit x of the group for inner ib*kInnerBlock + s*kThreads
+// + thread; pad slots are zero), one thread per element in output order.
+template <int G>
+__global__ void k_table_inner(TableArgs t) {
+  constexpr int WF = 4 * ebw_of(G);
+  const int ngroups = t.k * kH / G;
+  const int64_t total = (t.c_in_pad / kInnerBlock) * (int64_t)ngroups * kThreads * WF;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int slot = (int)(q % WF);
+    const int th = (int)((q / WF) % kThreads);
+    const int64_t rest = q / ((int64_t)WF * kThreads);
+    const int gi = (int)(rest % ngroups);
+    const int64_t ib = rest / ngroups;
+    const int x = slot / kInner, s = slot % kInner;
+    const int mj = gi * G + x;
+    const int64_t i = ib * kInnerBlock + (int64_t)s * kThreads + th;
+    float out = 0.0f;
+    if (x < G && i < t.c_in) {
+      const int64_t a = i / t.i_nlo, b = i % t.i_nlo;     // cb = 0 for dummy units
+      out = (float)(t.cb[mj] * __ldg(t.PiH + (size_t)mj * t.i_nhi + a) * __ldg(t.PiL + (size_t)mj * t.i_nlo + b));
+    }
+    t.ebp[q] = out;
   }
 }
 
@@ -498,14 +479,18 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     }
   }
   __syncthreads();
-  {  // final flush of this CTA's candidates
-    const float thf = fkey_inv(s_th);
+  {  // final flush of this CTA's candidates, against the freshest global threshold
+    const uint32_t g = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
+    const float thf = fkey_inv(min(s_th, g));
     const int n = min(s_n, kSB);
     for (int e = tid; e < n; e += kThreads)
       if (!(s_bval[e] > thf)) gappend(a, s_bidx[e], s_bval[e]);
   }
 }
 
+template __global__ void k_table_inner<1>(TableArgs t);
+template __global__ void k_table_inner<2>(TableArgs t);
+template __global__ void k_table_inner<3>(TableArgs t);
 template __global__ void k_sweep<1>(SweepArgs a);
 template __global__ void k_sweep<2>(SweepArgs a);
 template __global__ void k_sweep<3>(SweepArgs a);

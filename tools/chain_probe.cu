@@ -1,6 +1,6 @@
-// Probe: the sweep's group arithmetic in isolation (LDS-fed exp(-A'), per-thread
-// factors held in registers, no global loads) at the sweep's occupancy, to
-// separate the dependency structure from memory latency.
+// Probe: the sweep's group arithmetic in isolation (LDS-fed exp(-A'),
+// per-thread factors held in registers, no global loads) for several tilings /
+// occupancies / schedules, to find what the dependency structure allows.
 #include <cstdio>
 #include <cuda_runtime.h>
 typedef unsigned long long f2;
@@ -10,66 +10,103 @@ __device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) { f2 d; asm("fma.rn.f32x2 
 __device__ __forceinline__ f2 fmul2(f2 a, f2 b) { f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
 __device__ __forceinline__ f2 fadd2(f2 a, f2 b) { f2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
 __device__ __forceinline__ float rcpa(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
-constexpr int kOB = 16, kInner = 2, G = 3;
-template <int LDG>
-__global__ void __launch_bounds__(256, 2) k_probe(float* out, const float* __restrict__ gsrc, int ngroups, int stride) {
-  __shared__ float4 s_ea[480 * kOB / 4];
-  for (int q = threadIdx.x; q < 480 * kOB / 4; q += 256) s_ea[q] = make_float4(1e-3f * q, 2e-3f, 3e-3f, 4e-3f * q);
-  __syncthreads();
-  f2 acc[kInner][kOB / 2];
-  for (int s = 0; s < kInner; ++s) for (int q = 0; q < kOB / 2; ++q) acc[s][q] = 0ull;
-  float eb[kInner][G], uu[G];
-  for (int x = 0; x < G; ++x) { uu[x] = 1.0f + x; for (int s = 0; s < kInner; ++s) eb[s][x] = 0.5f + threadIdx.x * 1e-4f + s + x; }
-  const float* pe = gsrc + threadIdx.x;
-  for (int rep = 0; rep < 8; ++rep) {
-#pragma unroll 1
-    for (int gi = 0; gi < ngroups; ++gi) {
-      if (LDG) {
+constexpr int G = 3;
+
+template <int KOB, int KIN, int PIPE>
+__device__ __forceinline__ void step(f2 (&acc)[KIN][KOB / 2], const float* E, const float (&eb)[KIN][G], const float (&uu)[G]) {
+  if (PIPE == 0) {
 #pragma unroll
-        for (int x = 0; x < G; ++x)
+    for (int q = 0; q < KOB / 4; ++q) {
+      float4 ea[G];
 #pragma unroll
-          for (int s = 0; s < kInner; ++s) eb[s][x] = __ldg(pe + (size_t)(gi * G + x) * stride + s * 256);
-      }
-      const float* E = reinterpret_cast<const float*>(s_ea) + (gi % 160) * G * kOB;
+      for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * KOB + 4 * q);
 #pragma unroll
-      for (int q = 0; q < kOB / 4; ++q) {
+      for (int half = 0; half < 2; ++half)
+#pragma unroll
+        for (int s = 0; s < KIN; ++s) {
+          f2 d[G];
+#pragma unroll
+          for (int x = 0; x < G; ++x) d[x] = ffma2(half ? pk(ea[x].z, ea[x].w) : pk(ea[x].x, ea[x].y), pk(eb[s][x], eb[s][x]), pk(uu[x], uu[x]));
+          const f2 sm = fadd2(d[0], d[1]), pr = fmul2(d[0], d[1]);
+          const f2 num = ffma2(d[2], sm, pr), den = fmul2(pr, d[2]);
+          float dl, dh; upk(den, dl, dh);
+          acc[s][2 * q + half] = ffma2(num, pk(rcpa(dl), rcpa(dh)), acc[s][2 * q + half]);
+        }
+    }
+  } else {
+    // quad-level software pipeline: reciprocals of quad q-1 interleaved with the FP work of quad q
+    constexpr int NP = 2 * KIN;     // pairs per quad
+    f2 pnum[NP], pden[NP];
+#pragma unroll
+    for (int q = 0; q <= KOB / 4; ++q) {
+      f2 cnum[NP], cden[NP];
+      if (q < KOB / 4) {
         float4 ea[G];
 #pragma unroll
-        for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * kOB + 4 * q);
+        for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * KOB + 4 * q);
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < 2; ++half)
 #pragma unroll
-          for (int s = 0; s < kInner; ++s) {
+          for (int s = 0; s < KIN; ++s) {
             f2 d[G];
 #pragma unroll
             for (int x = 0; x < G; ++x) d[x] = ffma2(half ? pk(ea[x].z, ea[x].w) : pk(ea[x].x, ea[x].y), pk(eb[s][x], eb[s][x]), pk(uu[x], uu[x]));
             const f2 sm = fadd2(d[0], d[1]), pr = fmul2(d[0], d[1]);
-            const f2 num = ffma2(d[2], sm, pr), den = fmul2(pr, d[2]);
-            float dl, dh; upk(den, dl, dh);
-            acc[s][2 * q + half] = ffma2(num, pk(rcpa(dl), rcpa(dh)), acc[s][2 * q + half]);
+            cnum[half * KIN + s] = ffma2(d[2], sm, pr);
+            cden[half * KIN + s] = fmul2(pr, d[2]);
           }
-        }
       }
+      if (q > 0) {
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+#pragma unroll
+          for (int s = 0; s < KIN; ++s) {
+            float dl, dh; upk(pden[half * KIN + s], dl, dh);
+            acc[s][2 * (q - 1) + half] = ffma2(pnum[half * KIN + s], pk(rcpa(dl), rcpa(dh)), acc[s][2 * (q - 1) + half]);
+          }
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) { pnum[p] = cnum[p]; pden[p] = cden[p]; }
     }
   }
-  float t = 0; for (int s = 0; s < kInner; ++s) for (int q = 0; q < kOB / 2; ++q) { float a, b; upk(acc[s][q], a, b); t += a + b; }
+}
+
+template <int KOB, int KIN, int MINB, int PIPE>
+__global__ void __launch_bounds__(256, MINB) k_probe(float* out, int ngroups) {
+  __shared__ float4 s_ea[480 * 16 / 4];
+  for (int q = threadIdx.x; q < 480 * KOB / 4; q += 256) s_ea[q] = make_float4(1e-3f * q, 2e-3f, 3e-3f, 4e-3f * q);
+  __syncthreads();
+  f2 acc[KIN][KOB / 2];
+  for (int s = 0; s < KIN; ++s) for (int q = 0; q < KOB / 2; ++q) acc[s][q] = 0ull;
+  float eb[KIN][G], uu[G];
+  for (int x = 0; x < G; ++x) { uu[x] = 1.0f + x; for (int s = 0; s < KIN; ++s) eb[s][x] = 0.5f + threadIdx.x * 1e-4f + s + x; }
+  for (int rep = 0; rep < 8; ++rep) {
+#pragma unroll 1
+    for (int gi = 0; gi < ngroups; ++gi) {
+      const float* E = reinterpret_cast<const float*>(s_ea) + (gi % (2560 / KOB)) * G * KOB;
+      step<KOB, KIN, PIPE>(acc, E, eb, uu);
+    }
+  }
+  float t = 0; for (int s = 0; s < KIN; ++s) for (int q = 0; q < KOB / 2; ++q) { float a, b; upk(acc[s][q], a, b); t += a + b; }
   if (t == 1234.5f) out[0] = t;
 }
-template <int LDG>
-void run(float* out, float* g, int ngroups) {
+template <int KOB, int KIN, int MINB, int PIPE>
+void run(float* out) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  int blocks = 148 * 2;
-  k_probe<LDG><<<blocks, 256>>>(out, g, ngroups, 12288); cudaDeviceSynchronize();
-  cudaEventRecord(e0); k_probe<LDG><<<blocks, 256>>>(out, g, ngroups, 12288); cudaEventRecord(e1); cudaEventSynchronize(e1);
+  int nb = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_probe<KOB, KIN, MINB, PIPE>, 256, 0);
+  int blocks = 148 * nb;
+  const int ngroups = 160 * 32 / (KOB * KIN);   // same work per thread for every tiling (E index wraps)
+  k_probe<KOB, KIN, MINB, PIPE><<<blocks, 256>>>(out, ngroups); cudaDeviceSynchronize();
+  cudaEventRecord(e0); k_probe<KOB, KIN, MINB, PIPE><<<blocks, 256>>>(out, ngroups); cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  double pairs = (double)blocks * 256 * 8 * ngroups * kInner * (kOB / 2);    // pair-chains
-  double lanefma = pairs * 2 * 8;     // 8 packed FP per pair chain, 2 lanes each
-  double mufu = pairs * 2;
-  printf("{\"ldg\": %d, \"ms\": %.3f, \"fma_frac\": %.3f, \"mufu_frac\": %.3f}\n", LDG, ms,
-         lanefma / (ms * 1e-3) / (148.0 * 128 * 1.965e9), mufu / (ms * 1e-3) / (148.0 * 16 * 1.965e9));
+  double pairs = (double)blocks * 256 * 8 * ngroups * KIN * (KOB / 2);
+  cudaFuncAttributes fa; cudaFuncGetAttributes(&fa, k_probe<KOB, KIN, MINB, PIPE>);
+  printf("{\"kob\": %d, \"kin\": %d, \"minb\": %d, \"pipe\": %d, \"regs\": %d, \"ctas_per_sm\": %d, \"ms\": %.3f, \"frac\": %.3f}\n",
+         KOB, KIN, MINB, PIPE, fa.numRegs, nb, ms, pairs * 16 / (ms * 1e-3) / (148.0 * 128 * 1.965e9));
 }
 int main() {
-  float *out, *g; cudaMalloc(&out, 4); cudaMalloc(&g, 480 * 12288 * 4); cudaMemset(g, 0, 480 * 12288 * 4);
-  run<0>(out, g, 160); run<1>(out, g, 160);
+  float* out; cudaMalloc(&out, 4);
+  run<16, 2, 2, 0>(out); run<16, 2, 2, 1>(out); run<8, 2, 3, 0>(out); run<8, 2, 3, 1>(out); run<8, 4, 2, 0>(out);
+  run<8, 4, 2, 1>(out); run<16, 1, 3, 0>(out); run<32, 1, 2, 0>(out); run<8, 2, 4, 0>(out); run<16, 2, 1, 0>(out);
   return 0;
 }

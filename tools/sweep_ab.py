@@ -32,4 +32,4 @@ g = np.load(G / f"topm_{case}.npz")
 ok = bool(np.array_equal(oi[:on.value], g["m200_i"])) if "m200_i" in g.files else None
 print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "sweep_ms_min": min(sw),
                   "sweep_ms_med": float(np.median(sw)), "total_ms_med": float(np.median(tot)),
-                  "parity": ok, "group": st.group, "cands": st.candidates}))
+                  "parity": ok, "group": st.group, "cands": st.candidates, "raw": st.raw_candidates, "delta": st.delta}))
