@@ -21,12 +21,19 @@ bounded contiguous sample of the same workload.
 
 from __future__ import annotations
 
+import os
+import sys
+
+if "--impl" in sys.argv and "reference" in sys.argv:
+    # the CPU reference arm uses every host thread for BLAS, even under torchrun
+    # (which exports OMP_NUM_THREADS=1); must happen before numpy is imported
+    _n = str(len(os.sched_getaffinity(0)))
+    os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = _n
+
 import argparse
 import json
-import os
 import statistics
 import subprocess
-import sys
 import threading
 import time
 from pathlib import Path
@@ -121,6 +128,14 @@ def _oracle_workload(space_name):
     return space_from_doc(spaces[space_name]), ensemble_from_doc(json.loads((GOLDEN / f"model_{case}.json").read_text()))
 
 
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max(int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas")
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
 def cpu_baseline(space_name, m, n_cfg):
     """The reference algorithm (oracle restatement, bit-exact with `mltune` on
     every golden fixture) on a bounded contiguous sample, host cores, float64
@@ -131,11 +146,47 @@ def cpu_baseline(space_name, m, n_cfg):
     t0 = time.perf_counter()
     top_m(oens, osp, m, begin=0, end=n_cfg)
     dt = time.perf_counter() - t0
-    cores = len(os.sched_getaffinity(0))
+    cores = blas_threads()
     return {"value": n_cfg / dt, "unit": "configs/s", "cores": cores, "kind": "port",
             "sample": f"contiguous slice [0, {n_cfg}) of {space_name}, k={len(oens.nets)}, top-{m}, "
                       f"float64 numpy/OpenBLAS ({cores} threads for BLAS), {dt:.1f} s",
             "seconds": dt}
+
+
+def train_bench(space_name, with_cpu=True):
+    """Ensemble training (latency-bound, reported as wall
+    time): the device trainer on the 2000-sample stage-1 fixture of the
+    workload, all k members concurrently, vs one member of the reference
+    trainer (oracle `_fit`, the reference's numpy code path) on the host."""
+    import paper_1506_00842_b200 as b
+    from paper_1506_00842_b200.space import space_from_json
+    spaces = json.loads((GOLDEN / "spaces.json").read_text())
+    sp = space_from_json(spaces[space_name])
+    k = 16 if space_name == "synthetic-1e8" else 8
+    st = np.load(GOLDEN / f"stage1_{space_name}.npz")
+    samples = b.SampleSet(sp, "golden", tuple(
+        b.Sample(sp.config_at(int(i)), b.Outcome.valid(float(t)) if ok else b.Outcome.invalid("invalid-launch"))
+        for i, ok, t in zip(st["idx"], st["ok"], st["time"])))
+    b.train_ensemble(samples, sp, k=k, cfg=b.TrainConfig(seed=0, epochs=5))        # warm-up
+    t0 = time.perf_counter()
+    ens = b.train_ensemble(samples, sp, k=k, cfg=b.TrainConfig(seed=0))
+    dev_s = time.perf_counter() - t0
+    out = {"k": k, "epochs": 500, "samples_valid": int(st["ok"].sum()), "device_wall_s": dev_s,
+           "final_losses_mean": float(np.mean([m.final_epoch_loss for m in ens.members]))}
+    if with_cpu:
+        from oracle.model import OTrainCfg, fold_rows, fit
+        from oracle.space import space_from_doc
+        osp = space_from_doc(spaces[space_name])
+        X = osp.encode(st["idx"][st["ok"]])
+        y = np.log(st["time"][st["ok"]])
+        rows = fold_rows(X.shape[0], k, 0)[0]
+        t0 = time.perf_counter()
+        fit(X[rows], y[rows], OTrainCfg(seed=0), (0, 0))
+        cpu_member = time.perf_counter() - t0
+        out["cpu_reference_s_per_member"] = cpu_member
+        out["cpu_reference_s_all_members_sequential"] = cpu_member * k
+        out["speedup_vs_sequential_cpu"] = cpu_member * k / dev_s
+    return out
 
 
 def run_reference(args, rank):
@@ -155,7 +206,7 @@ def run_reference(args, rank):
         if s >= args.warmup:
             secs += time.perf_counter() - t0
     value = n_cfg * args.steps / secs
-    cores = len(os.sched_getaffinity(0))
+    cores = blas_threads()
     cb = {"value": value, "unit": "configs/s", "cores": cores, "kind": "port",
           "sample": f"{args.steps} contiguous slices of {n_cfg} configs of {args.workload}, k={len(oens.nets)}, "
                     f"top-{M_TOP}, float64 numpy/OpenBLAS ({cores} threads for BLAS)"}
@@ -179,6 +230,9 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 19)
     ap.add_argument("--cpu-sample", type=int, default=1 << 21)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the training measurement")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collective backend for N>1 (gloo: functional runs with ranks sharing one GPU)")
     ap.add_argument("--no-peaks", action="store_true", help="skip the live FFMA/MUFU microbenchmark (ncu runs)")
     args = ap.parse_args()
 
@@ -190,9 +244,13 @@ def main():
 
     import torch
     import torch.distributed as dist
+    local = local % max(torch.cuda.device_count(), 1)      # ranks may share a GPU in functional runs
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_1506_00842_b200 import _native as N
     from paper_1506_00842_b200 import distributed as D
     from paper_1506_00842_b200 import tuner as T
@@ -223,11 +281,12 @@ def main():
             n = out_n.value
             gi[:n] = torch.from_numpy(out_i[:n])
             gp[:n] = torch.from_numpy(out_p[:n])
-            ai = torch.empty(world * M_TOP, dtype=torch.int64, device="cuda")
-            ap_ = torch.empty(world * M_TOP, dtype=torch.float64, device="cuda")
-            dist.all_gather_into_tensor(ai, gi.cuda(), )
-            dist.all_gather_into_tensor(ap_, gp.cuda())
-            return D._device_merge(ai, ap_, M_TOP)
+            dev = "cuda" if args.backend == "nccl" else "cpu"
+            ai = torch.empty(world * M_TOP, dtype=torch.int64, device=dev)
+            ap_ = torch.empty(world * M_TOP, dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(ai, gi.to(dev))
+            dist.all_gather_into_tensor(ap_, gp.to(dev))
+            return D._device_merge(ai.cuda(), ap_.cuda(), M_TOP)
         return out_i[: out_n.value], out_p[: out_n.value]
 
     for _ in range(args.warmup):
@@ -325,6 +384,8 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.workload, M_TOP, args.cpu_sample)
             line["cpu_baseline"].pop("seconds")
+        if world == 1 and not args.no_train:
+            line["train"] = train_bench(args.workload, with_cpu=not args.no_cpu_baseline)
         print(json.dumps(line), flush=True)
     N.lib().mlt_plan_destroy(plan)
     if world > 1:

@@ -65,6 +65,8 @@ def top_m_arrays_sharded(ensemble, space, m: int, group=None, local_fn=None, mer
     dist.all_gather_into_tensor(gp, lp, group=group)
     if merge_fn is not None:
         return merge_fn(gi.cpu().numpy(), gp.cpu().numpy(), m)
+    if not gi.is_cuda:          # CPU-side collective (gloo): the merge still runs on this rank's B200
+        gi, gp = gi.cuda(), gp.cuda()
     return _device_merge(gi, gp, m)
 
 
