@@ -199,6 +199,28 @@ MLT_API int mlt_train_members(mlt_ctx* ctx, const mlt_train_desc* desc, double* 
                       double* w2, double* b2, double* loss_first, double* loss_final,
                       int32_t* diverged_epoch);
 
+/* ---------------------------------------------------------------------------
+ * Benchmark kernels behind the runner protocol (the
+ * reference has only the seam: ExternalRunner / runner.measure,
+ * measurement.py:274-348, tuner.py:80-92). The paper's 5x5 box-filter
+ * convolution (Tables 1-2) with its knobs realised on sm_100a.
+ * ------------------------------------------------------------------------- */
+typedef struct mlt_convbench mlt_convbench;
+
+/* Device-resident W x H fp32 image: `image` (host, W*H floats) or, when NULL,
+ * uniform [0,1) from a splitmix64 hash of (seed, pixel index). */
+MLT_API int mlt_convbench_create(int device, int32_t width, int32_t height, const float* image, uint64_t seed,
+                                 mlt_convbench** out);
+MLT_API int mlt_convbench_destroy(mlt_convbench* bench);
+/* knobs[9] = {wg_x, wg_y, ppt_x, ppt_y, use_image, use_local, padding, interleaved, unroll}.
+ * *status: 0 valid, 1 invalid-launch (Outcome "invalid-launch"). *seconds: min over reps. */
+MLT_API int mlt_convbench_run(mlt_convbench* bench, const int32_t* knobs, int32_t reps, double* seconds,
+                              int32_t* status);
+/* Output of the last run / the input image, W*H floats (host). */
+MLT_API int mlt_convbench_output(mlt_convbench* bench, float* host_out);
+MLT_API int mlt_convbench_input(mlt_convbench* bench, float* host_in);
+MLT_API const char* mlt_convbench_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

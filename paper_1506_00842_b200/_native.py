@@ -82,6 +82,13 @@ _SIGNATURES = [
     ("mlt_merge_top_m", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _i64p, _f64p, _i64p]),
     ("mlt_train_members", C.c_int, [C.c_void_p, C.POINTER(MltTrainDesc), _f64p, _f64p, _f64p, _f64p, _f64p,
                                      _f64p, _i32p]),
+    ("mlt_convbench_create", C.c_int, [C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_float), C.c_uint64,
+                                       C.POINTER(C.c_void_p)]),
+    ("mlt_convbench_destroy", C.c_int, [C.c_void_p]),
+    ("mlt_convbench_run", C.c_int, [C.c_void_p, _i32p, C.c_int32, _f64p, _i32p]),
+    ("mlt_convbench_output", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("mlt_convbench_input", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("mlt_convbench_last_error", C.c_char_p, []),
 ]
 EXPORTS = tuple(name for name, _, _ in _SIGNATURES)
 

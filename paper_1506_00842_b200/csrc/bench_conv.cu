@@ -1,0 +1,316 @@
+// bench_conv.cu — the paper's tunable 2D convolution benchmark (SURVEY §8(a)
+// A13, §8(f) next #1; Tables 1-2: 5x5 box filter over a 2D image),
+// written for sm_100a behind the runner protocol (measurement.py:250-258):
+//
+//   knob             realisation on the B200
+//   wg_x, wg_y       CTA shape (wg_x*wg_y > 1024 -> invalid-launch)
+//   ppt_x, ppt_y     output pixels per thread in x / y
+//   use_image        input read through a texture object (point sampling, clamp addressing)
+//   use_local        the CTA's input tile + 2-pixel halo staged in shared memory
+//                    (tile > 227 KB -> invalid-launch)
+//   padding          input pre-padded by 2 replicated pixels: no clamping in the kernel
+//   interleaved      a thread's pixels are strided by the CTA width (coalesced) instead of contiguous
+//   unroll           the 5x5 filter loops fully unrolled
+//
+// Every variant sums the 25 taps in the same (dy, dx) order in fp32 and
+// divides by 25, so all 32 variants produce bit-identical images, equal to
+// the numpy float32 golden of tests/ (clamp-to-edge borders).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "mltune_b200.h"
+
+namespace mlt {
+
+struct ConvArgs {
+  int W, H;
+  const float* in;        // W x H, or (W+4) x (H+4) when padded
+  int pitch;              // row pitch (elements) of `in`
+  cudaTextureObject_t tex;
+  float* out;             // W x H
+  int pptx, ppty;
+};
+
+template <bool IMG, bool PAD>
+__device__ __forceinline__ float fetch(const ConvArgs& a, int y, int x) {
+  // y, x may lie up to 2 pixels outside the image
+  if (PAD) {
+    if (IMG) return tex2D<float>(a.tex, (float)(x + 2) + 0.5f, (float)(y + 2) + 0.5f);
+    return __ldg(a.in + (size_t)(y + 2) * a.pitch + (x + 2));
+  }
+  if (IMG) return tex2D<float>(a.tex, (float)x + 0.5f, (float)y + 0.5f);   // clamp addressing
+  const int yy = min(max(y, 0), a.H - 1), xx = min(max(x, 0), a.W - 1);
+  return __ldg(a.in + (size_t)yy * a.pitch + xx);
+}
+
+template <bool IMG, bool LOCAL, bool PAD, bool INTER, bool UNROLL>
+__global__ void k_conv5(ConvArgs a) {
+  extern __shared__ float tile[];
+  const int wgx = blockDim.x, wgy = blockDim.y;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int bw = wgx * a.pptx, bh = wgy * a.ppty;           // output pixels per CTA
+  const int X0 = blockIdx.x * bw, Y0 = blockIdx.y * bh;
+  const int tw = bw + 4;
+  if (LOCAL) {
+    const int th = bh + 4;
+    for (int q = ty * wgx + tx; q < tw * th; q += wgx * wgy) {
+      const int r = q / tw, c = q - r * tw;
+      // rows/cols past the image's 2-pixel halo feed no valid output: clamp them in range
+      tile[q] = fetch<IMG, PAD>(a, min(Y0 - 2 + r, a.H + 1), min(X0 - 2 + c, a.W + 1));
+    }
+    __syncthreads();
+  }
+  for (int iy = 0; iy < a.ppty; ++iy) {
+    const int ly = INTER ? iy * wgy + ty : ty * a.ppty + iy;   // row within the CTA's output block
+    const int y = Y0 + ly;
+    if (y >= a.H) continue;
+    for (int ix = 0; ix < a.pptx; ++ix) {
+      const int lx = INTER ? ix * wgx + tx : tx * a.pptx + ix;
+      const int x = X0 + lx;
+      if (x >= a.W) continue;
+      float s = 0.0f;
+      if (UNROLL) {
+#pragma unroll
+        for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
+          for (int dx = -2; dx <= 2; ++dx)
+            s += LOCAL ? tile[(ly + 2 + dy) * tw + (lx + 2 + dx)] : fetch<IMG, PAD>(a, y + dy, x + dx);
+      } else {
+#pragma unroll 1
+        for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll 1
+          for (int dx = -2; dx <= 2; ++dx)
+            s += LOCAL ? tile[(ly + 2 + dy) * tw + (lx + 2 + dx)] : fetch<IMG, PAD>(a, y + dy, x + dx);
+      }
+      a.out[(size_t)y * a.W + x] = s / 25.0f;
+    }
+  }
+}
+
+typedef void (*ConvKernel)(ConvArgs);
+
+#define MLT_CONV_ENTRY(i)                                                                              \
+  k_conv5<((i) >> 4) & 1, ((i) >> 3) & 1, ((i) >> 2) & 1, ((i) >> 1) & 1, (i) & 1>
+static const ConvKernel kConvKernels[32] = {
+    MLT_CONV_ENTRY(0),  MLT_CONV_ENTRY(1),  MLT_CONV_ENTRY(2),  MLT_CONV_ENTRY(3),  MLT_CONV_ENTRY(4),
+    MLT_CONV_ENTRY(5),  MLT_CONV_ENTRY(6),  MLT_CONV_ENTRY(7),  MLT_CONV_ENTRY(8),  MLT_CONV_ENTRY(9),
+    MLT_CONV_ENTRY(10), MLT_CONV_ENTRY(11), MLT_CONV_ENTRY(12), MLT_CONV_ENTRY(13), MLT_CONV_ENTRY(14),
+    MLT_CONV_ENTRY(15), MLT_CONV_ENTRY(16), MLT_CONV_ENTRY(17), MLT_CONV_ENTRY(18), MLT_CONV_ENTRY(19),
+    MLT_CONV_ENTRY(20), MLT_CONV_ENTRY(21), MLT_CONV_ENTRY(22), MLT_CONV_ENTRY(23), MLT_CONV_ENTRY(24),
+    MLT_CONV_ENTRY(25), MLT_CONV_ENTRY(26), MLT_CONV_ENTRY(27), MLT_CONV_ENTRY(28), MLT_CONV_ENTRY(29),
+    MLT_CONV_ENTRY(30), MLT_CONV_ENTRY(31)};
+
+// deterministic synthetic image: uniform [0, 1) from a splitmix64 hash of (seed, pixel)
+__global__ void k_fill_image(float* img, int W, int H, uint64_t seed) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)W * H;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(q + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    img[q] = (float)((double)(z >> 40) * (1.0 / 16777216.0));
+  }
+}
+
+// padded copy with 2 replicated border pixels
+__global__ void k_pad_image(const float* img, float* pad, int W, int H) {
+  const int pw = W + 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)pw * (H + 4);
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(q / pw), c = (int)(q % pw);
+    const int y = min(max(r - 2, 0), H - 1), x = min(max(c - 2, 0), W - 1);
+    pad[q] = img[(size_t)y * W + x];
+  }
+}
+
+__global__ void k_flush_l2(uint4* buf, size_t n, uint32_t v) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x)
+    buf[q] = make_uint4(v, v, v, v);
+}
+
+}  // namespace mlt
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+struct mlt_convbench {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int W = 0, H = 0;
+  float* img = nullptr;
+  float* pad = nullptr;
+  float* out = nullptr;
+  cudaArray_t arr = nullptr, arr_pad = nullptr;
+  cudaTextureObject_t tex = 0, tex_pad = 0;
+  void* flush = nullptr;
+  size_t flush_n = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+thread_local std::string g_cerr;
+int cfail(int code, const std::string& msg) {
+  g_cerr = msg;
+  return code;
+}
+#define CK(expr)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return cfail(MLT_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+int make_texture(const float* src, int w, int h, cudaArray_t* arr, cudaTextureObject_t* tex, cudaStream_t s) {
+  cudaChannelFormatDesc cd = cudaCreateChannelDesc<float>();
+  CK(cudaMallocArray(arr, &cd, w, h));
+  CK(cudaMemcpy2DToArrayAsync(*arr, 0, 0, src, (size_t)w * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
+  cudaResourceDesc rd;
+  std::memset(&rd, 0, sizeof rd);
+  rd.resType = cudaResourceTypeArray;
+  rd.res.array.array = *arr;
+  cudaTextureDesc td;
+  std::memset(&td, 0, sizeof td);
+  td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+  td.filterMode = cudaFilterModePoint;          // hardware linear filtering would lose precision
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  CK(cudaCreateTextureObject(tex, &rd, &td, nullptr));
+  return MLT_OK;
+}
+}  // namespace
+
+extern "C" {
+
+MLT_API const char* mlt_convbench_last_error(void) { return g_cerr.c_str(); }
+
+MLT_API int mlt_convbench_create(int device, int32_t width, int32_t height, const float* image, uint64_t seed,
+                                 mlt_convbench** out) {
+  using namespace mlt;
+  if (!out) return cfail(MLT_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (width < 1 || height < 1 || width > 32768 || height > 32768) return cfail(MLT_EINVAL, "bad image size");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return cfail(MLT_ECUDA, "no CUDA device (no CPU fallback)");
+  CK(cudaSetDevice(device));
+  mlt_convbench* b = new mlt_convbench();
+  b->dev = device;
+  b->W = width;
+  b->H = height;
+  CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  const size_t px = (size_t)width * height;
+  CK(cudaMalloc(&b->img, px * 4));
+  CK(cudaMalloc(&b->out, px * 4));
+  CK(cudaMalloc(&b->pad, (size_t)(width + 4) * (height + 4) * 4));
+  if (image) {
+    CK(cudaMemcpyAsync(b->img, image, px * 4, cudaMemcpyHostToDevice, b->stream));
+  } else {
+    k_fill_image<<<1024, 256, 0, b->stream>>>(b->img, width, height, seed);
+  }
+  k_pad_image<<<1024, 256, 0, b->stream>>>(b->img, b->pad, width, height);
+  CK(cudaGetLastError());
+  int rc = make_texture(b->img, width, height, &b->arr, &b->tex, b->stream);
+  if (rc == MLT_OK) rc = make_texture(b->pad, width + 4, height + 4, &b->arr_pad, &b->tex_pad, b->stream);
+  if (rc != MLT_OK) return rc;
+  b->flush_n = (size_t)(256u << 20) / 16;           // 256 MiB > 126 MB L2
+  CK(cudaMalloc(&b->flush, b->flush_n * 16));
+  CK(cudaEventCreate(&b->e0));
+  CK(cudaEventCreate(&b->e1));
+  CK(cudaStreamSynchronize(b->stream));
+  *out = b;
+  return MLT_OK;
+}
+
+MLT_API int mlt_convbench_destroy(mlt_convbench* b) {
+  if (!b) return MLT_OK;
+  cudaSetDevice(b->dev);
+  cudaStreamSynchronize(b->stream);
+  cudaDestroyTextureObject(b->tex);
+  cudaDestroyTextureObject(b->tex_pad);
+  cudaFreeArray(b->arr);
+  cudaFreeArray(b->arr_pad);
+  cudaFree(b->img);
+  cudaFree(b->pad);
+  cudaFree(b->out);
+  cudaFree(b->flush);
+  cudaEventDestroy(b->e0);
+  cudaEventDestroy(b->e1);
+  cudaStreamDestroy(b->stream);
+  delete b;
+  return MLT_OK;
+}
+
+// knobs = {wg_x, wg_y, ppt_x, ppt_y, use_image, use_local, padding, interleaved, unroll}
+// (the convolution space's parameter order, paramspace.py:287-310). status: 0 = valid,
+// 1 = invalid-launch. seconds = min over `reps` runs, each after an L2 flush.
+MLT_API int mlt_convbench_run(mlt_convbench* b, const int32_t* knobs, int32_t reps, double* seconds, int32_t* status) {
+  using namespace mlt;
+  if (!b || !knobs || !seconds || !status) return cfail(MLT_EINVAL, "NULL argument");
+  if (reps < 1) return cfail(MLT_EINVAL, "repetitions must be >= 1");
+  CK(cudaSetDevice(b->dev));
+  const int wgx = knobs[0], wgy = knobs[1], pptx = knobs[2], ppty = knobs[3];
+  const bool img = knobs[4], local = knobs[5], pad = knobs[6], inter = knobs[7], unroll = knobs[8];
+  *status = 0;
+  *seconds = 0;
+  if (wgx < 1 || wgy < 1 || pptx < 1 || ppty < 1) return cfail(MLT_EINVAL, "non-positive knob");
+  const int64_t bw = (int64_t)wgx * pptx, bh = (int64_t)wgy * ppty;
+  const int64_t gx = (b->W + bw - 1) / bw, gy = (b->H + bh - 1) / bh;
+  const size_t smem = local ? (size_t)(bw + 4) * (size_t)(bh + 4) * 4 : 0;
+  if ((int64_t)wgx * wgy > 1024 || wgy > 1024 || smem > 227 * 1024 || gy > 65535) {
+    *status = 1;                                     // cannot launch on this device
+    return MLT_OK;
+  }
+  const int sel = (img << 4) | (local << 3) | (pad << 2) | (inter << 1) | (int)unroll;
+  ConvKernel k = kConvKernels[sel];
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ConvArgs a;
+  a.W = b->W;
+  a.H = b->H;
+  a.in = pad ? b->pad : b->img;
+  a.pitch = pad ? b->W + 4 : b->W;
+  a.tex = pad ? b->tex_pad : b->tex;
+  a.out = b->out;
+  a.pptx = pptx;
+  a.ppty = ppty;
+  double best = 1e30;
+  for (int r = 0; r < reps; ++r) {
+    k_flush_l2<<<1024, 256, 0, b->stream>>>(static_cast<uint4*>(b->flush), b->flush_n, (uint32_t)r);
+    CK(cudaEventRecord(b->e0, b->stream));
+    k<<<dim3((unsigned)gx, (unsigned)gy), dim3(wgx, wgy), smem, b->stream>>>(a);
+    const cudaError_t le = cudaGetLastError();
+    if (le == cudaErrorInvalidConfiguration || le == cudaErrorLaunchOutOfResources) {
+      *status = 1;
+      return MLT_OK;
+    }
+    if (le != cudaSuccess) return cfail(MLT_ECUDA, std::string("conv launch: ") + cudaGetErrorString(le));
+    CK(cudaEventRecord(b->e1, b->stream));
+    CK(cudaEventSynchronize(b->e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, b->e0, b->e1));
+    b->launches += 2;
+    if (ms * 1e-3 < best) best = ms * 1e-3;
+  }
+  *seconds = best;
+  return MLT_OK;
+}
+
+MLT_API int mlt_convbench_output(mlt_convbench* b, float* host_out) {
+  if (!b || !host_out) return cfail(MLT_EINVAL, "NULL argument");
+  CK(cudaSetDevice(b->dev));
+  CK(cudaMemcpyAsync(host_out, b->out, (size_t)b->W * b->H * 4, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return MLT_OK;
+}
+
+MLT_API int mlt_convbench_input(mlt_convbench* b, float* host_in) {
+  if (!b || !host_in) return cfail(MLT_EINVAL, "NULL argument");
+  CK(cudaSetDevice(b->dev));
+  CK(cudaMemcpyAsync(host_in, b->img, (size_t)b->W * b->H * 4, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return MLT_OK;
+}
+
+}  // extern "C"
