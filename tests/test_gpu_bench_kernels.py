@@ -32,6 +32,10 @@ def test_conv_variants_bit_exact(conv_runner, flags):
                     ((64, 16), (8, 32)), ((2, 2), (128, 128))):   # CTA blocks larger than the image
         cfg = (wg[0], wg[1], ppt[0], ppt[1]) + tuple(flags)
         t, ok = r.run(cfg, 1)
+        tile = (wg[0] * ppt[0] + 4) * (wg[1] * ppt[1] + 4) * 4
+        if flags[1] and tile > 227 * 1024:       # use_local tile cannot fit: invalid-launch
+            assert not ok
+            continue
         assert ok, cfg
         out = r.output()
         assert np.array_equal(out, gold), (cfg, np.abs(out - gold).max())
