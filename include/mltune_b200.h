@@ -202,8 +202,8 @@ MLT_API int mlt_train_members(mlt_ctx* ctx, const mlt_train_desc* desc, double* 
 /* ---------------------------------------------------------------------------
  * Benchmark kernels behind the runner protocol (the
  * reference has only the seam: ExternalRunner / runner.measure,
- * measurement.py:274-348, tuner.py:80-92). The paper's 5x5 box-filter
- * convolution (Tables 1-2) with its knobs realised on sm_100a.
+ * measurement.py:274-348, tuner.py:80-92). The paper's three benchmarks
+ * (Tables 1-2) with their knobs realised on sm_100a.
  * ------------------------------------------------------------------------- */
 typedef struct mlt_convbench mlt_convbench;
 
@@ -220,6 +220,42 @@ MLT_API int mlt_convbench_run(mlt_convbench* bench, const int32_t* knobs, int32_
 MLT_API int mlt_convbench_output(mlt_convbench* bench, float* host_out);
 MLT_API int mlt_convbench_input(mlt_convbench* bench, float* host_in);
 MLT_API const char* mlt_convbench_last_error(void);
+
+/* Stereo matching (Tables 1-2; bench_stereo.cu): winner-take-all SAD
+ * disparity over D disparities and a (2R+1)^2 window, 8-bit W x H images.
+ * `left`/`right` (host, W*H bytes each) or, when both NULL, a synthetic pair
+ * (random right image; left = right shifted by a piecewise-constant disparity
+ * field + noise) from `seed`. */
+typedef struct mlt_stereobench mlt_stereobench;
+MLT_API int mlt_stereobench_create(int device, int32_t width, int32_t height, int32_t disparities, int32_t radius,
+                                   const uint8_t* left, const uint8_t* right, uint64_t seed, mlt_stereobench** out);
+MLT_API int mlt_stereobench_destroy(mlt_stereobench* bench);
+/* knobs[11] = {wg_x, wg_y, ppt_x, ppt_y, img_left, img_right, local_left, local_right,
+ *              unroll_disparity, unroll_diff_x, unroll_diff_y}; status/seconds as for conv. */
+MLT_API int mlt_stereobench_run(mlt_stereobench* bench, const int32_t* knobs, int32_t reps, double* seconds,
+                                int32_t* status);
+MLT_API int mlt_stereobench_output(mlt_stereobench* bench, uint8_t* host_disparity);
+MLT_API int mlt_stereobench_input(mlt_stereobench* bench, uint8_t* host_left, uint8_t* host_right);
+MLT_API const char* mlt_stereobench_last_error(void);
+
+/* Volume raycasting (Tables 1-2; bench_raycast.cu): an image_w x
+ * image_h RGBA fp32 image from a vx x vy x vz 8-bit volume (x fastest) with a
+ * 256-entry RGBA transfer function, orthographic rays, front-to-back
+ * compositing. `volume` / `transfer` (host) or NULL for the synthetic
+ * volume (from `seed`) / the default transfer function. */
+typedef struct mlt_raybench mlt_raybench;
+MLT_API int mlt_raybench_create(int device, int32_t image_w, int32_t image_h, int32_t vx, int32_t vy, int32_t vz,
+                                const uint8_t* volume, const float* transfer, uint64_t seed, mlt_raybench** out);
+MLT_API int mlt_raybench_destroy(mlt_raybench* bench);
+/* knobs[10] = {wg_x, wg_y, ppt_x, ppt_y, img_data, img_transfer, local_transfer, const_transfer,
+ *              interleaved, unroll_ray}; status/seconds as for conv. */
+MLT_API int mlt_raybench_run(mlt_raybench* bench, const int32_t* knobs, int32_t reps, double* seconds, int32_t* status);
+MLT_API int mlt_raybench_output(mlt_raybench* bench, float* host_rgba);
+MLT_API int mlt_raybench_volume(mlt_raybench* bench, uint8_t* host_volume);
+MLT_API int mlt_raybench_transfer(mlt_raybench* bench, float* host_rgba256);
+/* 19 floats: centre[3], u[3], v[3], dir[3], 1/dir[3], scale, width/2, height/2, opacity threshold */
+MLT_API int mlt_raybench_camera(mlt_raybench* bench, float* host_cam19);
+MLT_API const char* mlt_raybench_last_error(void);
 
 #ifdef __cplusplus
 }

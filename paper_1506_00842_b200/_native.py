@@ -89,6 +89,22 @@ _SIGNATURES = [
     ("mlt_convbench_output", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ("mlt_convbench_input", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ("mlt_convbench_last_error", C.c_char_p, []),
+    ("mlt_stereobench_create", C.c_int, [C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _u8p, _u8p,
+                                         C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("mlt_stereobench_destroy", C.c_int, [C.c_void_p]),
+    ("mlt_stereobench_run", C.c_int, [C.c_void_p, _i32p, C.c_int32, _f64p, _i32p]),
+    ("mlt_stereobench_output", C.c_int, [C.c_void_p, _u8p]),
+    ("mlt_stereobench_input", C.c_int, [C.c_void_p, _u8p, _u8p]),
+    ("mlt_stereobench_last_error", C.c_char_p, []),
+    ("mlt_raybench_create", C.c_int, [C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _u8p,
+                                      C.POINTER(C.c_float), C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("mlt_raybench_destroy", C.c_int, [C.c_void_p]),
+    ("mlt_raybench_run", C.c_int, [C.c_void_p, _i32p, C.c_int32, _f64p, _i32p]),
+    ("mlt_raybench_output", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("mlt_raybench_volume", C.c_int, [C.c_void_p, _u8p]),
+    ("mlt_raybench_transfer", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("mlt_raybench_camera", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("mlt_raybench_last_error", C.c_char_p, []),
 ]
 EXPORTS = tuple(name for name, _, _ in _SIGNATURES)
 

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <string>
 
+#include "bench_common.cuh"
 #include "mltune_b200.h"
 
 namespace mlt {
@@ -106,13 +107,8 @@ static const ConvKernel kConvKernels[32] = {
 // deterministic synthetic image: uniform [0, 1) from a splitmix64 hash of (seed, pixel)
 __global__ void k_fill_image(float* img, int W, int H, uint64_t seed) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < (int64_t)W * H;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(q + 1);
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    z ^= z >> 31;
-    img[q] = (float)((double)(z >> 40) * (1.0 / 16777216.0));
-  }
+       q += (int64_t)gridDim.x * blockDim.x)
+    img[q] = (float)((double)(bench::hash_at(seed, (uint64_t)q) >> 40) * (1.0 / 16777216.0));
 }
 
 // padded copy with 2 replicated border pixels
@@ -124,11 +120,6 @@ __global__ void k_pad_image(const float* img, float* pad, int W, int H) {
     const int y = min(max(r - 2, 0), H - 1), x = min(max(c - 2, 0), W - 1);
     pad[q] = img[(size_t)y * W + x];
   }
-}
-
-__global__ void k_flush_l2(uint4* buf, size_t n, uint32_t v) {
-  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x)
-    buf[q] = make_uint4(v, v, v, v);
 }
 
 }  // namespace mlt
@@ -145,56 +136,26 @@ struct mlt_convbench {
   float* out = nullptr;
   cudaArray_t arr = nullptr, arr_pad = nullptr;
   cudaTextureObject_t tex = 0, tex_pad = 0;
-  void* flush = nullptr;
-  size_t flush_n = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  int64_t launches = 0;
-  std::string err;
+  mlt::bench::Timer timer;
 };
 
 namespace {
-thread_local std::string g_cerr;
-int cfail(int code, const std::string& msg) {
-  g_cerr = msg;
-  return code;
-}
-#define CK(expr)                                                                           \
-  do {                                                                                     \
-    cudaError_t e_ = (expr);                                                               \
-    if (e_ != cudaSuccess) return cfail(MLT_ECUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
-  } while (0)
-
-int make_texture(const float* src, int w, int h, cudaArray_t* arr, cudaTextureObject_t* tex, cudaStream_t s) {
-  cudaChannelFormatDesc cd = cudaCreateChannelDesc<float>();
-  CK(cudaMallocArray(arr, &cd, w, h));
-  CK(cudaMemcpy2DToArrayAsync(*arr, 0, 0, src, (size_t)w * 4, (size_t)w * 4, h, cudaMemcpyDeviceToDevice, s));
-  cudaResourceDesc rd;
-  std::memset(&rd, 0, sizeof rd);
-  rd.resType = cudaResourceTypeArray;
-  rd.res.array.array = *arr;
-  cudaTextureDesc td;
-  std::memset(&td, 0, sizeof td);
-  td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
-  td.filterMode = cudaFilterModePoint;          // hardware linear filtering would lose precision
-  td.readMode = cudaReadModeElementType;
-  td.normalizedCoords = 0;
-  CK(cudaCreateTextureObject(tex, &rd, &td, nullptr));
-  return MLT_OK;
-}
+thread_local mlt::bench::ErrSlot g_cerr;
+#define CK(expr) MLT_BENCH_CK(g_cerr, expr)
 }  // namespace
 
 extern "C" {
 
-MLT_API const char* mlt_convbench_last_error(void) { return g_cerr.c_str(); }
+MLT_API const char* mlt_convbench_last_error(void) { return g_cerr.msg.c_str(); }
 
 MLT_API int mlt_convbench_create(int device, int32_t width, int32_t height, const float* image, uint64_t seed,
                                  mlt_convbench** out) {
   using namespace mlt;
-  if (!out) return cfail(MLT_EINVAL, "out is NULL");
+  if (!out) return g_cerr.fail(MLT_EINVAL, "out is NULL");
   *out = nullptr;
-  if (width < 1 || height < 1 || width > 32768 || height > 32768) return cfail(MLT_EINVAL, "bad image size");
+  if (width < 1 || height < 1 || width > 32768 || height > 32768) return g_cerr.fail(MLT_EINVAL, "bad image size");
   int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return cfail(MLT_ECUDA, "no CUDA device (no CPU fallback)");
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return g_cerr.fail(MLT_ECUDA, "no CUDA device (no CPU fallback)");
   CK(cudaSetDevice(device));
   mlt_convbench* b = new mlt_convbench();
   b->dev = device;
@@ -212,13 +173,10 @@ MLT_API int mlt_convbench_create(int device, int32_t width, int32_t height, cons
   }
   k_pad_image<<<1024, 256, 0, b->stream>>>(b->img, b->pad, width, height);
   CK(cudaGetLastError());
-  int rc = make_texture(b->img, width, height, &b->arr, &b->tex, b->stream);
-  if (rc == MLT_OK) rc = make_texture(b->pad, width + 4, height + 4, &b->arr_pad, &b->tex_pad, b->stream);
+  int rc = bench::make_texture_2d(g_cerr, b->img, width, height, &b->arr, &b->tex, b->stream);
+  if (rc == MLT_OK) rc = bench::make_texture_2d(g_cerr, b->pad, width + 4, height + 4, &b->arr_pad, &b->tex_pad, b->stream);
+  if (rc == MLT_OK) rc = b->timer.init(g_cerr, b->stream);
   if (rc != MLT_OK) return rc;
-  b->flush_n = (size_t)(256u << 20) / 16;           // 256 MiB > 126 MB L2
-  CK(cudaMalloc(&b->flush, b->flush_n * 16));
-  CK(cudaEventCreate(&b->e0));
-  CK(cudaEventCreate(&b->e1));
   CK(cudaStreamSynchronize(b->stream));
   *out = b;
   return MLT_OK;
@@ -235,9 +193,7 @@ MLT_API int mlt_convbench_destroy(mlt_convbench* b) {
   cudaFree(b->img);
   cudaFree(b->pad);
   cudaFree(b->out);
-  cudaFree(b->flush);
-  cudaEventDestroy(b->e0);
-  cudaEventDestroy(b->e1);
+  b->timer.release();
   cudaStreamDestroy(b->stream);
   delete b;
   return MLT_OK;
@@ -248,18 +204,18 @@ MLT_API int mlt_convbench_destroy(mlt_convbench* b) {
 // 1 = invalid-launch. seconds = min over `reps` runs, each after an L2 flush.
 MLT_API int mlt_convbench_run(mlt_convbench* b, const int32_t* knobs, int32_t reps, double* seconds, int32_t* status) {
   using namespace mlt;
-  if (!b || !knobs || !seconds || !status) return cfail(MLT_EINVAL, "NULL argument");
-  if (reps < 1) return cfail(MLT_EINVAL, "repetitions must be >= 1");
+  if (!b || !knobs || !seconds || !status) return g_cerr.fail(MLT_EINVAL, "NULL argument");
+  if (reps < 1) return g_cerr.fail(MLT_EINVAL, "repetitions must be >= 1");
   CK(cudaSetDevice(b->dev));
   const int wgx = knobs[0], wgy = knobs[1], pptx = knobs[2], ppty = knobs[3];
   const bool img = knobs[4], local = knobs[5], pad = knobs[6], inter = knobs[7], unroll = knobs[8];
   *status = 0;
   *seconds = 0;
-  if (wgx < 1 || wgy < 1 || pptx < 1 || ppty < 1) return cfail(MLT_EINVAL, "non-positive knob");
+  if (wgx < 1 || wgy < 1 || pptx < 1 || ppty < 1) return g_cerr.fail(MLT_EINVAL, "non-positive knob");
   const int64_t bw = (int64_t)wgx * pptx, bh = (int64_t)wgy * ppty;
   const int64_t gx = (b->W + bw - 1) / bw, gy = (b->H + bh - 1) / bh;
   const size_t smem = local ? (size_t)(bw + 4) * (size_t)(bh + 4) * 4 : 0;
-  if ((int64_t)wgx * wgy > 1024 || wgy > 1024 || smem > 227 * 1024 || gy > 65535) {
+  if ((int64_t)wgx * wgy > 1024 || wgy > 1024 || smem > bench::kMaxSmem || gy > 65535) {
     *status = 1;                                     // cannot launch on this device
     return MLT_OK;
   }
@@ -275,30 +231,14 @@ MLT_API int mlt_convbench_run(mlt_convbench* b, const int32_t* knobs, int32_t re
   a.out = b->out;
   a.pptx = pptx;
   a.ppty = ppty;
-  double best = 1e30;
-  for (int r = 0; r < reps; ++r) {
-    k_flush_l2<<<1024, 256, 0, b->stream>>>(static_cast<uint4*>(b->flush), b->flush_n, (uint32_t)r);
-    CK(cudaEventRecord(b->e0, b->stream));
+  return b->timer.run(g_cerr, reps, [&]() {
     k<<<dim3((unsigned)gx, (unsigned)gy), dim3(wgx, wgy), smem, b->stream>>>(a);
-    const cudaError_t le = cudaGetLastError();
-    if (le == cudaErrorInvalidConfiguration || le == cudaErrorLaunchOutOfResources) {
-      *status = 1;
-      return MLT_OK;
-    }
-    if (le != cudaSuccess) return cfail(MLT_ECUDA, std::string("conv launch: ") + cudaGetErrorString(le));
-    CK(cudaEventRecord(b->e1, b->stream));
-    CK(cudaEventSynchronize(b->e1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, b->e0, b->e1));
-    b->launches += 2;
-    if (ms * 1e-3 < best) best = ms * 1e-3;
-  }
-  *seconds = best;
-  return MLT_OK;
+    return cudaGetLastError();
+  }, seconds, status);
 }
 
 MLT_API int mlt_convbench_output(mlt_convbench* b, float* host_out) {
-  if (!b || !host_out) return cfail(MLT_EINVAL, "NULL argument");
+  if (!b || !host_out) return g_cerr.fail(MLT_EINVAL, "NULL argument");
   CK(cudaSetDevice(b->dev));
   CK(cudaMemcpyAsync(host_out, b->out, (size_t)b->W * b->H * 4, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
@@ -306,7 +246,7 @@ MLT_API int mlt_convbench_output(mlt_convbench* b, float* host_out) {
 }
 
 MLT_API int mlt_convbench_input(mlt_convbench* b, float* host_in) {
-  if (!b || !host_in) return cfail(MLT_EINVAL, "NULL argument");
+  if (!b || !host_in) return g_cerr.fail(MLT_EINVAL, "NULL argument");
   CK(cudaSetDevice(b->dev));
   CK(cudaMemcpyAsync(host_in, b->img, (size_t)b->W * b->H * 4, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
