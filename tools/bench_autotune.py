@@ -1,0 +1,160 @@
+"""The end-to-end auto-tuning loop (sample -> measure -> train -> predict ->
+re-measure top-M) on one of the B200 benchmark kernels, optionally against
+exhaustive search or a large random-sample baseline.
+
+    BASELINE configs[4]  python tools/bench_autotune.py --bench conv --tune --exhaustive
+    BASELINE configs[2]  python tools/bench_autotune.py --bench raycast --tune --random-best 20000
+    stereo (configs[1])  python tools/bench_autotune.py --bench stereo --tune
+    time distribution    python tools/bench_autotune.py --bench stereo --sample 300
+
+Every measurement is the B200 kernel itself (CUDA events, min over
+repetitions, L2 flushed before each run). Prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_1506_00842_b200 as b  # noqa: E402
+from paper_1506_00842_b200.runners import B200ConvRunner, B200RaycastRunner, B200StereoRunner  # noqa: E402
+
+
+class CachingRunner:
+    """Memoises measure() per configuration so the M values of one seed share
+    their stage-1 measurements (the same seeded sample) instead of re-running
+    them; stage-2 configurations already measured are reused too."""
+
+    def __init__(self, runner):
+        self.runner = runner
+        self.runner_id = runner.runner_id
+        self.default_repetitions = runner.default_repetitions
+        self.cache = {}
+
+    def measure(self, config, repetitions=None):
+        key = (tuple(config), repetitions)
+        if key not in self.cache:
+            self.cache[key] = self.runner.measure(config, repetitions)
+        return self.cache[key]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bench", choices=("conv", "stereo", "raycast"), default="conv")
+    ap.add_argument("--size", type=int, default=0, help="image side (default: 4096 conv, 1024 stereo/raycast)")
+    ap.add_argument("--volume", type=int, default=512, help="raycast volume side")
+    ap.add_argument("--random-best", type=int, default=0,
+                    help="measure this many random configurations as a ground-truth proxy (spaces too large to sweep)")
+    ap.add_argument("--sample", type=int, default=0)
+    ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--exhaustive", action="store_true")
+    ap.add_argument("--n-train", type=int, default=2000)
+    ap.add_argument("--m", type=int, nargs="+", default=[10, 200])
+    ap.add_argument("--seeds", type=int, nargs="+", default=[0])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--budget-s", type=float, default=1800.0, help="stop the exhaustive sweep after this long")
+    ap.add_argument("--rep-cutoff-s", type=float, default=0.05,
+                    help="skip further repetitions after one longer than this (0: always run every repetition)")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+
+    size = args.size or (4096 if args.bench == "conv" else 1024)
+    if args.bench == "conv":
+        space = b.builtin_space("convolution")
+        runner = B200ConvRunner(space, width=size, height=size, seed=0, default_repetitions=args.reps)
+        what = {"experiment": "configs[4]: autotune vs exhaustive, B200 convolution (5x5 box, fp32)"}
+    elif args.bench == "stereo":
+        space = b.builtin_space("stereo")
+        runner = B200StereoRunner(space, width=size, height=size, seed=0, default_repetitions=args.reps)
+        what = {"experiment": "autotune, B200 stereo matching (SAD, D=64, 9x9 window, u8)",
+                "disparities": runner.disparities, "radius": runner.radius}
+    else:
+        space = b.builtin_space("raycasting")
+        v = args.volume
+        runner = B200RaycastRunner(space, width=size, height=size, volume_shape=(v, v, v), seed=0,
+                                   default_repetitions=args.reps)
+        what = {"experiment": "configs[2]: autotune + measured top-N re-benchmark, B200 raycasting",
+                "volume": [v, v, v]}
+    runner.rep_cutoff_s = args.rep_cutoff_s or None
+    res = dict(what, image=[size, size], space=space.name, cardinality=space.cardinality(), reps=args.reps,
+               rep_cutoff_s=runner.rep_cutoff_s)
+
+    if args.sample:
+        rng = np.random.default_rng(1)
+        idx = rng.choice(space.cardinality(), args.sample, replace=False)
+        t0 = time.perf_counter()
+        times, ok = runner.measured_times(idx, 1)
+        res["sample"] = {"n": int(args.sample), "valid": int(ok.sum()), "wall_s": time.perf_counter() - t0,
+                         "ms_quantiles": {q: float(np.nanquantile(times[ok], q) * 1e3) for q in (0, 0.1, 0.5, 0.9, 0.99, 1)},
+                         "ms_mean": float(np.nanmean(times[ok]) * 1e3)}
+
+    if args.tune:
+        res["tune"] = []
+        cached = CachingRunner(runner)
+        for seed in args.seeds:
+            for m in args.m:
+                t0 = time.perf_counter()
+                rep = b.autotune(space, cached, b.TunerConfig(n_train=args.n_train, m_candidates=m, k_bag=11, seed=seed))
+                res["tune"].append({"seed": seed, "m": m, "best_index": rep.best_index, "best_config": rep.best_config,
+                                    "best_time_s": rep.best_time, "predicted_best_s": rep.predicted_best_time,
+                                    "stage2_invalid": rep.stage2_invalid_count, "wall_s": time.perf_counter() - t0})
+
+    if args.random_best:
+        rng = np.random.default_rng(12345)
+        idx = rng.choice(space.cardinality(), args.random_best, replace=False)
+        t0 = time.perf_counter()
+        times, ok = runner.measured_times(idx, 1)
+        order = idx[np.argsort(np.where(ok, times, np.inf))[:20]]
+        best = None
+        for i in order.tolist():
+            tt, good = runner.run(space.config_at(i), args.reps)
+            if good and (best is None or (tt, i) < best):
+                best = (tt, i)
+        res["random_best"] = {"measured": int(args.random_best), "valid": int(ok.sum()),
+                              "wall_s": time.perf_counter() - t0, "best_index": best[1],
+                              "best_config": space.config_at(best[1]), "best_time_s": best[0]}
+        for t in res.get("tune", []):
+            t["slowdown_vs_random_best"] = t["best_time_s"] / best[0]
+
+    if args.exhaustive:
+        card = space.cardinality()
+        t0 = time.perf_counter()
+        times = np.full(card, np.nan)
+        done = 0
+        for s in range(0, card, 4096):
+            idx = np.arange(s, min(s + 4096, card))
+            t, ok = runner.measured_times(idx, 1)
+            times[idx[ok]] = t[ok]
+            done = idx[-1] + 1
+            if time.perf_counter() - t0 > args.budget_s:
+                break
+        wall = time.perf_counter() - t0
+        order = np.argsort(np.where(np.isnan(times), np.inf, times))[:20]
+        # re-measure the 20 fastest with the tuner's repetitions
+        best = None
+        for i in order.tolist():
+            tt, ok = runner.run(space.config_at(i), args.reps)
+            if ok and (best is None or (tt, i) < best):
+                best = (tt, i)
+        res["exhaustive"] = {"measured": int(done), "complete": bool(done == card), "valid": int(np.isfinite(times).sum()),
+                             "wall_s": wall, "best_index": best[1], "best_config": space.config_at(best[1]),
+                             "best_time_s": best[0]}
+        for t in res.get("tune", []):
+            t["slowdown_vs_exhaustive"] = t["best_time_s"] / best[0]
+    runner.close()
+    line = json.dumps(res)
+    print(line)
+    if args.out:
+        Path(args.out).write_text(line + "\n")
+
+
+if __name__ == "__main__":
+    main()
