@@ -14,6 +14,9 @@
  *   mlt_top_m             tuner.top_m_predicted            tuner.py:95-131 (one contiguous slice or an index list)
  *   mlt_merge_top_m       the final lexsort of tuner.py:128-131, applied to per-GPU lists
  *   mlt_train_member(s)   model._fit / train_ensemble      model.py:194-249, :308-341
+ *   mlt_surrogate_times   SurrogateRunner.true_times / measured_times  measurement.py:212-238
+ *   mlt_surrogate_best    exhaustive_search over a surrogate tuner.py:191-224
+ *   mlt_{conv,stereo,ray}bench_*  the paper's benchmark kernels behind runner.measure (measurement.py:250-258)
  *
  * Conventions
  *   - Plain C types only; every pointer argument is HOST memory owned by the
@@ -198,6 +201,43 @@ typedef struct mlt_train_desc {
 MLT_API int mlt_train_members(mlt_ctx* ctx, const mlt_train_desc* desc, double* w1, double* b1,
                       double* w2, double* b2, double* loss_first, double* loss_final,
                       int32_t* diverged_epoch);
+
+/* ---------------------------------------------------------------------------
+ * A12: the analytic surrogate device (SurrogateSpec / SurrogateRunner,
+ * measurement.py:146-238): base time x matching term factors (in spec order),
+ * launch rules -> invalid, frozen log-normal noise from splitmix64 + ndtri.
+ * ------------------------------------------------------------------------- */
+typedef struct mlt_surrogate {
+  double base_time;
+  int32_t n_terms;             /* T */
+  const int32_t* term_nparams; /* [T] 1 or 2 */
+  const int32_t* term_pos;     /* [T][2] parameter positions (second ignored for 1-param terms) */
+  const int64_t* term_match;   /* [T][2] matched VALUES */
+  const double* term_factor;   /* [T] */
+  double log_sigma;            /* sqrt(log1p(noise_cv^2)) as the caller computes it; 0 = no noise */
+  uint64_t seed;
+  int32_t n_rules;             /* launch-failure rules, same encoding as mlt_space */
+  const int32_t* rule_kind;
+  const int32_t* rule_nops;
+  const int32_t* rule_pos;
+  const int64_t* rule_coeff;
+  const int64_t* rule_bound;
+} mlt_surrogate;
+
+/* times[n], ok[n] for configuration indices: reps = 0 -> true_times
+ * (measurement.py:212-226), reps >= 1 -> measured_times(indices, reps)
+ * (:228-238). Times are NaN where a launch rule fires. Static space rules are
+ * NOT applied (as in the reference runner). */
+MLT_API int mlt_surrogate_times(mlt_ctx* ctx, const mlt_space* space, const mlt_surrogate* spec, const int64_t* idx,
+                                int64_t n, int32_t reps, double* times, uint8_t* ok);
+/* Exhaustive search over [begin, end) (tuner.py:191-224): among statically
+ * valid, launchable configurations, the minimum (time, index) with times
+ * measured with `reps` repetitions (0 = noise-free); *n_valid = how many were
+ * measured, *n_below = how many were strictly faster than `threshold` (the
+ * rank of a tuned result). *best_idx = -1 when none is valid. */
+MLT_API int mlt_surrogate_best(mlt_ctx* ctx, const mlt_space* space, const mlt_surrogate* spec, int64_t begin,
+                               int64_t end, int32_t reps, double threshold, int64_t* best_idx, double* best_time,
+                               int64_t* n_valid, int64_t* n_below);
 
 /* ---------------------------------------------------------------------------
  * Benchmark kernels behind the runner protocol (the

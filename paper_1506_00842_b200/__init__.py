@@ -19,6 +19,7 @@ from .model import (Encoder, Ensemble, Network, TrainConfig, forward, gradient, 
                     predict, save_model, train_ensemble, train_network)
 from .tuner import (TunerConfig, TuningReport, autotune, exhaustive_search, measure_configs, top_m_arrays,
                     top_m_predicted)
+from .surrogate import B200SurrogateRunner
 from .install import install, uninstall
 
 __version__ = "0.1.0"

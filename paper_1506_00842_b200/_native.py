@@ -57,6 +57,13 @@ class MltTrainDesc(C.Structure):
                 ("init_w1", _f64p), ("init_w2", _f64p), ("perms", _i32p)]
 
 
+class MltSurrogate(C.Structure):
+    _fields_ = [("base_time", C.c_double), ("n_terms", C.c_int32), ("term_nparams", _i32p), ("term_pos", _i32p),
+                ("term_match", _i64p), ("term_factor", _f64p), ("log_sigma", C.c_double), ("seed", C.c_uint64),
+                ("n_rules", C.c_int32), ("rule_kind", _i32p), ("rule_nops", _i32p), ("rule_pos", _i32p),
+                ("rule_coeff", _i64p), ("rule_bound", _i64p)]
+
+
 # (name, restype, argtypes) of every exported entry point of the header.
 _SIGNATURES = [
     ("mlt_abi_version", C.c_int, []),
@@ -82,6 +89,10 @@ _SIGNATURES = [
     ("mlt_merge_top_m", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _i64p, _f64p, _i64p]),
     ("mlt_train_members", C.c_int, [C.c_void_p, C.POINTER(MltTrainDesc), _f64p, _f64p, _f64p, _f64p, _f64p,
                                      _f64p, _i32p]),
+    ("mlt_surrogate_times", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltSurrogate), _i64p, C.c_int64,
+                                      C.c_int32, _f64p, _u8p]),
+    ("mlt_surrogate_best", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltSurrogate), C.c_int64, C.c_int64,
+                                     C.c_int32, C.c_double, _i64p, _f64p, _i64p, _i64p]),
     ("mlt_convbench_create", C.c_int, [C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_float), C.c_uint64,
                                        C.POINTER(C.c_void_p)]),
     ("mlt_convbench_destroy", C.c_int, [C.c_void_p]),
@@ -180,6 +191,29 @@ def ptr(a: np.ndarray, ctype):
 
 # ---- descriptor packing ------------------------------------------------------
 
+def pack_rules(rules, pos):
+    """ValidityRule-likes (kind, operands, coefficients, bound) -> the five
+    mlt_space rule arrays (paramspace.py:66-107 semantics; empty coefficients
+    mean all ones except for forbidden combinations)."""
+    kinds, nops, rpos, coeff, bound = [], [], [], [], []
+    for r in rules:
+        kind = r["kind"] if isinstance(r, dict) else r.kind
+        ops = list(r["operands"] if isinstance(r, dict) else r.operands)
+        co = [int(c) for c in (r.get("coefficients", ()) if isinstance(r, dict) else r.coefficients)]
+        if not co and kind != "forbidden-combination":
+            co = [1] * len(ops)
+        if len(co) != len(ops):
+            raise ValueError(f"rule {kind} has {len(ops)} operands but {len(co)} coefficients")
+        kinds.append(RULE_KIND[kind])
+        nops.append(len(ops))
+        rpos.extend(pos[o] for o in ops)
+        coeff.extend(co)
+        bound.append(int(r.get("bound", 0) if isinstance(r, dict) else r.bound))
+    return (np.ascontiguousarray(kinds or [0], dtype=np.int32), np.ascontiguousarray(nops or [0], dtype=np.int32),
+            np.ascontiguousarray(rpos or [0], dtype=np.int32), np.ascontiguousarray(coeff or [0], dtype=np.int64),
+            np.ascontiguousarray(bound or [0], dtype=np.int64))
+
+
 class PackedSpace:
     """mlt_space over host arrays kept alive by this object."""
 
@@ -189,23 +223,9 @@ class PackedSpace:
         pos = {n: i for i, n in enumerate(names)}
         self.radix = np.ascontiguousarray([len(p.values) for p in params], dtype=np.int32)
         self.values = np.ascontiguousarray([int(v) for p in params for v in p.values], dtype=np.int64)
-        kinds, nops, rpos, coeff, bound = [], [], [], [], []
-        for r in getattr(space, "rules", ()):
-            kinds.append(RULE_KIND[r.kind])
-            ops = list(r.operands)
-            co = [int(c) for c in r.coefficients]
-            if not co and r.kind != "forbidden-combination":
-                co = [1] * len(ops)
-            nops.append(len(ops))
-            rpos.extend(pos[o] for o in ops)
-            coeff.extend(co)
-            bound.append(int(r.bound))
-        self.kind = np.ascontiguousarray(kinds or [0], dtype=np.int32)
-        self.nops = np.ascontiguousarray(nops or [0], dtype=np.int32)
-        self.rpos = np.ascontiguousarray(rpos or [0], dtype=np.int32)
-        self.coeff = np.ascontiguousarray(coeff or [0], dtype=np.int64)
-        self.bound = np.ascontiguousarray(bound or [0], dtype=np.int64)
-        self.c = MltSpace(len(params), ptr(self.radix, C.c_int32), ptr(self.values, C.c_int64), len(kinds),
+        rules = list(getattr(space, "rules", ()))
+        self.kind, self.nops, self.rpos, self.coeff, self.bound = pack_rules(rules, pos)
+        self.c = MltSpace(len(params), ptr(self.radix, C.c_int32), ptr(self.values, C.c_int64), len(rules),
                           ptr(self.kind, C.c_int32), ptr(self.nops, C.c_int32), ptr(self.rpos, C.c_int32),
                           ptr(self.coeff, C.c_int64), ptr(self.bound, C.c_int64))
         self.card = int(np.prod(self.radix.astype(object)))

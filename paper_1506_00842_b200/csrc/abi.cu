@@ -69,7 +69,8 @@ namespace {
 
 enum Slot {
   S_SPACE_VALUES, S_SPACE_RPOS, S_SPACE_RCOEFF, S_ENS, S_IDX, S_OUT_A, S_OUT_B, S_OUT_C, S_OUT_D,
-  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT, S_TOPI, S_TOPP, S_POH, S_POL, S_PIH, S_PIL
+  S_EA, S_EBP, S_U, S_TAB, S_GSCAL, S_CIDX, S_CVAL, S_SORT_TMP, S_FEAT, S_TOPI, S_TOPP, S_POH, S_POL, S_PIH, S_PIL,
+  S_L_VALUES, S_L_RPOS, S_L_RCOEFF, S_SURR, S_PART
 };
 
 int ws(mlt_ctx* c, int slot, size_t bytes, void** out) {
@@ -155,7 +156,8 @@ int read_space(const mlt_space* s, HostSpace* h) {
   return MLT_OK;
 }
 
-int upload_space(mlt_ctx* c, const HostSpace& h, DSpace* d, int base_slot_values = S_SPACE_VALUES) {
+int upload_space(mlt_ctx* c, const HostSpace& h, DSpace* d, int base_slot_values = S_SPACE_VALUES,
+                 int slot_rpos = S_SPACE_RPOS, int slot_rcoeff = S_SPACE_RCOEFF) {
   std::memset(d, 0, sizeof *d);
   d->P = h.P;
   d->R = (int)h.rkind.size();
@@ -176,8 +178,8 @@ int upload_space(mlt_ctx* c, const HostSpace& h, DSpace* d, int base_slot_values
   for (int r = 0; r <= d->R; ++r) d->roff[r] = h.roff[r];
   int* rp;
   int64_t* rc;
-  TRY(ws_t(c, S_SPACE_RPOS, std::max<size_t>(1, h.rpos.size()), &rp));
-  TRY(ws_t(c, S_SPACE_RCOEFF, std::max<size_t>(1, h.rcoeff.size()), &rc));
+  TRY(ws_t(c, slot_rpos, std::max<size_t>(1, h.rpos.size()), &rp));
+  TRY(ws_t(c, slot_rcoeff, std::max<size_t>(1, h.rcoeff.size()), &rc));
   if (!h.rpos.empty()) {
     CU(cudaMemcpyAsync(rp, h.rpos.data(), h.rpos.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(rc, h.rcoeff.data(), h.rcoeff.size() * 8, cudaMemcpyHostToDevice, c->stream));
@@ -1179,6 +1181,167 @@ int mlt_train_members(mlt_ctx* c, const mlt_train_desc* desc, double* w1, double
   const int rc = mlt_train_members_impl(c->dev, c->stream, &c->launches, desc, w1, b1, w2, b2, loss_first,
                                         loss_final, diverged_epoch, &err);
   if (rc != MLT_OK) return fail(rc, "%s", err);
+  return MLT_OK;
+}
+
+}  // extern "C"
+
+// ---- A12: surrogate device ---------------------------------------------------
+namespace {
+
+constexpr int kMaxTerms = 4096;
+
+// The spec's launch rules as a second space (same parameters, its own rules);
+// terms with their matched values mapped to digits (-1 = value not in the list).
+int read_surrogate(const mlt_space* space, const mlt_surrogate* sp, const HostSpace& hs, HostSpace* lr,
+                   std::vector<int>* tpos, std::vector<int>* tdig, std::vector<double>* tfac) {
+  if (!sp) return fail(MLT_EINVAL, "surrogate spec is NULL");
+  if (!(sp->base_time > 0)) return fail(MLT_EINVAL, "base_time must be strictly positive");
+  if (sp->n_terms < 0 || sp->n_terms > kMaxTerms) return fail(MLT_EINVAL, "0..%d terms supported", kMaxTerms);
+  if (!(sp->log_sigma >= 0)) return fail(MLT_EINVAL, "log_sigma must be non-negative");
+  mlt_space ls = *space;
+  ls.n_rules = sp->n_rules;
+  ls.rule_kind = sp->rule_kind;
+  ls.rule_nops = sp->rule_nops;
+  ls.rule_pos = sp->rule_pos;
+  ls.rule_coeff = sp->rule_coeff;
+  ls.rule_bound = sp->rule_bound;
+  TRY(read_space(&ls, lr));
+  std::vector<int> voff(hs.P, 0);
+  for (int p = 1; p < hs.P; ++p) voff[p] = voff[p - 1] + hs.radix[p - 1];
+  auto digit_of = [&](int p, int64_t v) {
+    for (int q = 0; q < hs.radix[p]; ++q)
+      if (hs.values[voff[p] + q] == v) return q;
+    return -1;
+  };
+  tpos->assign(2 * std::max(sp->n_terms, 1), -1);
+  tdig->assign(2 * std::max(sp->n_terms, 1), -1);
+  tfac->assign(std::max(sp->n_terms, 1), 1.0);
+  for (int t = 0; t < sp->n_terms; ++t) {
+    const int np = sp->term_nparams[t];
+    if (np != 1 && np != 2) return fail(MLT_EINVAL, "term %d covers %d parameters (1 or 2 allowed)", t, np);
+    if (!(sp->term_factor[t] > 0)) return fail(MLT_EINVAL, "term %d factor must be strictly positive", t);
+    for (int j = 0; j < np; ++j) {
+      const int p = sp->term_pos[2 * t + j];
+      if (p < 0 || p >= hs.P) return fail(MLT_EINVAL, "term %d parameter position %d out of range", t, p);
+      (*tpos)[2 * t + j] = p;
+      (*tdig)[2 * t + j] = digit_of(p, sp->term_match[2 * t + j]);
+    }
+    if (np == 2 && ((*tdig)[2 * t] < 0 || (*tdig)[2 * t + 1] < 0)) (*tdig)[2 * t] = -1;
+    if (np == 1) (*tdig)[2 * t + 1] = -1;
+    (*tfac)[t] = sp->term_factor[t];
+  }
+  return MLT_OK;
+}
+
+// never-hitting terms keep their position but an impossible digit (-2 never equals a digit)
+int upload_surrogate(mlt_ctx* c, const mlt_surrogate* sp, int reps, std::vector<int>& tpos, std::vector<int>& tdig,
+                     const std::vector<double>& tfac, DSurr* d, size_t* smem) {
+  const int T = sp->n_terms;
+  for (int t = 0; t < T; ++t)
+    if (tdig[2 * t] < 0) tdig[2 * t] = -2;
+  const size_t bytes = tfac.size() * 8 + tpos.size() * 4 * 2;
+  char* buf;
+  TRY(ws_t(c, S_SURR, bytes, &buf));
+  CU(cudaMemcpyAsync(buf, tfac.data(), tfac.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(buf + tfac.size() * 8, tpos.data(), tpos.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemcpyAsync(buf + tfac.size() * 8 + tpos.size() * 4, tdig.data(), tdig.size() * 4, cudaMemcpyHostToDevice,
+                     c->stream));
+  d->base = sp->base_time;
+  d->sigma = sp->log_sigma;
+  d->seed = sp->seed;
+  d->T = T;
+  d->reps = reps;
+  d->tfac = reinterpret_cast<const double*>(buf);
+  d->tpos = reinterpret_cast<const int*>(buf + tfac.size() * 8);
+  d->tdig = reinterpret_cast<const int*>(buf + tfac.size() * 8 + tpos.size() * 4);
+  *smem = (size_t)T * (8 + 16);
+  return MLT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mlt_surrogate_times(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* spec, const int64_t* idx, int64_t n,
+                        int32_t reps, double* times, uint8_t* ok) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(MLT_EINVAL, "negative count");
+  if (reps < 0) return fail(MLT_EINVAL, "repetitions must be >= 0");
+  CU(cudaSetDevice(c->dev));
+  HostSpace hs, lr;
+  TRY(read_space(space, &hs));
+  std::vector<int> tpos, tdig;
+  std::vector<double> tfac;
+  TRY(read_surrogate(space, spec, hs, &lr, &tpos, &tdig, &tfac));
+  if (n == 0) return MLT_OK;
+  for (int64_t t = 0; t < n; ++t)
+    if (idx[t] < 0 || idx[t] >= hs.card_i)
+      return fail(MLT_EINVAL, "index %lld out of range for %lld configurations", (long long)idx[t],
+                  (long long)hs.card_i);
+  DSpace dl;
+  TRY(upload_space(c, lr, &dl, S_L_VALUES, S_L_RPOS, S_L_RCOEFF));
+  DSurr ds;
+  size_t smem = 0;
+  TRY(upload_surrogate(c, spec, reps, tpos, tdig, tfac, &ds, &smem));
+  int64_t* di;
+  double* dt;
+  uint8_t* dok;
+  TRY(ws_t(c, S_IDX, n, &di));
+  TRY(ws_t(c, S_OUT_A, n, &dt));
+  TRY(ws_t(c, S_OUT_C, n, &dok));
+  CU(cudaMemcpyAsync(di, idx, n * 8, cudaMemcpyHostToDevice, c->stream));
+  if (smem > 48 * 1024) CU(cudaFuncSetAttribute(k_surr_times, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_surr_times<<<grid_for(c, n, 256), 256, smem, c->stream>>>(dl, ds, di, n, dt, dok);
+  TRY(check_launch(c));
+  CU(cudaMemcpyAsync(times, dt, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MLT_OK;
+}
+
+int mlt_surrogate_best(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* spec, int64_t begin, int64_t end,
+                       int32_t reps, double threshold, int64_t* best_idx, double* best_time, int64_t* n_valid,
+                       int64_t* n_below) {
+  if (!c || !best_idx || !best_time || !n_valid || !n_below) return fail(MLT_EINVAL, "NULL argument");
+  if (reps < 0) return fail(MLT_EINVAL, "repetitions must be >= 0");
+  CU(cudaSetDevice(c->dev));
+  HostSpace hs, lr;
+  TRY(read_space(space, &hs));
+  std::vector<int> tpos, tdig;
+  std::vector<double> tfac;
+  TRY(read_surrogate(space, spec, hs, &lr, &tpos, &tdig, &tfac));
+  if (begin < 0 || end > hs.card_i || begin > end) return fail(MLT_EINVAL, "bad range [%lld, %lld)", (long long)begin,
+                                                               (long long)end);
+  *best_idx = -1;
+  *best_time = std::nan("");
+  *n_valid = *n_below = 0;
+  if (begin == end) return MLT_OK;
+  DSpace dsp, dl;
+  TRY(upload_space(c, hs, &dsp));
+  TRY(upload_space(c, lr, &dl, S_L_VALUES, S_L_RPOS, S_L_RCOEFF));
+  DSurr ds;
+  size_t smem = 0;
+  TRY(upload_surrogate(c, spec, reps, tpos, tdig, tfac, &ds, &smem));
+  const int threads = 256;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((end - begin + threads - 1) / threads, (int64_t)c->sms * 8));
+  SurrPart* part;
+  TRY(ws_t(c, S_PART, (size_t)grid + 1, &part));
+  if (smem > 48 * 1024) CU(cudaFuncSetAttribute(k_surr_best, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_surr_best<<<grid, threads, smem, c->stream>>>(dsp, dl, ds, begin, end, std::isnan(threshold) ? -HUGE_VAL : threshold,
+                                                  part);
+  TRY(check_launch(c));
+  k_surr_best_final<<<1, 1024, 0, c->stream>>>(part, grid, part + grid);
+  TRY(check_launch(c));
+  SurrPart r;
+  CU(cudaMemcpyAsync(&r, part + grid, sizeof r, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  *n_valid = r.n_valid;
+  *n_below = r.n_below;
+  if (r.n_valid > 0) {
+    *best_idx = r.i;
+    *best_time = r.t;
+  }
   return MLT_OK;
 }
 

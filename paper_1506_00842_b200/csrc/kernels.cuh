@@ -18,6 +18,26 @@ __global__ void k_member_out64(DEns e, const double* feat, int64_t n, double* ou
 size_t predict64_smem(const DEns& e);
 __global__ void k_rescore_warp(DEns e, const int64_t* idx, const uint32_t* n_ptr, double* pred);
 
+// ---- analytic surrogate device (surrogate.cu) -------------------------------
+struct DSurr {
+  double base;                  // base_time
+  double sigma;                 // log-time noise std (0 = noise-free)
+  uint64_t seed;
+  int T;                        // terms
+  int reps;                     // 0 = true times; >= 1 = measured (min over reps of the noise)
+  const int* tpos;              // [T][2] parameter positions (second -1 for one-parameter terms)
+  const int* tdig;              // [T][2] matched DIGITS (-1: the value is not in the list, never hits)
+  const double* tfac;           // [T]
+};
+struct SurrPart {
+  double t;
+  int64_t i;
+  int64_t n_valid, n_below;
+};
+__global__ void k_surr_times(DSpace lr, DSurr su, const int64_t* idx, int64_t n, double* times, uint8_t* ok);
+__global__ void k_surr_best(DSpace sp, DSpace lr, DSurr su, int64_t begin, int64_t end, double thr, SurrPart* part);
+__global__ void k_surr_best_final(const SurrPart* part, int n, SurrPart* out);
+
 // ---- final guard-band stage (select.cu) ------------------------------------
 constexpr int kSmallSort = 4096;  // survivors sorted in one CTA's shared memory
 __global__ void k_band_filter(const int64_t* cidx, const float* cval, uint32_t count, int m, float band,
@@ -38,6 +58,10 @@ __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint3
 #ifndef MLT_MINB
 #define MLT_MINB 2
 #endif
+#ifndef MLT_EBS
+#define MLT_EBS 0
+#endif
+constexpr int kEbStages = MLT_EBS;  // cp.async ring depth for the per-thread exp(-B')/w' factors (0 = LDG ping-pong)
 constexpr int kThreads = MLT_THREADS;   // threads per sweep CTA
 constexpr int kInner = MLT_INNER;   // inner configurations per thread (share every exp(-A') load)
 constexpr int kInnerBlock = kThreads * kInner;   // inner configurations per work item

@@ -258,10 +258,21 @@ __device__ __forceinline__ void lower_threshold(const SweepArgs& a, uint32_t* s_
   }
 }
 
+// the per-thread factor ring: [stage][w][thread] float4 (conflict-free LDS.128)
+constexpr size_t eb_ring_bytes() { return (size_t)kEbStages * ebw_of(3) * kThreads * 16; }
+
 size_t sweep_smem(int k) {
   const size_t KH = (size_t)k * kH;
-  return KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4;
+  return KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4 + eb_ring_bytes();
 }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 // ---------------------------------------------------------------------------
 // the sweep
 //
@@ -280,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   int64_t* s_bidx = reinterpret_cast<int64_t*>(s_u + ((KH + 3) & ~3));
   float* s_bval = reinterpret_cast<float*>(s_bidx + kSB);
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_bval + kSB);
+  float4* s_eb = reinterpret_cast<float4*>(s_hist + 256);        // [kEbStages][W][kThreads]
   __shared__ int s_n, s_tot;
   __shared__ uint32_t s_th, s_sel[2], s_wsum[kThreads / 32];
 
@@ -315,27 +327,71 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
 #pragma unroll
       for (int q = 0; q < kOB / 2; ++q) acc[s][q] = 0ull;
 
-    // Two register sets (A, B) ping-pong so the next group's per-thread factors
-    // are in flight from L2 while the current group computes, with no copies.
     constexpr int W = ebw_of(G);
     const size_t gstride = (size_t)kThreads * W;   // float4s per group
     const float4* pe = reinterpret_cast<const float4*>(a.ebp) + ((size_t)ib * ngroups * kThreads + tid) * W;
     const float* pu = s_u;                   // 1/w' of the current group
     const float* E = s_ea;                   // exp(-A') rows of the current group
-    float ebA[kInner][G], uA[G], ebB[kInner][G], uB[G];
-    load_group<G>(pe, pu, ebA, uA);
+    if (kEbStages > 0) {
+      // Each thread streams ITS OWN factors through a private cp.async ring
+      // kEbStages groups ahead: the L2 latency hides behind kEbStages-1 groups
+      // of math, with no cross-thread synchronisation (a thread only reads
+      // back what it copied).
+      constexpr int S = kEbStages > 0 ? kEbStages : 1;
+      auto issue = [&](int g) {
+        if (g < ngroups) {
+          const float4* src = pe + (size_t)g * gstride;
+          float4* dst = s_eb + (size_t)(g % S) * W * kThreads + tid;
+#pragma unroll
+          for (int w = 0; w < W; ++w) cp_async16(dst + w * kThreads, src + w);
+        }
+        cp_async_commit();   // empty groups keep the wait count uniform
+      };
+#pragma unroll
+      for (int g = 0; g < S - 1; ++g) issue(g);
 #pragma unroll 1
-    for (int gi = 0; gi < ngroups; gi += 2) {
-      const bool has_b = gi + 1 < ngroups;
-      load_group<G>(has_b ? pe + gstride : pe, has_b ? pu + G : pu, ebB, uB);
-      group_step<G>(acc, E, ebA, uA);
-      if (!has_b) break;
-      const bool has_c = gi + 2 < ngroups;
-      load_group<G>(has_c ? pe + 2 * gstride : pe, has_c ? pu + 2 * G : pu, ebA, uA);
-      group_step<G>(acc, E + G * kOB, ebB, uB);
-      pe += 2 * gstride;
-      pu += 2 * G;
-      E += 2 * G * kOB;
+      for (int gi = 0; gi < ngroups; ++gi) {
+        issue(gi + S - 1);
+        cp_async_wait<S - 1>();
+        const float4* src = s_eb + (size_t)(gi % S) * W * kThreads + tid;
+        float f[4 * W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const float4 v = src[w * kThreads];
+          f[4 * w] = v.x;
+          f[4 * w + 1] = v.y;
+          f[4 * w + 2] = v.z;
+          f[4 * w + 3] = v.w;
+        }
+        float eb[kInner][G], uu[G];
+#pragma unroll
+        for (int x = 0; x < G; ++x) {
+#pragma unroll
+          for (int s2 = 0; s2 < kInner; ++s2) eb[s2][x] = f[x * kInner + s2];
+          uu[x] = pu[x];
+        }
+        group_step<G>(acc, E, eb, uu);
+        pu += G;
+        E += G * kOB;
+      }
+    } else {
+      // Two register sets (A, B) ping-pong so the next group's per-thread factors
+      // are in flight from L2 while the current group computes, with no copies.
+      float ebA[kInner][G], uA[G], ebB[kInner][G], uB[G];
+      load_group<G>(pe, pu, ebA, uA);
+#pragma unroll 1
+      for (int gi = 0; gi < ngroups; gi += 2) {
+        const bool has_b = gi + 1 < ngroups;
+        load_group<G>(has_b ? pe + gstride : pe, has_b ? pu + G : pu, ebB, uB);
+        group_step<G>(acc, E, ebA, uA);
+        if (!has_b) break;
+        const bool has_c = gi + 2 < ngroups;
+        load_group<G>(has_c ? pe + 2 * gstride : pe, has_c ? pu + 2 * G : pu, ebA, uA);
+        group_step<G>(acc, E + G * kOB, ebB, uB);
+        pe += 2 * gstride;
+        pu += 2 * G;
+        E += 2 * G * kOB;
+      }
     }
 
     // ---- candidates: bit (s*kOB + r) <-> inner s, outer r -----------------------

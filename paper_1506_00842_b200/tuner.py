@@ -160,7 +160,11 @@ def exhaustive_search(space, runner):
     (tuner.py:191-224). Vectorised through `runner.measured_times` when present."""
     card = space.cardinality()
     best = None
-    if hasattr(runner, "measured_times"):
+    if hasattr(runner, "exhaustive_best"):      # device surrogate: one fused sweep of the whole space
+        i, t, n_valid, _ = runner.exhaustive_best()
+        if n_valid > 0:
+            best = (t, i)
+    elif hasattr(runner, "measured_times"):
         reps = getattr(runner, "default_repetitions", 1)
         for s in range(0, card, SWEEP_CHUNK):
             idx = np.arange(s, min(s + SWEEP_CHUNK, card), dtype=np.int64)

@@ -16,6 +16,8 @@ Fixtures (all small):
   pred_<case>.npz    probe indices + reference predict_indices
   topm_<case>.npz    reference top_m_predicted (indices, predictions) per m
   train_small.npz    reference _fit outputs on small cases (weights + losses)
+  formats/           (--formats) files written by the reference's own writers:
+                     sample CSVs, a surrogate spec JSON, a `mltune predict` CSV
 """
 
 from __future__ import annotations
@@ -98,7 +100,10 @@ def probe_indices(card, n=2048, seed=7):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--synth", action="store_true", help="run the full 1e8 reference sweep")
+    ap.add_argument("--formats", action="store_true", help="only (re)write the on-disk format fixtures")
     args = ap.parse_args()
+    if args.formats:
+        return formats_fixtures()
     t0 = time.time()
     spaces = {n: PS.builtin_space(n) for n in PS.BUILTIN_SPACE_NAMES}
     spaces["synthetic-1e8"] = synthetic_space()
@@ -223,6 +228,34 @@ def main():
     small["div_time"] = np.array([s.outcome.time for s in ss.samples])
     np.savez_compressed(OUT / "train_small.npz", **small)
     print("done", time.time() - t0)
+
+
+def formats_fixtures():
+    """Sample CSV / surrogate JSON / prediction CSV written by the reference's
+    own writers (measurement.py:353-554, cli.py:330-353)."""
+    from mltune import cli
+    d = OUT / "formats"
+    d.mkdir(exist_ok=True)
+    conv = PS.builtin_space("convolution")
+    spec = builtin_surrogate("gpu-a", conv)
+    runner = M.SurrogateRunner(spec, conv, runner_id="gpu-a", default_repetitions=2)
+    ss = M.SampleSet(conv, "gpu-a", tuple(T.measure_configs(conv, runner, conv.sample_random(300, 4), 2)))
+    M.save_samples(ss, d / "samples_convolution.csv")
+    M.save_surrogate_spec(spec, d / "surrogate_gpu-a_convolution.json")
+    tiny = PS.ParamSpace("tiny", (PS.ParamDef("a", (1, 2, 4)), PS.ParamDef("b", (0, 1)),
+                                  PS.ParamDef("c", (10, 20, 30, 40))),
+                         (PS.ValidityRule("max-product", ("a", "c"), bound=80),))
+    tspec = M.SurrogateSpec(0.5, (M.SurrogateTerm(("a",), (4,), 2.5), M.SurrogateTerm(("b", "c"), (1, 30), 0.4)),
+                            noise_cv=0.1, seed=7)
+    tr = M.SurrogateRunner(tspec, tiny, runner_id="tiny-sur")
+    tss = M.SampleSet(tiny, "tiny-sur", tuple(T.measure_configs(tiny, tr, [tiny.config_at(i) for i in range(24)])))
+    M.save_samples(tss, d / "samples_tiny.csv")
+    ens = MD.train_ensemble(tss, tiny, k=3, cfg=MD.TrainConfig(seed=3, epochs=50))
+    MD.save_model(ens, d / "model_tiny.json")
+    assert cli.main(["predict", "--model", str(d / "model_tiny.json"), "--out", str(d / "pred_tiny.csv")]) == 0
+    assert cli.main(["predict", "--model", str(OUT / "model_conv_k11.json"), "--index", "4242",
+                     "--out", str(d / "pred_conv_4242.csv")]) == 0
+    print("formats written to", d)
 
 
 def slice_top(ens, sp, m, lo, hi):

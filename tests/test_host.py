@@ -159,3 +159,26 @@ def test_install_rebinds_a_reference_shaped_package():
         b.uninstall()
         del sys.modules["fakemltune.errors"]
     assert fake.tuner.top_m_predicted is None
+
+
+def test_surrogate_spec_packing():
+    """The mlt_surrogate descriptor built from the reference's spec JSON
+    (measurement.py:497-554): term positions/values/factors in spec order,
+    launch rules in the mlt_space encoding, log_sigma as SurrogateSpec computes it."""
+    from conftest import surrogates_doc
+    from paper_1506_00842_b200.surrogate import PackedSurrogate
+    doc = surrogates_doc()["synthetic-1e8"]
+    sp = product_space("synthetic-1e8")
+    pk = PackedSurrogate(doc, sp)
+    names = sp.param_names()
+    assert pk.c.n_terms == len(doc["terms"]) and pk.c.n_rules == len(doc["invalid_rules"])
+    for t, term in enumerate(doc["terms"]):
+        assert pk.nparams[t] == len(term["params"])
+        assert [names[p] for p in pk.tpos[t, :len(term["params"])]] == term["params"]
+        assert list(pk.match[t, :len(term["match"])]) == term["match"]
+        assert pk.factor[t] == term["factor"]
+    assert pk.log_sigma == float(np.sqrt(np.log1p(doc["noise_cv"] ** 2)))
+    assert pk.c.seed == doc["seed"] and pk.c.base_time == doc["base_time"]
+    assert list(pk.kind[:pk.c.n_rules]) == [0] * pk.c.n_rules      # gpu-a: max-product launch limits
+    noiseless = PackedSurrogate(dict(doc, noise_cv=0.0), sp)
+    assert noiseless.c.log_sigma == 0.0

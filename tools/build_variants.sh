@@ -1,18 +1,22 @@
 #!/bin/bash
-# Build sweep-kernel tiling variants for A/B timing on the GPU box:
-#   tools/build_variants.sh tag:THREADS:INNER:OB:MINB ...
+# Build sweep-kernel variants for A/B timing on the GPU box:
+#   tools/build_variants.sh tag:THREADS:INNER:OB:MINB[:DEF=V,DEF=V...] ...
 # -> build/variants/<tag>/libmltune_b200.so (select with MLTUNE_B200_LIB=...)
+# Only the core translation units are rebuilt with the variant's defines; the
+# benchmark-kernel objects come from the regular build (make -C .../csrc first).
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 SRC=$ROOT/paper_1506_00842_b200/csrc
+BENCH_OBJS=$(ls $ROOT/build/bench_*.o)
 for spec in "$@"; do
-  IFS=: read tag thr inner ob minb <<< "$spec"
+  IFS=: read tag thr inner ob minb extra <<< "$spec"
   out=$ROOT/build/variants/$tag
   mkdir -p $out
+  defs="-DMLT_THREADS=$thr -DMLT_INNER=$inner -DMLT_OB=$ob -DMLT_MINB=$minb"
+  for d in ${extra//,/ }; do defs="$defs -D$d"; done
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-    -Xcompiler -fvisibility=hidden -I$ROOT/include -DMLT_THREADS=$thr -DMLT_INNER=$inner -DMLT_OB=$ob \
-    -DMLT_MINB=$minb -Xptxas -v -o $out/libmltune_b200.so $SRC/abi.cu $SRC/predict.cu $SRC/select.cu \
-    $SRC/sweep.cu $SRC/train.cu 2> $out/ptxas.txt &
+    -Xcompiler -fvisibility=hidden -I$ROOT/include $defs -Xptxas -v -o $out/libmltune_b200.so $SRC/abi.cu \
+    $SRC/predict.cu $SRC/select.cu $SRC/surrogate.cu $SRC/sweep.cu $SRC/train.cu $BENCH_OBJS 2> $out/ptxas.txt &
 done
 wait
 for spec in "$@"; do
