@@ -379,7 +379,8 @@ def main():
             "guard_band": {"delta": st.delta, "group": st.group, "split_inner_params": st.split},
             "parity_top200_vs_reference": ok,
             "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step_median": 1e3 * statistics.median(e2e_times),
+                    "ms_per_step_max": 1e3 * max(e2e_times)},
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.workload, M_TOP, args.cpu_sample)

@@ -95,6 +95,14 @@ int ws_t(mlt_ctx* c, int slot, size_t count, T** out) {
   return MLT_OK;
 }
 
+// Plan-owned buffers come from the device's stream-ordered memory pool
+// (cudaMallocAsync / cudaFreeAsync on the context stream; the pool keeps its
+// memory, see mlt_ctx_create), so a per-call plan costs no cudaMalloc/cudaFree
+// round trips or device-wide synchronisation.
+void pool_free(mlt_ctx* c, void* ptr) {
+  if (ptr) cudaFreeAsync(ptr, c->stream);
+}
+
 int check_launch(mlt_ctx* c) {
   c->launches++;
   CU(cudaGetLastError());
@@ -482,8 +490,8 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   b.delta = 1.5 * uu * (cg * S + acc_bound + S + 3.0 * std::fabs(cst)) + 1e-12 * (1.0 + std::fabs(cst));
 
   mlt_ctx* c = p->ctx;
-  CU(cudaMalloc(&b.d_tab, tab.size() * 8));
-  CU(cudaMalloc(&b.d_u, (size_t)KH * 4));
+  CU(cudaMallocAsync(&b.d_tab, tab.size() * 8, c->stream));
+  CU(cudaMallocAsync(&b.d_u, (size_t)KH * 4, c->stream));
   CU(cudaMemcpyAsync(b.d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
   CU(cudaMemcpyAsync(b.d_u, u.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
   b.ok = true;
@@ -496,8 +504,8 @@ int get_setup(mlt_plan* p, int split, BandSetup** out) {
     BandSetup b;
     const int rc = band_setup(p, split, b);
     if (rc != MLT_OK) {
-      cudaFree(b.d_tab);
-      cudaFree(b.d_u);
+      pool_free(p->ctx, b.d_tab);
+      pool_free(p->ctx, b.d_u);
       return rc;
     }
     it = p->setups.emplace(split, b).first;
@@ -518,7 +526,7 @@ int plan_factors(mlt_plan* p) {
   for (int q = 0; q < s.P; ++q) p->foff[q + 1] = p->foff[q] + s.radix[q];
   const int KH = e.k * kH;
   mlt_ctx* c = p->ctx;
-  CU(cudaMalloc(&p->d_F, (size_t)KH * p->foff[s.P] * 8));
+  CU(cudaMallocAsync(&p->d_F, (size_t)KH * p->foff[s.P] * 8, c->stream));
   TableArgs ta;
   std::memset(&ta, 0, sizeof ta);
   ta.k = e.k;
@@ -547,7 +555,7 @@ int plan_upload(mlt_plan* p) {
     d.voff[q] = off;
     off += h.radix[q];
   }
-  CU(cudaMalloc(&p->d_values, h.values.size() * 8));
+  CU(cudaMallocAsync(&p->d_values, h.values.size() * 8, c->stream));
   CU(cudaMemcpyAsync(p->d_values, h.values.data(), h.values.size() * 8, cudaMemcpyHostToDevice, c->stream));
   d.values = p->d_values;
   for (int r = 0; r < d.R; ++r) {
@@ -555,8 +563,8 @@ int plan_upload(mlt_plan* p) {
     d.rbound[r] = h.rbound[r];
   }
   for (int r = 0; r <= d.R; ++r) d.roff[r] = h.roff[r];
-  CU(cudaMalloc(&p->d_rpos, std::max<size_t>(1, h.rpos.size()) * 4));
-  CU(cudaMalloc(&p->d_rcoeff, std::max<size_t>(1, h.rcoeff.size()) * 8));
+  CU(cudaMallocAsync(&p->d_rpos, std::max<size_t>(1, h.rpos.size()) * 4, c->stream));
+  CU(cudaMallocAsync(&p->d_rcoeff, std::max<size_t>(1, h.rcoeff.size()) * 8, c->stream));
   if (!h.rpos.empty()) {
     CU(cudaMemcpyAsync(p->d_rpos, h.rpos.data(), h.rpos.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(p->d_rcoeff, h.rcoeff.data(), h.rcoeff.size() * 8, cudaMemcpyHostToDevice, c->stream));
@@ -571,7 +579,7 @@ int plan_upload(mlt_plan* p) {
   de.d = e.d;
   de.h = e.h;
   for (int q = 0; q < e.d; ++q) de.counts[q] = e.counts[q];
-  CU(cudaMalloc(&p->d_ens, e.packed.size() * 8));
+  CU(cudaMallocAsync(&p->d_ens, e.packed.size() * 8, c->stream));
   CU(cudaMemcpyAsync(p->d_ens, e.packed.data(), e.packed.size() * 8, cudaMemcpyHostToDevice, c->stream));
   const size_t nw = (size_t)e.k * e.h * e.d, nh = (size_t)e.k * e.h;
   de.w1 = p->d_ens;
@@ -584,14 +592,15 @@ int plan_upload(mlt_plan* p) {
 }
 
 void plan_free(mlt_plan* p) {
-  cudaFree(p->d_values);
-  cudaFree(p->d_rpos);
-  cudaFree(p->d_rcoeff);
-  cudaFree(p->d_ens);
-  cudaFree(p->d_F);
+  mlt_ctx* c = p->ctx;
+  pool_free(c, p->d_values);
+  pool_free(c, p->d_rpos);
+  pool_free(c, p->d_rcoeff);
+  pool_free(c, p->d_ens);
+  pool_free(c, p->d_F);
   for (auto& kv : p->setups) {
-    cudaFree(kv.second.d_tab);
-    cudaFree(kv.second.d_u);
+    pool_free(c, kv.second.d_tab);
+    pool_free(c, kv.second.d_u);
   }
   p->setups.clear();
 }
@@ -642,6 +651,12 @@ int mlt_ctx_create(int device, mlt_ctx** out) {
   c->sms = prop.multiProcessorCount;
   CU(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
+  {
+    cudaMemPool_t pool;
+    CU(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;   // never trim: per-call plans reuse the same blocks
+    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   CU(cudaMallocHost(&c->pinned, 4096));
   for (auto& ev : c->ev) CU(cudaEventCreate(&ev));
   *out = c;

@@ -10,7 +10,8 @@
 //                    (tile > 227 KB -> invalid-launch)
 //   padding          input pre-padded by 2 replicated pixels: no clamping in the kernel
 //   interleaved      a thread's pixels are strided by the CTA width (coalesced) instead of contiguous
-//   unroll           the 5x5 filter loops fully unrolled
+//   unroll           the 5x5 filter loops fully unrolled; with contiguous pixels (interleaved = 0)
+//                    each thread also keeps 8-tap row segments in registers for 4 adjacent outputs
 //
 // Every variant sums the 25 taps in the same (dy, dx) order in fp32 and
 // divides by 25, so all 32 variants produce bit-identical images, equal to
@@ -68,7 +69,42 @@ __global__ void k_conv5(ConvArgs a) {
     const int ly = INTER ? iy * wgy + ty : ty * a.ppty + iy;   // row within the CTA's output block
     const int y = Y0 + ly;
     if (y >= a.H) continue;
-    for (int ix = 0; ix < a.pptx; ++ix) {
+    int ix0 = 0;
+    if (UNROLL && !INTER) {
+      // Unrolled + contiguous: 4 horizontally adjacent outputs share each
+      // row segment of 8 taps held in registers (8 loads per row instead of
+      // 20); every output still sums its 25 taps in (dy, dx) order.
+      for (; ix0 + 4 <= a.pptx; ix0 += 4) {
+        const int lx = tx * a.pptx + ix0;
+        const int x = X0 + lx;
+        if (x + 3 >= a.W) break;
+        float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
+#pragma unroll
+        for (int dy = -2; dy <= 2; ++dy) {
+          float r[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            r[q] = LOCAL ? tile[(ly + 2 + dy) * tw + (lx + q)] : fetch<IMG, PAD>(a, y + dy, x - 2 + q);
+#pragma unroll
+          for (int dx = 0; dx < 5; ++dx) {
+            s0 += r[dx];
+            s1 += r[dx + 1];
+            s2 += r[dx + 2];
+            s3 += r[dx + 3];
+          }
+        }
+        float* o = a.out + (size_t)y * a.W + x;
+        if ((a.W & 3) == 0) {
+          *reinterpret_cast<float4*>(o) = make_float4(s0 / 25.0f, s1 / 25.0f, s2 / 25.0f, s3 / 25.0f);
+        } else {
+          o[0] = s0 / 25.0f;
+          o[1] = s1 / 25.0f;
+          o[2] = s2 / 25.0f;
+          o[3] = s3 / 25.0f;
+        }
+      }
+    }
+    for (int ix = ix0; ix < a.pptx; ++ix) {
       const int lx = INTER ? ix * wgx + tx : tx * a.pptx + ix;
       const int x = X0 + lx;
       if (x >= a.W) continue;

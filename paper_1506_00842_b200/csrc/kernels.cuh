@@ -47,16 +47,16 @@ __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint3
 
 // ---- fp32 factored sweep (sweep.cu) ---------------------------------------
 #ifndef MLT_THREADS
-#define MLT_THREADS 256
+#define MLT_THREADS 1024
 #endif
 #ifndef MLT_INNER
 #define MLT_INNER 2
 #endif
 #ifndef MLT_OB
-#define MLT_OB 16
+#define MLT_OB 8
 #endif
 #ifndef MLT_MINB
-#define MLT_MINB 2
+#define MLT_MINB 1
 #endif
 #ifndef MLT_EBS
 #define MLT_EBS 0
