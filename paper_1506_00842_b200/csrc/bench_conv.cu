@@ -11,7 +11,7 @@
 //   padding          input pre-padded by 2 replicated pixels: no clamping in the kernel
 //   interleaved      a thread's pixels are strided by the CTA width (coalesced) instead of contiguous
 //   unroll           the 5x5 filter loops fully unrolled; with contiguous pixels (interleaved = 0)
-//                    each thread also keeps 8-tap row segments in registers for 4 adjacent outputs
+//                    each thread also streams 8 input rows once for 4 vertically adjacent outputs
 //
 // Every variant sums the 25 taps in the same (dy, dx) order in fp32 and
 // divides by 25, so all 32 variants produce bit-identical images, equal to
@@ -65,46 +65,44 @@ __global__ void k_conv5(ConvArgs a) {
     }
     __syncthreads();
   }
-  for (int iy = 0; iy < a.ppty; ++iy) {
+  int iy0 = 0;
+  if (UNROLL && !INTER) {
+    // Unrolled + contiguous rows: 4 vertically adjacent outputs of a column
+    // stream the 8 input rows they cover once (8 x 5 loads for 4 outputs
+    // instead of 4 x 25); each output still adds its 25 taps in (dy, dx)
+    // order. Adjacent lanes read adjacent columns (conflict-free when ppt_x = 1).
+    for (; iy0 + 4 <= a.ppty; iy0 += 4) {
+      const int ly = ty * a.ppty + iy0;
+      const int y = Y0 + ly;
+      if (y + 3 >= a.H) break;
+      for (int ix = 0; ix < a.pptx; ++ix) {
+        const int lx = tx * a.pptx + ix;
+        const int x = X0 + lx;
+        if (x >= a.W) break;
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          float t[5];
+#pragma unroll
+          for (int dx = 0; dx < 5; ++dx)
+            t[dx] = LOCAL ? tile[(ly + r) * tw + (lx + dx)] : fetch<IMG, PAD>(a, y - 2 + r, x - 2 + dx);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (r - k >= 0 && r - k <= 4) {
+#pragma unroll
+              for (int dx = 0; dx < 5; ++dx) acc[k] += t[dx];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a.out[(size_t)(y + k) * a.W + x] = acc[k] / 25.0f;
+      }
+    }
+  }
+  for (int iy = iy0; iy < a.ppty; ++iy) {
     const int ly = INTER ? iy * wgy + ty : ty * a.ppty + iy;   // row within the CTA's output block
     const int y = Y0 + ly;
     if (y >= a.H) continue;
-    int ix0 = 0;
-    if (UNROLL && !INTER) {
-      // Unrolled + contiguous: 4 horizontally adjacent outputs share each
-      // row segment of 8 taps held in registers (8 loads per row instead of
-      // 20); every output still sums its 25 taps in (dy, dx) order.
-      for (; ix0 + 4 <= a.pptx; ix0 += 4) {
-        const int lx = tx * a.pptx + ix0;
-        const int x = X0 + lx;
-        if (x + 3 >= a.W) break;
-        float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
-#pragma unroll
-        for (int dy = -2; dy <= 2; ++dy) {
-          float r[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            r[q] = LOCAL ? tile[(ly + 2 + dy) * tw + (lx + q)] : fetch<IMG, PAD>(a, y + dy, x - 2 + q);
-#pragma unroll
-          for (int dx = 0; dx < 5; ++dx) {
-            s0 += r[dx];
-            s1 += r[dx + 1];
-            s2 += r[dx + 2];
-            s3 += r[dx + 3];
-          }
-        }
-        float* o = a.out + (size_t)y * a.W + x;
-        if ((a.W & 3) == 0) {
-          *reinterpret_cast<float4*>(o) = make_float4(s0 / 25.0f, s1 / 25.0f, s2 / 25.0f, s3 / 25.0f);
-        } else {
-          o[0] = s0 / 25.0f;
-          o[1] = s1 / 25.0f;
-          o[2] = s2 / 25.0f;
-          o[3] = s3 / 25.0f;
-        }
-      }
-    }
-    for (int ix = ix0; ix < a.pptx; ++ix) {
+    for (int ix = 0; ix < a.pptx; ++ix) {
       const int lx = INTER ? ix * wgx + tx : tx * a.pptx + ix;
       const int x = X0 + lx;
       if (x >= a.W) continue;

@@ -59,9 +59,10 @@ def test_conv_4096_input_and_default_image(gpu_ok):
     x = r.input()
     assert x.min() >= 0 and x.max() < 1 and x.std() > 0.2
     gold = conv5_box(x)
-    # W % 4 == 0: the register-blocked unrolled path stores float4s
-    for cfg in ((32, 8, 1, 4, 0, 0, 1, 1, 1), (16, 8, 8, 1, 0, 1, 1, 0, 1), (16, 8, 4, 2, 0, 0, 0, 0, 1),
-                (8, 8, 16, 2, 1, 1, 0, 0, 1), (32, 4, 4, 4, 1, 0, 1, 0, 1)):
+    # unroll + contiguous rows: the 4-row register-blocked path (and its row tails)
+    for cfg in ((32, 8, 1, 4, 0, 0, 1, 1, 1), (32, 4, 1, 4, 0, 1, 1, 0, 1), (32, 8, 1, 8, 0, 0, 0, 0, 1),
+                (16, 16, 2, 4, 1, 1, 0, 0, 1), (32, 4, 4, 4, 1, 0, 1, 0, 1), (64, 2, 1, 16, 0, 1, 0, 0, 1),
+                (32, 8, 1, 6, 0, 1, 1, 0, 1)):
         t, ok = r.run(cfg, 3)
         assert ok and np.array_equal(r.output(), gold), cfg
     r.close()

@@ -1,3 +1,2 @@
-for v in t1024 t1024i1 t1024o4 t512m2 t256m4 t1024i1o8 t1024; do MLTUNE_B200_LIB=build/variants/$v/libmltune_b200.so python tools/sweep_ab.py synthetic-1e8 10; done > gpurun_out/tile_ab3.log 2>&1
-for v in t1024 t1024o4; do MLTUNE_B200_LIB=build/variants/$v/libmltune_b200.so python tools/sweep_ab.py stereo 10; done >> gpurun_out/tile_ab3.log 2>&1
-cat gpurun_out/tile_ab3.log
+python -m pytest tests/test_gpu_bench_kernels.py -x -q 2>&1 | tail -2
+for c in "32 16 4 4 0 1 1 1 1" "32 8 1 4 0 1 1 0 1" "32 8 1 8 0 1 1 0 1" "64 4 1 8 0 1 0 0 1" "32 16 1 4 0 0 1 0 1" "128 2 1 16 0 1 1 0 1" "32 4 1 16 0 1 1 0 1" "64 8 1 4 0 1 1 0 1" "32 8 1 4 0 0 0 0 1" "32 8 2 4 0 1 1 0 1"; do python tools/bench_kernel_probe.py conv $c; done
