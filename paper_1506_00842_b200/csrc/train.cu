@@ -246,7 +246,7 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
   const size_t outb = bytes_w1 + 2 * kh * 8 + (size_t)D.k * 8 * 3 + (size_t)D.k * 4;
   char* buf = nullptr;
   const size_t total = bytes_x + bytes_t + bytes_r + bytes_n + bytes_o + bytes_p + bytes_w1 + bytes_w2 + outb + 1024;
-  if ((e = cudaMalloc(&buf, total)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMallocAsync(&buf, total, stream)) != cudaSuccess) return cuda_fail(e);
   size_t at = 0;
   auto take = [&](size_t nb) {
     char* p = buf + at;
@@ -318,7 +318,7 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
     cudaMemcpyAsync(div, odiv, D.k * 4, cudaMemcpyDeviceToHost, stream);
     e = cudaStreamSynchronize(stream);
   }
-  cudaFree(buf);
+  cudaFreeAsync(buf, stream);
   if (e != cudaSuccess) return cuda_fail(e);
   for (int m = 0; m < D.k; ++m)
     if (div[m] != 0) {

@@ -263,27 +263,55 @@ def _member_draws(n: int, d: int, cfg: TrainConfig, seed_parts):
 
 def fit_members(X, y, member_rows, cfg: TrainConfig, seed_parts, device=None) -> list:
     """Train one network per entry of `member_rows` (row indices into X/y) on the device."""
-    k, d = len(member_rows), X.shape[1]
-    n_m = np.asarray([len(r) for r in member_rows], dtype=np.int32)
-    ts, means, stds, w1s, w2s, perms = [], [], [], [], [], []
-    for rows, sp in zip(member_rows, seed_parts):
-        targets = y[rows]
-        mean = float(targets.mean())
-        std = float(targets.std())
-        if std == 0.0:
-            std = 1.0
-        ts.append((targets - mean) / std)
-        means.append(mean)
-        stds.append(std)
-        w1, w2, pm = _member_draws(len(rows), d, cfg, sp)
-        w1s.append(w1)
-        w2s.append(w2)
-        perms.append(pm.ravel())
-    x = np.ascontiguousarray(X, dtype=np.float64)
+    res = fit_member_batches([(X, y, member_rows, seed_parts, cfg)], device)[0]
+    if isinstance(res, Exception):
+        raise res
+    return res
+
+
+def fit_member_batches(jobs, device=None) -> list:
+    """Train the members of several independent fits in ONE device launch
+    (one CTA per member, all concurrent). `jobs` = [(X, y, member_rows,
+    seed_parts, cfg)]; the jobs must share the optimiser settings (epochs,
+    batch size, learning rate, momentum) and the input width; each job's own
+    cfg drives its host draws (init scale; the seed is in seed_parts).
+    Returns, per job, its list of Networks or the DivergenceError it would
+    raise alone (first diverged member in member order, as model.py:239-243)."""
+    d = jobs[0][0].shape[1]
+    cfg = jobs[0][4]
+    opt = (cfg.epochs, cfg.batch_size, cfg.learning_rate, cfg.momentum)
+    xs, ts, rows_all, n_m, iw1s, iw2s, perms, meta = [], [], [], [], [], [], [], []
+    row_base = 0
+    for X, y, member_rows, seed_parts, jcfg in jobs:
+        if X.shape[1] != d:
+            raise ValueError("batched fits must share the input width")
+        if (jcfg.epochs, jcfg.batch_size, jcfg.learning_rate, jcfg.momentum) != opt:
+            raise ValueError("batched fits must share the optimiser settings")
+        xs.append(np.asarray(X, dtype=np.float64))
+        job_meta = []
+        for rows, sp in zip(member_rows, seed_parts):
+            targets = y[rows]
+            mean = float(targets.mean())
+            std = float(targets.std())
+            if std == 0.0:
+                std = 1.0
+            ts.append((targets - mean) / std)
+            job_meta.append((mean, std))
+            w1, w2, pm = _member_draws(len(rows), d, jcfg, sp)
+            iw1s.append(w1)
+            iw2s.append(w2)
+            perms.append(pm.ravel())
+            rows_all.append(np.asarray(rows) + row_base)
+            n_m.append(len(rows))
+        meta.append(job_meta)
+        row_base += X.shape[0]
+    k = len(n_m)
+    x = np.ascontiguousarray(np.concatenate(xs))
     t = np.ascontiguousarray(np.concatenate(ts))
-    rows = np.ascontiguousarray(np.concatenate(member_rows).astype(np.int32))
-    iw1 = np.ascontiguousarray(np.stack(w1s))
-    iw2 = np.ascontiguousarray(np.stack(w2s))
+    rows = np.ascontiguousarray(np.concatenate(rows_all).astype(np.int32))
+    n_m = np.asarray(n_m, dtype=np.int32)
+    iw1 = np.ascontiguousarray(np.stack(iw1s))
+    iw2 = np.ascontiguousarray(np.stack(iw2s))
     pall = np.ascontiguousarray(np.concatenate(perms))
     desc = N.MltTrainDesc(k, d, HIDDEN_UNITS, cfg.epochs, cfg.batch_size, cfg.learning_rate, cfg.momentum,
                           x.shape[0], N.ptr(x, N.C.c_double), N.ptr(t, N.C.c_double), N.ptr(rows, N.C.c_int32),
@@ -299,12 +327,19 @@ def fit_members(X, y, member_rows, cfg: TrainConfig, seed_parts, device=None) ->
     rc = N.lib().mlt_train_members(N.ctx(device), N.C.byref(desc), N.ptr(ow1, N.C.c_double),
                                    N.ptr(ob1, N.C.c_double), N.ptr(ow2, N.C.c_double), N.ptr(ob2, N.C.c_double),
                                    N.ptr(lf, N.C.c_double), N.ptr(ll, N.C.c_double), N.ptr(div, N.C.c_int32))
-    if rc == N.MLT_EDIVERGED:
-        first = int(div[np.nonzero(div)[0][0]])
-        raise errors.active["DivergenceError"]("training loss became non-finite", epoch=first)
-    N.check(rc, "mlt_train_members")
-    return [Network(ow1[i], ob1[i], ow2[i], ob2[i], means[i], stds[i], float(lf[i]), float(ll[i]))
-            for i in range(k)]
+    if rc != N.MLT_EDIVERGED:
+        N.check(rc, "mlt_train_members")
+    out, i = [], 0
+    for job_meta in meta:
+        dj = div[i:i + len(job_meta)]
+        if dj.any():
+            out.append(errors.active["DivergenceError"]("training loss became non-finite",
+                                                        epoch=int(dj[np.nonzero(dj)[0][0]])))
+        else:
+            out.append([Network(ow1[i + q], ob1[i + q], ow2[i + q], ob2[i + q], mean, std, float(lf[i + q]),
+                                float(ll[i + q])) for q, (mean, std) in enumerate(job_meta)])
+        i += len(job_meta)
+    return out
 
 
 def train_network(samples, space, cfg: TrainConfig) -> Network:
@@ -314,10 +349,9 @@ def train_network(samples, space, cfg: TrainConfig) -> Network:
     return fit_members(X, y, [np.arange(X.shape[0])], cfg, [(cfg.seed, 0)])[0]
 
 
-def train_ensemble(samples, space, k: int = DEFAULT_BAG_COUNT, cfg: TrainConfig = TrainConfig(),
-                   jobs: int = 1) -> Ensemble:
-    """Fold-exclusion bagging (model.py:308-341); all k members train
-    concurrently on the device (`jobs` is accepted for API compatibility)."""
+def _ensemble_job(samples, space, k: int, cfg: TrainConfig):
+    """Everything train_ensemble computes on the host before the device fit:
+    (encoder, X, y, member rows, member seed parts) (model.py:308-341)."""
     if k < 1:
         raise ValueError("k must be >= 1")
     enc = Encoder.from_space(space)
@@ -330,8 +364,38 @@ def train_ensemble(samples, space, k: int = DEFAULT_BAG_COUNT, cfg: TrainConfig 
     else:
         folds = np.array_split(make_rng(cfg.seed).permutation(n), k)
         rows = [np.setdiff1d(np.arange(n), f, assume_unique=True) for f in folds]
-    members = fit_members(X, y, rows, cfg, [(cfg.seed, i) for i in range(k)])
-    return Ensemble(members, enc, space.name)
+    return enc, X, y, rows, [(cfg.seed, i) for i in range(k)]
+
+
+def train_ensemble(samples, space, k: int = DEFAULT_BAG_COUNT, cfg: TrainConfig = TrainConfig(),
+                   jobs: int = 1) -> Ensemble:
+    """Fold-exclusion bagging (model.py:308-341); all k members train
+    concurrently on the device (`jobs` is accepted for API compatibility)."""
+    enc, X, y, rows, parts = _ensemble_job(samples, space, k, cfg)
+    return Ensemble(fit_members(X, y, rows, cfg, parts), enc, space.name)
+
+
+def train_ensembles(requests, device=None) -> list:
+    """Many independent `train_ensemble(samples, space, k, cfg)` calls with
+    their members trained together: one device launch per distinct
+    (optimiser settings, input width). Returns, aligned with `requests`, an
+    Ensemble or the exception that call would have raised. Each result is
+    bit-identical to its own train_ensemble call (members are independent CTAs)."""
+    out = [None] * len(requests)
+    groups = {}
+    for q, (samples, space, k, cfg) in enumerate(requests):
+        try:
+            enc, X, y, rows, parts = _ensemble_job(samples, space, k, cfg)
+        except Exception as exc:   # ValueError / InsufficientDataError (ours or, install()ed, the reference's)
+            out[q] = exc
+            continue
+        key = (cfg.epochs, cfg.batch_size, cfg.learning_rate, cfg.momentum, X.shape[1])
+        groups.setdefault(key, []).append((q, enc, space.name, (X, y, rows, parts, cfg)))
+    for items in groups.values():
+        res = fit_member_batches([it[3] for it in items], device)
+        for (q, enc, name, _), r in zip(items, res):
+            out[q] = r if isinstance(r, Exception) else Ensemble(r, enc, name)
+    return out
 
 
 # -- persistence (schema v1, model.py:351-410) ----------------------------------------

@@ -204,6 +204,22 @@ class ParamSpace:
     def sample_random(self, n: int, seed: int) -> list:
         return self.configs_at(self.sample_indices(n, seed))
 
+    def iter_random_indices(self, seed: int):
+        """Prefix-stable seeded stream of distinct indices (paramspace.py:237-255):
+        a PCG64 permutation up to 2^22 configurations, else rejection sampling
+        in batches of 4096 against a seen-set."""
+        card = self.cardinality()
+        rng = make_rng(seed)
+        if card <= PERMUTATION_LIMIT:
+            yield from (int(i) for i in rng.permutation(card))
+            return
+        seen = set()
+        while len(seen) < card:
+            for i in rng.integers(0, card, size=4096).tolist():
+                if i not in seen:
+                    seen.add(i)
+                    yield i
+
 
 def decode_indices(space, indices, device=None) -> np.ndarray:
     idx = np.ascontiguousarray(indices, dtype=np.int64)

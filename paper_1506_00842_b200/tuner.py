@@ -125,6 +125,14 @@ def autotune(space, runner, cfg: TunerConfig, jobs: int = 1, sweep=None) -> Tuni
     """Sample -> measure -> train (device) -> sweep + top-M (device) -> re-measure
     -> best of stage 2 by (time, index) (tuner.py:134-188). `sweep` may replace
     the top-M function (e.g. the multi-GPU `distributed.top_m_predicted`)."""
+    stage1 = autotune_stage1(space, runner, cfg)
+    ens = train_ensemble(stage1, space, k=cfg.k_bag, cfg=cfg.resolved_train_cfg(), jobs=jobs)
+    return autotune_stage2(space, runner, cfg, stage1, ens, sweep)
+
+
+def autotune_stage1(space, runner, cfg: TunerConfig) -> SampleSet:
+    """The first half of autotune up to training: the seeded sample, measured,
+    with the valid-count check (tuner.py:145-151)."""
     if space.cardinality() < cfg.n_train:
         raise ValueError(f"n_train={cfg.n_train} exceeds space cardinality {space.cardinality()}")
     rid = getattr(runner, "runner_id", "runner")
@@ -133,7 +141,13 @@ def autotune(space, runner, cfg: TunerConfig, jobs: int = 1, sweep=None) -> Tuni
     if n_valid < cfg.k_bag:
         raise errors.active["InsufficientDataError"](
             f"stage 1 produced {n_valid} valid samples, need at least {cfg.k_bag}")
-    ens = train_ensemble(stage1, space, k=cfg.k_bag, cfg=cfg.resolved_train_cfg(), jobs=jobs)
+    return stage1
+
+
+def autotune_stage2(space, runner, cfg: TunerConfig, stage1, ens, sweep=None) -> TuningReport:
+    """The second half of autotune after training (tuner.py:155-188): device
+    sweep + top-M, re-measure, best by (time, index)."""
+    rid = getattr(runner, "runner_id", "runner")
     sweep = sweep or top_m_predicted
     cands = sweep(ens, space, cfg.m_candidates, cfg.max_prediction_sweep, cfg.seed)
     predicted = {space.index_of(c): p for c, p in cands}

@@ -101,9 +101,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--synth", action="store_true", help="run the full 1e8 reference sweep")
     ap.add_argument("--formats", action="store_true", help="only (re)write the on-disk format fixtures")
+    ap.add_argument("--eval", action="store_true", help="only (re)write the evaluation-harness fixture")
     args = ap.parse_args()
     if args.formats:
         return formats_fixtures()
+    if args.eval:
+        return eval_fixtures()
     t0 = time.time()
     spaces = {n: PS.builtin_space(n) for n in PS.BUILTIN_SPACE_NAMES}
     spaces["synthetic-1e8"] = synthetic_space()
@@ -256,6 +259,30 @@ def formats_fixtures():
     assert cli.main(["predict", "--model", str(OUT / "model_conv_k11.json"), "--index", "4242",
                      "--out", str(d / "pred_conv_4242.csv")]) == 0
     print("formats written to", d)
+
+
+def eval_fixtures():
+    """The reference's learning_curve / slowdown_grid / random_baseline on the
+    512-configuration test space (evaluation.py:110-251), default training."""
+    import conftest_ref
+    from mltune import evaluation as EV
+    sp = conftest_ref.make_space512()
+    spec = conftest_ref.make_surrogate512(noise_cv=0.05)
+    runner = M.SurrogateRunner(spec, sp, runner_id="s512")
+    t0 = time.time()
+    pts = EV.learning_curve(sp, runner, [40, 80, 160], repeats=2, seed=5, k=3, holdout_size=100)
+    cells = EV.slowdown_grid(sp, runner, [60, 120], [4, 16], repeats=2, seed=9, k=3)
+    rb = EV.random_baseline(sp, runner, 50, 3)
+    doc = {"learning_curve": [{"n_train": p.n_train, "mre": p.mre, "repeat_mres": list(p.repeat_mres),
+                               "failure_reasons": list(p.failure_reasons)} for p in pts],
+           "slowdown_grid": [{"n_train": c.n_train, "m_candidates": c.m_candidates, "mean_slowdown": c.mean_slowdown,
+                              "n_repeats": c.n_repeats, "invalid_run_count": c.invalid_run_count} for c in cells],
+           "random_baseline": {"config": list(rb[0]), "time": rb[1]},
+           "surrogate": M.surrogate_to_json(spec),
+           "args": {"learning_curve": [[40, 80, 160], 2, 5, 3, 100], "slowdown_grid": [[60, 120], [4, 16], 2, 9, 3],
+                    "random_baseline": [50, 3], "noise_cv": 0.05}}
+    (OUT / "eval_bench512.json").write_text(json.dumps(doc, indent=1))
+    print("eval fixtures", time.time() - t0)
 
 
 def slice_top(ens, sp, m, lo, hi):

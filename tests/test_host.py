@@ -182,3 +182,15 @@ def test_surrogate_spec_packing():
     assert list(pk.kind[:pk.c.n_rules]) == [0] * pk.c.n_rules      # gpu-a: max-product launch limits
     noiseless = PackedSurrogate(dict(doc, noise_cv=0.0), sp)
     assert noiseless.c.log_sigma == 0.0
+
+
+@pytest.mark.parametrize("name", ["bench512", "synthetic-1e8"])
+def test_iter_random_indices_prefix_stable(name):
+    """paramspace.py:237-255: the stream equals sample_indices' draw (permutation
+    below 2^22 configurations, rejection sampling above) and is prefix-stable."""
+    import itertools
+    sp = product_space(name)
+    head = list(itertools.islice(sp.iter_random_indices(17), 300))
+    assert head == sp.sample_indices(300, 17).tolist()
+    assert list(itertools.islice(sp.iter_random_indices(17), 120)) == head[:120]
+    assert len(set(head)) == 300
