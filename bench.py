@@ -189,6 +189,35 @@ def train_bench(space_name, with_cpu=True):
     return out
 
 
+def autotune_quality(space_name):
+    """The metric's second half — measured runtime of the tuner's pick vs the
+    exhaustive best — on the workload's surrogate device (the golden spec, as
+    the reference's SurrogateRunner would measure it), entirely on the B200:
+    the fused exhaustive search over the whole space, then autotune with
+    N = 2000, M = 200, k = 16 (stage 1 on the device surrogate, device
+    training, device sweep, stage 2)."""
+    import paper_1506_00842_b200 as b
+    from paper_1506_00842_b200.space import space_from_json
+    sp = space_from_json(json.loads((GOLDEN / "spaces.json").read_text())[space_name])
+    runner = b.B200SurrogateRunner(json.loads((GOLDEN / "surrogates.json").read_text())[space_name], sp,
+                                   runner_id="gpu-a-synth")
+    runner.exhaustive_best(0, 1 << 20)                                   # warm-up
+    t0 = time.perf_counter()
+    best_i, best_t, n_valid, _ = runner.exhaustive_best()
+    ex_s = time.perf_counter() - t0
+    k = 16 if space_name == "synthetic-1e8" else 8
+    t0 = time.perf_counter()
+    rep = b.autotune(sp, runner, b.TunerConfig(n_train=2000, m_candidates=200, k_bag=k, seed=0))
+    at_s = time.perf_counter() - t0
+    _, _, _, rank = runner.exhaustive_best(threshold=rep.best_time)
+    return {"runner": "device surrogate (golden spec of the workload)", "n_train": 2000, "m": 200, "k": k,
+            "exhaustive": {"best_index": best_i, "best_time_s": best_t, "valid": n_valid, "wall_s": ex_s,
+                           "configs_per_s": sp.cardinality() / ex_s},
+            "tuned": {"best_index": rep.best_index, "best_time_s": rep.best_time, "wall_s": at_s,
+                      "faster_configs_in_space": rank},
+            "slowdown_vs_exhaustive": rep.best_time / best_t}
+
+
 def run_reference(args, rank):
     """The reference's CPU path on this host: every step is the reference
     top-m sweep (tuner.py:95-131, via the oracle port) over a fresh contiguous
@@ -387,6 +416,7 @@ def main():
             line["cpu_baseline"].pop("seconds")
         if world == 1 and not args.no_train:
             line["train"] = train_bench(args.workload, with_cpu=not args.no_cpu_baseline)
+            line["autotune_vs_exhaustive"] = autotune_quality(args.workload)
         print(json.dumps(line), flush=True)
     N.lib().mlt_plan_destroy(plan)
     if world > 1:
