@@ -78,3 +78,43 @@ def top_m_predicted(ensemble, space, m: int, sweep_cap=None, seed: int = 0, grou
         return single(ensemble, space, m, sweep_cap, seed)
     idx, pred = top_m_arrays_sharded(ensemble, space, m, group)
     return [(space.config_at(int(i)), float(p)) for i, p in zip(idx, pred)]
+
+
+def exhaustive_best_sharded(runner, space, group=None, repetitions=None, local_fn=None):
+    """Exhaustive search (tuner.py:191-224) over the ranks of `group`: rank r
+    runs the fused device search (`runner.exhaustive_best`) on its slice, one
+    all-gather moves 4 numbers per rank (best time, best index, valid count),
+    and every rank picks the (time, index) minimum — identical to the
+    single-GPU search. Returns (best index or -1, best time, total valid)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    lo, hi = shard_bounds(space.cardinality(), rank, world)
+    fn = local_fn or (lambda a, b: runner.exhaustive_best(a, b, repetitions))
+    i, t, nv, _ = fn(lo, hi)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    mine = torch.tensor([t if i >= 0 else float("inf"), float(i), float(nv)], dtype=torch.float64, device=dev)
+    allv = torch.empty(world * 3, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    v = allv.cpu().numpy().reshape(world, 3)
+    total = int(v[:, 2].sum())
+    ok = v[:, 1] >= 0
+    if not ok.any():
+        return -1, float("nan"), total
+    cand = sorted((float(tt), int(ii)) for tt, ii in zip(v[ok, 0], v[ok, 1]))
+    return cand[0][1], cand[0][0], total
+
+
+def exhaustive_search(space, runner, group=None):
+    """Drop-in for tuner.exhaustive_search across ranks when the runner has a
+    fused device search; any other runner falls back to the single-rank path."""
+    from . import errors
+    from .tuner import exhaustive_search as single
+    if not hasattr(runner, "exhaustive_best"):
+        return single(space, runner)
+    i, t, _ = exhaustive_best_sharded(runner, space, group)
+    if i < 0:
+        raise errors.active["EmptySpaceError"](f"space {space.name!r} has no valid configuration")
+    return space.config_at(i), t

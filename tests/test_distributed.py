@@ -84,3 +84,55 @@ def test_shard_bounds_partition_the_space():
             bounds = [shard_bounds(card, r, world) for r in range(world)]
             assert bounds[0][0] == 0 and bounds[-1][1] == card
             assert all(bounds[r][1] == bounds[r + 1][0] for r in range(world - 1))
+
+
+def _ex_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+    from conftest import oracle_space, surrogates_doc
+    from oracle.surrogate import OSurrogate
+    from paper_1506_00842_b200.distributed import exhaustive_best_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        osp = oracle_space("convolution")
+        ora = OSurrogate(surrogates_doc()["convolution"], osp)
+
+        class SpaceView:
+            def cardinality(self):
+                return osp.card
+
+        def local(lo, hi):         # the oracle slice search standing in for the device kernel
+            idx = np.arange(lo, hi, dtype=np.int64)
+            t, ok = ora.measured_times(idx, 1)
+            if not ok.any():
+                return -1, float("nan"), 0, 0
+            tt = np.where(ok, t, np.inf)
+            p = int(np.argmin(tt))
+            return int(idx[p]), float(tt[p]), int(ok.sum()), 0
+
+        q.put((rank,) + tuple(exhaustive_best_sharded(None, SpaceView(), local_fn=local)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_exhaustive_equals_single(world):
+    """the conv gpu-a optimum is index 88599 — from any shard count."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ex_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, i, t, nv in res:
+        assert i == 88599 and abs(t - 0.014444711) < 1e-8 and nv > 0

@@ -164,3 +164,53 @@ def test_spec_errors(gpu_ok):
     t, ok = r.true_times(np.arange(10))
     assert ok.all() and (t == 2.0).all()          # a value not in the list never matches
     assert spaces_doc()["convolution"]["name"] == "convolution"
+
+
+def _sharded_worker(rank, world, port, q):
+    import os
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch
+    import torch.distributed as dist
+    from conftest import product_space, surrogates_doc
+    from paper_1506_00842_b200 import B200SurrogateRunner
+    from paper_1506_00842_b200.distributed import exhaustive_search
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)                 # functional run: both ranks share the one B200
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sp = product_space("synthetic-1e8")
+        r = B200SurrogateRunner(surrogates_doc()["synthetic-1e8"], sp)
+        cfg, t = exhaustive_search(sp, r)
+        q.put((rank, sp.index_of(cfg), t))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_exhaustive_on_device(gpu_ok):
+    """distributed.exhaustive_search over 2 gloo ranks (device search per slice,
+    one all-gather) == the single-GPU fused search of the 10^8 space."""
+    import socket
+
+    import torch.multiprocessing as mp
+    dev, _ = _runners("synthetic-1e8")
+    i1, t1, _, _ = dev.exhaustive_best()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, i, t in res:
+        assert i == i1 and t == t1, rank
