@@ -202,6 +202,15 @@ MLT_API int mlt_train_members(mlt_ctx* ctx, const mlt_train_desc* desc, double* 
                       double* w2, double* b2, double* loss_first, double* loss_final,
                       int32_t* diverged_epoch);
 
+/* Host helper for A10's draws (model.py:218): `count` successive
+ * `rng.permutation(n[g])` results of each of n_gen numpy Generators, written
+ * generator-major to out (count * n[g] int32 each). bitgens[g] is numpy's
+ * bitgen_t* (`Generator.bit_generator.ctypes.bit_generator`): the bits come
+ * from numpy's own PCG64 and advance its state exactly as numpy would. Runs
+ * on `threads` host threads (0 = all); no GPU involved. */
+MLT_API int mlt_host_permutations(void* const* bitgens, int32_t n_gen, const int32_t* n, int32_t count,
+                                  int32_t* out, int32_t threads);
+
 /* ---------------------------------------------------------------------------
  * A12: the analytic surrogate device (SurrogateSpec / SurrogateRunner,
  * measurement.py:146-238): base time x matching term factors (in spec order),

@@ -252,13 +252,38 @@ def _valid_rows(samples, encoder: Encoder):
 
 def _member_draws(n: int, d: int, cfg: TrainConfig, seed_parts):
     """Every random draw of one `_fit` in the reference's order (model.py:204-218)."""
-    rng = make_rng(*seed_parts)
-    w1 = rng.uniform(-0.5, 0.5, (HIDDEN_UNITS, d)) * cfg.weight_init_scale
-    w2 = rng.uniform(-0.5, 0.5, HIDDEN_UNITS) * cfg.weight_init_scale
-    perms = np.empty((cfg.epochs, n), dtype=np.int32)
-    for e in range(cfg.epochs):
-        perms[e] = rng.permutation(n)
-    return w1, w2, perms
+    return _member_draws_many([(n, d, cfg, seed_parts)])[0]
+
+
+def _member_draws_many(specs):
+    """`_member_draws` for many members: the W1 / w2 uniforms per member in
+    numpy, then every member's per-epoch permutations in one native call
+    (numpy's own bit generators driven from host threads, bit-identical)."""
+    rngs, inits = [], []
+    for n, d, cfg, seed_parts in specs:
+        rng = make_rng(*seed_parts)
+        w1 = rng.uniform(-0.5, 0.5, (HIDDEN_UNITS, d)) * cfg.weight_init_scale
+        w2 = rng.uniform(-0.5, 0.5, HIDDEN_UNITS) * cfg.weight_init_scale
+        rngs.append(rng)
+        inits.append((w1, w2))
+    out = []
+    by_epochs = {}
+    for q, (n, d, cfg, _) in enumerate(specs):
+        by_epochs.setdefault(cfg.epochs, []).append(q)
+    perms = [None] * len(specs)
+    for epochs, qs in by_epochs.items():
+        ns = np.ascontiguousarray([specs[q][0] for q in qs], dtype=np.int32)
+        buf = np.empty(int(ns.sum()) * epochs, dtype=np.int32)
+        gens = (N.C.c_void_p * len(qs))(*[rngs[q].bit_generator.ctypes.bit_generator.value for q in qs])
+        rc = N.lib().mlt_host_permutations(gens, len(qs), N.ptr(ns, N.C.c_int32), epochs, N.ptr(buf, N.C.c_int32), 0)
+        N.check(rc, "mlt_host_permutations")
+        at = 0
+        for q, nq in zip(qs, ns.tolist()):
+            perms[q] = buf[at:at + epochs * nq].reshape(epochs, nq)
+            at += epochs * nq
+    for (w1, w2), pm in zip(inits, perms):
+        out.append((w1, w2, pm))
+    return out
 
 
 def fit_members(X, y, member_rows, cfg: TrainConfig, seed_parts, device=None) -> list:
@@ -281,6 +306,7 @@ def fit_member_batches(jobs, device=None) -> list:
     cfg = jobs[0][4]
     opt = (cfg.epochs, cfg.batch_size, cfg.learning_rate, cfg.momentum)
     xs, ts, rows_all, n_m, iw1s, iw2s, perms, meta = [], [], [], [], [], [], [], []
+    draw_specs = []
     row_base = 0
     for X, y, member_rows, seed_parts, jcfg in jobs:
         if X.shape[1] != d:
@@ -297,14 +323,15 @@ def fit_member_batches(jobs, device=None) -> list:
                 std = 1.0
             ts.append((targets - mean) / std)
             job_meta.append((mean, std))
-            w1, w2, pm = _member_draws(len(rows), d, jcfg, sp)
-            iw1s.append(w1)
-            iw2s.append(w2)
-            perms.append(pm.ravel())
+            draw_specs.append((len(rows), d, jcfg, sp))
             rows_all.append(np.asarray(rows) + row_base)
             n_m.append(len(rows))
         meta.append(job_meta)
         row_base += X.shape[0]
+    for w1, w2, pm in _member_draws_many(draw_specs):
+        iw1s.append(w1)
+        iw2s.append(w2)
+        perms.append(pm.ravel())
     k = len(n_m)
     x = np.ascontiguousarray(np.concatenate(xs))
     t = np.ascontiguousarray(np.concatenate(ts))

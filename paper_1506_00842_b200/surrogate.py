@@ -121,6 +121,19 @@ class B200SurrogateRunner:
             return Sample(tuple(config), Outcome.invalid(STATUS_INVALID_LAUNCH), reps)
         return Sample(tuple(config), Outcome.valid(float(times[0])), reps)
 
+    def measure_many(self, configs, repetitions: int | None = None) -> list:
+        """`measure` of many configurations in one device call (same results)."""
+        reps = self.default_repetitions if repetitions is None else repetitions
+        if reps < 1:
+            raise ValueError("repetitions must be >= 1")
+        configs = [tuple(c) for c in configs]
+        if not configs:
+            return []
+        idx = np.fromiter((self.space.index_of(c) for c in configs), dtype=np.int64, count=len(configs))
+        times, ok = self.measured_times(idx, reps)
+        return [Sample(c, Outcome.valid(float(t)) if good else Outcome.invalid(STATUS_INVALID_LAUNCH), reps)
+                for c, t, good in zip(configs, times.tolist(), ok.tolist())]
+
     def exhaustive_best(self, begin: int = 0, end: int | None = None, repetitions: int | None = None,
                         threshold: float = math.nan):
         """Device exhaustive search over [begin, end): (best index or -1, best

@@ -110,14 +110,23 @@ def top_m_predicted(ensemble, space, m: int, sweep_cap: int | None = None, seed:
 
 
 def measure_configs(space, runner, configs, repetitions: int | None = None) -> list:
-    """Static invalids never reach the runner (tuner.py:80-92)."""
-    out = []
-    for config in configs:
+    """Static invalids never reach the runner (tuner.py:80-92). A runner with
+    `measure_many(configs, repetitions)` (the device surrogate) measures the
+    statically valid ones in one batch; otherwise one `measure` per config."""
+    reps_default = repetitions if repetitions is not None else getattr(runner, "default_repetitions", 1)
+    out = [None] * len(configs)
+    todo = []
+    for q, config in enumerate(configs):
         if space.is_statically_valid(config):
-            out.append(runner.measure(config, repetitions))
+            todo.append(q)
         else:
-            reps = repetitions if repetitions is not None else getattr(runner, "default_repetitions", 1)
-            out.append(Sample(config, Outcome.invalid(STATUS_INVALID_STATIC), reps))
+            out[q] = Sample(config, Outcome.invalid(STATUS_INVALID_STATIC), reps_default)
+    if hasattr(runner, "measure_many"):
+        for q, smp in zip(todo, runner.measure_many([configs[q] for q in todo], repetitions)):
+            out[q] = smp
+    else:
+        for q in todo:
+            out[q] = runner.measure(configs[q], repetitions)
     return out
 
 
