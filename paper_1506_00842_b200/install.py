@@ -24,7 +24,7 @@ def install(mltune_module=None) -> None:
     mt = mltune_module or importlib.import_module("mltune")
     ref_err = importlib.import_module(mt.__name__ + ".errors")
     for name in list(errors.active):
-        errors.active[name] = getattr(ref_err, name)
+        errors.active[name] = getattr(ref_err, name, errors.active[name])
     targets = [(mt.tuner, "top_m_predicted", tuner.top_m_predicted),
                (mt.tuner, "train_ensemble", model.train_ensemble),
                (mt.evaluation, "train_ensemble", model.train_ensemble),
