@@ -362,6 +362,13 @@ struct mlt_plan {
   DEns de{};
   bool factors_ok = false;
   std::map<int, BandSetup> setups;
+  // Factored tables of the last band sweep: a derived, resident layout of the
+  // weights for one (split, group, outer range); repeated sweeps of the same
+  // slice with this plan reuse them instead of rebuilding.
+  float* t_ea = nullptr;
+  float* t_ebp = nullptr;
+  size_t t_ea_cap = 0, t_ebp_cap = 0;
+  int64_t t_key[4] = {-1, -1, -1, -1};
 };
 
 namespace {
@@ -603,6 +610,9 @@ void plan_free(mlt_plan* p) {
     pool_free(c, kv.second.d_u);
   }
   p->setups.clear();
+  pool_free(c, p->t_ea);
+  pool_free(c, p->t_ebp);
+  p->t_ea = p->t_ebp = nullptr;
 }
 
 // fp64 materialise over a range or list, then sort: exact and general.
@@ -926,9 +936,29 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     float *ea, *ebp, *cval;
     int64_t* cidx;
     uint32_t* gs;
-    TRY(ws_t(c, S_EA, (size_t)n_ob * KH * kOB, &ea));
     const int ebw = B.G == 3 ? ebw_of(3) : (B.G == 2 ? ebw_of(2) : ebw_of(1));
-    TRY(ws_t(c, S_EBP, (size_t)n_ib * (KH / B.G) * kThreads * ebw * 4, &ebp));
+    const size_t n_ea = (size_t)n_ob * KH * kOB, n_ebp = (size_t)n_ib * (KH / B.G) * kThreads * ebw * 4;
+    const int64_t key[4] = {B.split, B.G, o_lo, n_ob};
+    const bool tables_cached = std::equal(key, key + 4, p->t_key);
+    if (!tables_cached) {
+      if (p->t_ea_cap < n_ea) {
+        pool_free(c, p->t_ea);
+        p->t_ea = nullptr;
+        p->t_ea_cap = 0;
+        CU(cudaMallocAsync(&p->t_ea, n_ea * 4, c->stream));
+        p->t_ea_cap = n_ea;
+      }
+      if (p->t_ebp_cap < n_ebp) {
+        pool_free(c, p->t_ebp);
+        p->t_ebp = nullptr;
+        p->t_ebp_cap = 0;
+        CU(cudaMallocAsync(&p->t_ebp, n_ebp * 4, c->stream));
+        p->t_ebp_cap = n_ebp;
+      }
+      std::fill(p->t_key, p->t_key + 4, -1);   // valid again only once the tables below are built
+    }
+    ea = p->t_ea;
+    ebp = p->t_ebp;
     TRY(ws_t(c, S_GSCAL, 8, &gs));
     TRY(ws_t(c, S_CIDX, (size_t)c->cand_cap, &cidx));
     TRY(ws_t(c, S_CVAL, (size_t)c->cand_cap, &cval));
@@ -957,7 +987,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     hs[0] = 0xFF800000u;   // fkey(+inf)
     hs[1] = 0u;
     CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
-    {
+    if (!tables_cached) {
       // two-level split of each side: lo = trailing parameters with <= 64 combinations
       auto lo_split = [&](int p_lo, int p_hi, int* sa, int64_t* nlo) {
         int64_t n = 1;
@@ -1000,6 +1030,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       void (*tin)(TableArgs) = B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
       tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads * 4 * ebw, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
+      std::copy(key, key + 4, p->t_key);
     }
 
     SweepArgs sa;
