@@ -218,6 +218,49 @@ def autotune_quality(space_name):
             "slowdown_vs_exhaustive": rep.best_time / best_t}
 
 
+def seed_variance(space_name, steps=5):
+    """throughput with ensembles trained from seeds 1-4 (device
+    trainer, same stage-1 sample): full-space top-200 step time per seed, the
+    guard band's size, and a cross-check of each top-200 against the exact
+    fp64 materialising path on the device."""
+    import paper_1506_00842_b200 as b
+    from paper_1506_00842_b200 import _native as N
+    from paper_1506_00842_b200.space import space_from_json
+    sp = space_from_json(json.loads((GOLDEN / "spaces.json").read_text())[space_name])
+    st = np.load(GOLDEN / f"stage1_{space_name}.npz")
+    samples = b.SampleSet(sp, "golden", tuple(
+        b.Sample(sp.config_at(int(i)), b.Outcome.valid(float(t)) if ok else b.Outcome.invalid("invalid-launch"))
+        for i, ok, t in zip(st["idx"], st["ok"], st["time"])))
+    k = 16 if space_name == "synthetic-1e8" else 8
+    ens = b.model.train_ensembles([(samples, sp, k, b.TrainConfig(seed=s)) for s in (1, 2, 3, 4)])
+    ctx = N.ctx(0)
+    N.check(N.lib().mlt_ctx_set_profiling(ctx, 1))
+    out = {}
+    for seed, e in zip((1, 2, 3, 4), ens):
+        ps, pe = N.packed(sp, "space"), N.packed(e, "ensemble")
+        plan = N.C.c_void_p()
+        N.check(N.lib().mlt_plan_create(ctx, N.C.byref(ps.c), N.C.byref(pe.c), N.C.byref(plan)))
+        oi, op, on, stt = np.empty(M_TOP, np.int64), np.empty(M_TOP), N.C.c_int64(), N.MltSweepStats()
+        tot = []
+        for r in range(steps + 2):
+            N.check(N.lib().mlt_plan_top_m(plan, M_TOP, 0, sp.cardinality(), N.ptr(oi, N.C.c_int64),
+                                           N.ptr(op, N.C.c_double), N.C.byref(on), N.C.byref(stt)))
+            if r >= 2:
+                tot.append(stt.total_ms)
+        N.lib().mlt_plan_destroy(plan)
+        # exact cross-check on a 2^22 slice: guard-band path vs fp64 materialise + sort
+        lo, hi = 37_000_000, 37_000_000 + (1 << 22)
+        a = b.top_m_arrays(e, sp, M_TOP, begin=lo, end=hi)
+        N.check(N.lib().mlt_ctx_set_option(ctx, 1, 1))          # MLT_OPT_PATH = exact
+        x = b.top_m_arrays(e, sp, M_TOP, begin=lo, end=hi)
+        N.check(N.lib().mlt_ctx_set_option(ctx, 1, -1))
+        out[str(seed)] = {"ms_per_step": float(np.median(tot)), "configs_per_s": sp.cardinality() / np.median(tot) * 1e3,
+                          "candidates": int(stt.candidates), "delta": stt.delta, "group": int(stt.group),
+                          "slice_top200_equals_exact_path": bool(np.array_equal(a[0], x[0]))}
+    N.check(N.lib().mlt_ctx_set_profiling(ctx, 0))
+    return out
+
+
 def run_reference(args, rank):
     """The reference's CPU path on this host: every step is the reference
     top-m sweep (tuner.py:95-131, via the oracle port) over a fresh contiguous
@@ -417,6 +460,7 @@ def main():
         if world == 1 and not args.no_train:
             line["train"] = train_bench(args.workload, with_cpu=not args.no_cpu_baseline)
             line["autotune_vs_exhaustive"] = autotune_quality(args.workload)
+            line["seed_variance"] = seed_variance(args.workload)
         print(json.dumps(line), flush=True)
     N.lib().mlt_plan_destroy(plan)
     if world > 1:
