@@ -10,6 +10,7 @@
 // the reference step sequence exactly; arithmetic mirrors the reference's
 // rounding sequence (separate multiplies/subtractions where numpy does them),
 // leaving only BLAS summation-order differences (~1e-16 relative per step).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -35,6 +36,11 @@ struct TrainArgs {
   const int* perms;              // per member: epochs x n_m
   const double* iw1;             // [k][h][d]
   const double* iw2;             // [k][h]
+  // compact features: x[r][p] == ftab[foff[p] + codes[r*d + p]] (every column has <= 256 values)
+  const uint8_t* codes;          // [n_rows][d] or null
+  const double* ftab;
+  int foff[kTMaxD + 1];
+  int smem_rows;                 // rows staged per member (0: read x / t from global memory)
   double *ow1, *ob1, *ow2, *ob2, *lfirst, *llast;
   int* div_epoch;
 };
@@ -45,7 +51,22 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a) {
+// dynamic shared memory: part [kTW][kTMaxD + 2][32] doubles, then (SMEM) the
+// member's targets [n] doubles, the feature table, and its codes [n][d] bytes
+size_t train_smem(const TrainArgs& a, int n_max, int ftab_n) {
+  size_t b = sizeof(double) * kTW * (kTMaxD + 2) * 32;
+  if (a.smem_rows) b += sizeof(double) * ((size_t)n_max + ftab_n) + (size_t)n_max * a.d;
+  return (b + 15) & ~(size_t)15;
+}
+
+// SMEM: the member's rows live in shared memory as 1-byte feature codes (+ a
+// small fp64 table) and its targets as fp64, so a step's only global access
+// is the permutation chunk, prefetched one step ahead. Rows of a warp are
+// processed with instruction-level parallelism (8 independent forward
+// chains, interleaved butterflies); per-row arithmetic and every
+// accumulation order are unchanged.
+template <bool SMEM>
+__global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a, int ftab_n) {
   const int m = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int d = a.d, h = a.h;
@@ -56,13 +77,15 @@ __global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a) {
 
   __shared__ double W1[kTMaxD][32], V1[kTMaxD][32];
   __shared__ double B1[32], VB1[32], W2[32], VW2[32];
-  extern __shared__ double part_raw[];   // [kTW][kTMaxD + 2][32] (dynamic: > 48 KB static limit)
-  auto part = reinterpret_cast<double(*)[kTMaxD + 2][32]>(part_raw);
+  extern __shared__ double dyn[];
+  auto part = reinterpret_cast<double(*)[kTMaxD + 2][32]>(dyn);
+  double* s_t = dyn + kTW * (kTMaxD + 2) * 32;      // SMEM: [n] targets
+  double* s_f = s_t + (SMEM ? n : 0);                // SMEM: feature table
+  uint8_t* s_c = reinterpret_cast<uint8_t*>(s_f + (SMEM ? ftab_n : 0));   // SMEM: [n][d] codes
   __shared__ double pscal[kTW][2];            // per-warp (sum dout, sum r^2)
   __shared__ double xs[kTW][kRowsPerWarp][kTMaxD];
   __shared__ double ts[kTW][kRowsPerWarp];
   __shared__ double s_b2, s_vb2, s_sse;
-  __shared__ int s_stop;
 
   for (int q = tid; q < kTMaxD * 32; q += blockDim.x) {
     const int p = q / 32, j = q % 32;
@@ -78,7 +101,14 @@ __global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a) {
   if (tid == 0) {
     s_b2 = 0.0;
     s_vb2 = 0.0;
-    s_stop = 0;
+  }
+  if (SMEM) {
+    for (int q = tid; q < n; q += blockDim.x) s_t[q] = T[q];
+    for (int q = tid; q < ftab_n; q += blockDim.x) s_f[q] = a.ftab[q];
+    for (int q = tid; q < n * d; q += blockDim.x) {
+      const int ex = q / d, p = q - ex * d;
+      s_c[q] = a.codes[(size_t)R[ex] * d + p];
+    }
   }
   __syncthreads();
   const bool active = lane < h;
@@ -88,6 +118,8 @@ __global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a) {
   for (int e = 1; e <= a.epochs; ++e) {
     const int* perm = PERM + (size_t)(e - 1) * n;
     if (tid == 0) s_sse = 0.0;
+    int pf = 0;   // SMEM: prefetched permutation entry of this lane's row in the next chunk
+    if (SMEM && lane < max(0, min(kRowsPerWarp, min(a.B, n) - warp * kRowsPerWarp))) pf = perm[warp * kRowsPerWarp + lane];
     for (int s = 0; s < n; s += a.B) {
       const int mb = min(a.B, n - s);
       const double c2m = 2.0 / (double)mb;
@@ -100,32 +132,101 @@ __global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a) {
         const int rbase = c0 + warp * kRowsPerWarp;
         const int nr = max(0, min(kRowsPerWarp, mb - rbase));
         // stage this warp's rows (features + targets)
-        for (int q = lane; q < nr * d; q += 32) {
-          const int rr = q / d, p = q - rr * d;
-          const int ex = perm[s + rbase + rr];
-          xs[warp][rr][p] = a.x[(size_t)R[ex] * d + p];
+        if (SMEM) {
+          // this chunk's permutation entries were prefetched one chunk ahead
+          // (the permutations stream from DRAM: a dependent load per step
+          // would put its latency on the critical path)
+          const int ex_l = pf;
+          {
+            int ns = s, nc = c0 + 32;
+            if (nc >= mb) {
+              ns = s + a.B;
+              nc = 0;
+            }
+            const int nrb = nc + warp * kRowsPerWarp;
+            const int nmb = min(a.B, n - ns);
+            pf = (ns < n && lane < max(0, min(kRowsPerWarp, nmb - nrb))) ? __ldcs(perm + ns + nrb + lane) : 0;
+          }
+          for (int base = 0; base < nr * d; base += 32) {   // uniform trip count: every lane shuffles
+            const int q = base + lane;
+            const int rr = q < nr * d ? q / d : 0, p = q - rr * d;
+            const int ex = __shfl_sync(0xffffffffu, ex_l, rr);
+            if (q < nr * d) xs[warp][rr][p] = s_f[a.foff[p] + s_c[ex * d + p]];
+          }
+          if (lane < nr) ts[warp][lane] = s_t[ex_l];
+        } else {
+          for (int q = lane; q < nr * d; q += 32) {
+            const int rr = q / d, p = q - rr * d;
+            const int ex = perm[s + rbase + rr];
+            xs[warp][rr][p] = a.x[(size_t)R[ex] * d + p];
+          }
+          if (lane < nr) ts[warp][lane] = T[perm[s + rbase + lane]];
         }
-        if (lane < nr) ts[warp][lane] = T[perm[s + rbase + lane]];
         __syncwarp();
-        for (int rr = 0; rr < nr; ++rr) {
-          double z = 0.0;
+        if (nr == kRowsPerWarp) {
+          // forward of 8 rows, interleaved
+          double z[kRowsPerWarp];
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerWarp; ++rr) z[rr] = 0.0;
 #pragma unroll
           for (int p = 0; p < kTMaxD; ++p)
-            if (p < d) z = fma(xs[warp][rr][p], W1[p][lane], z);
-          z = __dadd_rn(z, b1j);
-          const double hj = 1.0 / (1.0 + exp(-z));
-          const double out = __dadd_rn(warp_sum(active ? hj * w2j : 0.0), b2);
-          const double r = __dsub_rn(out, ts[warp][rr]);
-          const double dout = __dmul_rn(c2m, r);
-          sse = fma(r, r, sse);
-          gb2 = __dadd_rn(gb2, dout);
+            if (p < d) {
+              const double w = W1[p][lane];
+#pragma unroll
+              for (int rr = 0; rr < kRowsPerWarp; ++rr) z[rr] = fma(xs[warp][rr][p], w, z[rr]);
+            }
+          double hj[kRowsPerWarp], o[kRowsPerWarp];
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+            hj[rr] = 1.0 / (1.0 + exp(-__dadd_rn(z[rr], b1j)));
+            o[rr] = active ? hj[rr] * w2j : 0.0;
+          }
+#pragma unroll
+          for (int sh = 16; sh > 0; sh >>= 1)
+#pragma unroll
+            for (int rr = 0; rr < kRowsPerWarp; ++rr) o[rr] += __shfl_xor_sync(0xffffffffu, o[rr], sh);
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+            const double r = __dsub_rn(__dadd_rn(o[rr], b2), ts[warp][rr]);
+            const double dout = __dmul_rn(c2m, r);
+            sse = fma(r, r, sse);
+            gb2 = __dadd_rn(gb2, dout);
+            if (active) {
+              gw2 = fma(hj[rr], dout, gw2);
+              const double dz = __dmul_rn(__dmul_rn(__dmul_rn(dout, w2j), hj[rr]), __dsub_rn(1.0, hj[rr]));
+              gb1 = __dadd_rn(gb1, dz);
+              z[rr] = dz;
+            }
+          }
           if (active) {
-            gw2 = fma(hj, dout, gw2);
-            const double dz = __dmul_rn(__dmul_rn(__dmul_rn(dout, w2j), hj), __dsub_rn(1.0, hj));
-            gb1 = __dadd_rn(gb1, dz);
 #pragma unroll
             for (int p = 0; p < kTMaxD; ++p)
-              if (p < d) gW[p] = fma(dz, xs[warp][rr][p], gW[p]);
+              if (p < d) {
+#pragma unroll
+                for (int rr = 0; rr < kRowsPerWarp; ++rr) gW[p] = fma(z[rr], xs[warp][rr][p], gW[p]);
+              }
+          }
+        } else {
+          for (int rr = 0; rr < nr; ++rr) {
+            double zz = 0.0;
+#pragma unroll
+            for (int p = 0; p < kTMaxD; ++p)
+              if (p < d) zz = fma(xs[warp][rr][p], W1[p][lane], zz);
+            zz = __dadd_rn(zz, b1j);
+            const double hh = 1.0 / (1.0 + exp(-zz));
+            const double out = __dadd_rn(warp_sum(active ? hh * w2j : 0.0), b2);
+            const double r = __dsub_rn(out, ts[warp][rr]);
+            const double dout = __dmul_rn(c2m, r);
+            sse = fma(r, r, sse);
+            gb2 = __dadd_rn(gb2, dout);
+            if (active) {
+              gw2 = fma(hh, dout, gw2);
+              const double dz = __dmul_rn(__dmul_rn(__dmul_rn(dout, w2j), hh), __dsub_rn(1.0, hh));
+              gb1 = __dadd_rn(gb1, dz);
+#pragma unroll
+              for (int p = 0; p < kTMaxD; ++p)
+                if (p < d) gW[p] = fma(dz, xs[warp][rr][p], gW[p]);
+            }
           }
         }
         __syncwarp();
@@ -280,6 +381,43 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
   cudaMemcpyAsync(diw2, D.init_w2, bytes_w2, cudaMemcpyHostToDevice, stream);
   TrainArgs a;
   std::memset(&a, 0, sizeof a);
+  // compact feature codes: every column of x takes few distinct values (digit / (count - 1))
+  std::vector<double> ftab;
+  std::vector<uint8_t> codes;
+  bool compact = D.d <= kTMaxD;
+  {
+    std::vector<std::vector<double>> cols(D.d);
+    for (int p = 0; compact && p < D.d; ++p) {
+      std::vector<double>& v = cols[p];
+      for (int64_t r = 0; r < D.n_rows; ++r) v.push_back(D.x[(size_t)r * D.d + p]);
+      std::sort(v.begin(), v.end(), [](double u, double w) { return u < w || (u == w && std::signbit(u) && !std::signbit(w)); });
+      v.erase(std::unique(v.begin(), v.end(), [](double u, double w) {
+                return std::memcmp(&u, &w, 8) == 0;
+              }), v.end());
+      if (v.size() > 256) compact = false;
+    }
+    if (compact) {
+      codes.resize((size_t)D.n_rows * D.d);
+      for (int p = 0; p < D.d; ++p) {
+        a.foff[p] = (int)ftab.size();
+        ftab.insert(ftab.end(), cols[p].begin(), cols[p].end());
+        for (int64_t r = 0; r < D.n_rows; ++r) {
+          const double xv = D.x[(size_t)r * D.d + p];
+          int c = -1;
+          for (size_t u = 0; u < cols[p].size(); ++u)
+            if (std::memcmp(&cols[p][u], &xv, 8) == 0) {
+              c = (int)u;
+              break;
+            }
+          if (c < 0) compact = false;
+          codes[(size_t)r * D.d + p] = (uint8_t)(c < 0 ? 0 : c);
+        }
+      }
+      a.foff[D.d] = (int)ftab.size();
+    }
+  }
+  int n_max = 0;
+  for (int m = 0; m < D.k; ++m) n_max = std::max(n_max, (int)D.n_m[m]);
   a.k = D.k;
   a.d = D.d;
   a.h = D.h;
@@ -303,9 +441,28 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
   a.lfirst = olf;
   a.llast = oll;
   a.div_epoch = odiv;
-  const int smem = (int)(sizeof(double) * kTW * (kTMaxD + 2) * 32);
-  cudaFuncSetAttribute(k_train, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_train<<<D.k, kTW * 32, smem, stream>>>(a);
+  a.smem_rows = compact ? 1 : 0;
+  size_t smem = train_smem(a, n_max, (int)ftab.size());
+  if (smem > 200 * 1024) {          // the member's rows do not fit: read them from global memory
+    a.smem_rows = 0;
+    smem = train_smem(a, n_max, 0);
+  }
+  uint8_t* dcodes = nullptr;
+  double* dftab = nullptr;
+  if (a.smem_rows) {
+    if ((e = cudaMallocAsync(&dcodes, codes.size() + ftab.size() * 8 + 16, stream)) != cudaSuccess) {
+      cudaFreeAsync(buf, stream);
+      return cuda_fail(e);
+    }
+    dftab = reinterpret_cast<double*>(dcodes + ((codes.size() + 15) & ~(size_t)15));
+    cudaMemcpyAsync(dcodes, codes.data(), codes.size(), cudaMemcpyHostToDevice, stream);
+    cudaMemcpyAsync(dftab, ftab.data(), ftab.size() * 8, cudaMemcpyHostToDevice, stream);
+    a.codes = dcodes;
+    a.ftab = dftab;
+  }
+  void (*kern)(TrainArgs, int) = a.smem_rows ? k_train<true> : k_train<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<D.k, kTW * 32, smem, stream>>>(a, (int)ftab.size());
   (*launches)++;
   e = cudaGetLastError();
   if (e == cudaSuccess) {
@@ -319,6 +476,7 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
     e = cudaStreamSynchronize(stream);
   }
   cudaFreeAsync(buf, stream);
+  if (dcodes) cudaFreeAsync(dcodes, stream);
   if (e != cudaSuccess) return cuda_fail(e);
   for (int m = 0; m < D.k; ++m)
     if (div[m] != 0) {

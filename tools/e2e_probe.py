@@ -11,7 +11,7 @@ from paper_1506_00842_b200.model import model_from_json
 from paper_1506_00842_b200.space import space_from_json
 G = ROOT / "tests" / "golden"
 name = sys.argv[1] if len(sys.argv) > 1 else "synthetic-1e8"
-case = {"synthetic-1e8": "synth_k16", "stereo": "stereo_k8"}[name]
+case = {"synthetic-1e8": "synth_k16", "stereo": "stereo_k8", "convolution": "conv_k11", "raycasting": "raycast_k11"}[name]
 sp = space_from_json(json.loads((G / "spaces.json").read_text())[name])
 ens = model_from_json(json.loads((G / f"model_{case}.json").read_text()))
 c = N.ctx(0)
