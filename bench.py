@@ -389,6 +389,26 @@ def main():
     ms_step = t[0].item() / args.steps
     value = card / (ms_step / 1e3)
 
+    # ---- the same step with exact bound-based pruning (MLT_OPT_PRUNE): reported
+    # beside the headline, which evaluates every configuration
+    pruned = None
+    if world == 1:
+        N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_PRUNE, 1))
+        for _ in range(args.warmup):
+            flush.zero_()
+            step()
+        pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for s_ in range(args.steps):
+            flush.zero_()
+            pev[s_][0].record(stream)
+            pres = step()
+            pev[s_][1].record(stream)
+        torch.cuda.synchronize()
+        N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_PRUNE, 0))
+        pms = sum(a.elapsed_time(b) for a, b in pev) / args.steps
+        pruned = {"ms_per_step": pms, "configs_per_s": card / (pms / 1e3), "evaluated_frac": st.evaluated_frac,
+                  "same_top200": bool(np.array_equal(np.asarray(pres[0]), np.asarray(res[0])))}
+
     # ---- e2e: public API from host objects (weights H2D + results D2H every step)
     N.check(N.lib().mlt_ctx_set_profiling(ctx, 0))
     e2e_api = (lambda: D.top_m_predicted(ens, space, M_TOP)) if world > 1 else \
@@ -450,6 +470,7 @@ def main():
             "candidates_rescored": int(np.mean(cands)),
             "guard_band": {"delta": st.delta, "group": st.group, "split_inner_params": st.split},
             "parity_top200_vs_reference": ok,
+            "pruned_sweep": pruned,
             "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step_median": 1e3 * statistics.median(e2e_times),
                     "ms_per_step_max": 1e3 * max(e2e_times)},

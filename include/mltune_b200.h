@@ -106,6 +106,7 @@ typedef struct mlt_sweep_stats {
   int32_t launches;            /* kernels launched by this call */
   int32_t split;               /* parameters in the inner (per-thread) factor */
   int64_t raw_candidates;      /* configurations the streaming band kept before the exact filter */
+  double evaluated_frac;       /* (configuration, unit) pairs evaluated / all: 1 without pruning */
 } mlt_sweep_stats;
 
 typedef struct mlt_ctx mlt_ctx;
@@ -128,6 +129,11 @@ MLT_API int64_t mlt_ctx_launches(mlt_ctx* ctx);
 #define MLT_OPT_PATH 1
 #define MLT_OPT_GROUP 2
 #define MLT_OPT_CAND_CAP 3
+/*   MLT_OPT_PRUNE     1 = exact bound-based pruning in the fp32 sweep: a work item whose
+ *                     partial sums plus a rigorous lower bound of the remaining hidden
+ *                     units exceed the threshold stops early (same top-m; fewer
+ *                     configurations fully evaluated). 0 (default) = evaluate all.   */
+#define MLT_OPT_PRUNE 4
 MLT_API int mlt_ctx_set_option(mlt_ctx* ctx, int key, int64_t value);
 
 /* A1: values[n][P] = decode(idx[n]).                 paramspace.py:184-193 */

@@ -21,7 +21,7 @@ from . import errors
 _LIB_PATH = Path(os.environ.get("MLTUNE_B200_LIB", Path(__file__).resolve().parent / "libmltune_b200.so"))
 
 MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
-MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP = 1, 2, 3
+MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE = 1, 2, 3, 4
 RULE_KIND = {"max-product": 0, "max-weighted-sum": 1, "forbidden-combination": 2}
 
 _i32p = C.POINTER(C.c_int32)
@@ -44,7 +44,8 @@ class MltEnsemble(C.Structure):
 class MltSweepStats(C.Structure):
     _fields_ = [("configs", C.c_int64), ("candidates", C.c_int64), ("path", C.c_int32), ("group", C.c_int32),
                 ("delta", C.c_double), ("sweep_ms", C.c_float), ("total_ms", C.c_float),
-                ("launches", C.c_int32), ("split", C.c_int32), ("raw_candidates", C.c_int64)]
+                ("launches", C.c_int32), ("split", C.c_int32), ("raw_candidates", C.c_int64),
+                ("evaluated_frac", C.c_double)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

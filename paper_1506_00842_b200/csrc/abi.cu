@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -57,7 +58,7 @@ struct mlt_ctx {
   cudaStream_t stream = nullptr;
   bool prof = false;
   int64_t launches = 0;
-  int opt_path = -1, opt_group = -1;
+  int opt_path = -1, opt_group = -1, opt_prune = 0;
   int64_t cand_cap = 1 << 20;
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
   std::vector<size_t> sizes = std::vector<size_t>(32, 0);
@@ -342,6 +343,7 @@ struct BandSetup {
   int split = 0, G = 3, dummies = 0;
   int64_t c_in = 1, c_in_pad = kInnerBlock;
   double delta = 0, cst = 0;
+  double mag = 0;               // sum |w'| + dummies + |cst|: scale of every partial sum
   double* d_tab = nullptr;      // [ca | cb | wprime] (k*kH each)
   float* d_u = nullptr;         // [k*kH] 1/w'
 };
@@ -361,14 +363,19 @@ struct mlt_plan {
   DSpace ds{};
   DEns de{};
   bool factors_ok = false;
+  std::vector<int> unit_of;     // table position -> original unit m*kH + j
+  int* d_unit_of = nullptr;
   std::map<int, BandSetup> setups;
   // Factored tables of the last band sweep: a derived, resident layout of the
   // weights for one (split, group, outer range); repeated sweeps of the same
   // slice with this plan reuse them instead of rebuilding.
   float* t_ea = nullptr;
   float* t_ebp = nullptr;
-  size_t t_ea_cap = 0, t_ebp_cap = 0;
-  int64_t t_key[4] = {-1, -1, -1, -1};
+  float* t_remlo = nullptr;     // pruning bounds [outer][checkpoint]
+  int* t_order = nullptr;       // pruning: outer blocks in ascending order of their lower bound
+  size_t t_order_cap = 0;
+  size_t t_ea_cap = 0, t_ebp_cap = 0, t_remlo_cap = 0;
+  int64_t t_key[5] = {-1, -1, -1, -1, -1};
 };
 
 namespace {
@@ -418,9 +425,11 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   std::vector<float> u(KH, 1.0f);
   double S = 0, log2dmax = -1e300, log2dmin = 1e300;
   int dummies = 0;
-  for (int m = 0; m < e.k; ++m) {
-    for (int j = 0; j < kH; ++j) {
-      const int mj = m * kH + j;
+  // table position `mj` holds original unit unit_of[mj] (plan_factors' order)
+  for (int pos = 0; pos < KH; ++pos) {
+    {
+      const int mj = pos;
+      const int m = p->unit_of[pos] / kH, j = p->unit_of[pos] % kH;
       const double wp = (j < e.h) ? e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k : 0.0;
       if (wp == 0.0) {
         ++dummies;                // contributes exactly 1/d' = 1/(Ea*0 + 1) = 1
@@ -480,6 +489,7 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   for (int m = 0; m < e.k; ++m) cst += (e.b2()[m] * e.sd()[m] + e.mean()[m]) / e.k;
   cst -= dummies;
   b.cst = cst;
+  b.mag = S + std::fabs(cst);
   const double uu = std::ldexp(1.0, -24);
   // A-priori |fp32 - exact| bound on the mean log:
   //  * each unit term 1/d' = w' sigma carries <= 4u relative error from the
@@ -533,6 +543,33 @@ int plan_factors(mlt_plan* p) {
   for (int q = 0; q < s.P; ++q) p->foff[q + 1] = p->foff[q] + s.radix[q];
   const int KH = e.k * kH;
   mlt_ctx* c = p->ctx;
+  // Unit order of every table: decreasing range of the unit's contribution
+  // over the whole space, |w'| * (sigmoid(zmax) - sigmoid(zmin)), so that the
+  // sweep's partial sums settle early (the pruning bounds of the remaining
+  // units are then tight); padding / zero-weight units last.
+  {
+    std::vector<double> range(KH, -1.0);
+    for (int mj = 0; mj < KH; ++mj) {
+      const int m = mj / kH, j = mj % kH;
+      if (j >= e.h) continue;
+      const double wp = e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k;
+      if (wp == 0.0) continue;
+      double zmin = e.b1()[(size_t)m * e.h + j], zmax = zmin;
+      const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
+      for (int q = 0; q < s.P; ++q)
+        if (s.radix[q] >= 2) {
+          zmin += std::min(0.0, w[q]);
+          zmax += std::max(0.0, w[q]);
+        }
+      auto sg = [](double z) { return 1.0 / (1.0 + std::exp(-z)); };
+      range[mj] = std::fabs(wp) * (sg(zmax) - sg(zmin));
+    }
+    p->unit_of.resize(KH);
+    for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = mj;
+    std::stable_sort(p->unit_of.begin(), p->unit_of.end(), [&](int x, int y) { return range[x] > range[y]; });
+    CU(cudaMallocAsync(&p->d_unit_of, (size_t)KH * 4, c->stream));
+    CU(cudaMemcpyAsync(p->d_unit_of, p->unit_of.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
+  }
   CU(cudaMallocAsync(&p->d_F, (size_t)KH * p->foff[s.P] * 8, c->stream));
   TableArgs ta;
   std::memset(&ta, 0, sizeof ta);
@@ -542,6 +579,7 @@ int plan_factors(mlt_plan* p) {
   for (int q = 0; q < s.P; ++q) ta.radix[q] = s.radix[q];
   for (int q = 0; q <= s.P; ++q) ta.foff[q] = p->foff[q];
   ta.w1 = p->de.w1;
+  ta.unit_of = p->d_unit_of;
   ta.F = p->d_F;
   k_table_factors<<<grid_for(c, (int64_t)KH * p->foff[s.P], 256), 256, 0, c->stream>>>(ta);
   TRY(check_launch(c));
@@ -605,6 +643,7 @@ void plan_free(mlt_plan* p) {
   pool_free(c, p->d_rcoeff);
   pool_free(c, p->d_ens);
   pool_free(c, p->d_F);
+  pool_free(c, p->d_unit_of);
   for (auto& kv : p->setups) {
     pool_free(c, kv.second.d_tab);
     pool_free(c, kv.second.d_u);
@@ -612,7 +651,10 @@ void plan_free(mlt_plan* p) {
   p->setups.clear();
   pool_free(c, p->t_ea);
   pool_free(c, p->t_ebp);
-  p->t_ea = p->t_ebp = nullptr;
+  pool_free(c, p->t_remlo);
+  pool_free(c, p->t_order);
+  p->t_ea = p->t_ebp = p->t_remlo = nullptr;
+  p->t_order = nullptr;
 }
 
 // fp64 materialise over a range or list, then sort: exact and general.
@@ -707,6 +749,7 @@ int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
     case MLT_OPT_PATH: c->opt_path = (int)value; return MLT_OK;
     case MLT_OPT_GROUP: c->opt_group = (int)value; return MLT_OK;
     case MLT_OPT_CAND_CAP: c->cand_cap = value < 0 ? (1 << 20) : std::max<int64_t>(value, 1); return MLT_OK;
+    case MLT_OPT_PRUNE: c->opt_prune = value == 1 ? 1 : 0; return MLT_OK;
     default: return fail(MLT_EINVAL, "unknown option %d", key);
   }
 }
@@ -898,6 +941,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
   *out_n = 0;
   mlt_sweep_stats local;
   std::memset(&local, 0, sizeof local);
+  local.evaluated_frac = 1.0;
   const int64_t l0 = c->launches;
   const int64_t card = p->hs.card_i;
   int64_t n;
@@ -938,9 +982,35 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     uint32_t* gs;
     const int ebw = B.G == 3 ? ebw_of(3) : (B.G == 2 ? ebw_of(2) : ebw_of(1));
     const size_t n_ea = (size_t)n_ob * KH * kOB, n_ebp = (size_t)n_ib * (KH / B.G) * kThreads * ebw * 4;
-    const int64_t key[4] = {B.split, B.G, o_lo, n_ob};
-    const bool tables_cached = std::equal(key, key + 4, p->t_key);
+    const bool prune = c->opt_prune == 1;
+    const int ngroups = KH / B.G;
+    CkList ck;
+    std::memset(&ck, 0, sizeof ck);
+    int ck_group[kMaxCk] = {0};
+    if (prune) {
+      ck_group[0] = 0;            // before any unit: the item's lower bound alone
+      ck.unit[0] = 0;
+      ck.n = 1;
+      for (int f = 5; f <= 19 && ck.n < kMaxCk; ++f) {   // every 5 % of the units from 25 %
+        const int g = (f * ngroups / 20) / 2 * 2;
+        if (g > 0 && g < ngroups && (ck.n == 0 || g > ck_group[ck.n - 1])) {
+          ck_group[ck.n] = g;
+          ck.unit[ck.n] = g * B.G;
+          ++ck.n;
+        }
+      }
+    }
+    const size_t n_remlo = prune ? (size_t)n_ob * kOB * n_ib * ck.n : 0;
+    const int64_t key[5] = {B.split, B.G, o_lo, n_ob, prune ? 1 : 0};
+    const bool tables_cached = std::equal(key, key + 5, p->t_key);
     if (!tables_cached) {
+      if (p->t_remlo_cap < n_remlo) {
+        pool_free(c, p->t_remlo);
+        p->t_remlo = nullptr;
+        p->t_remlo_cap = 0;
+        CU(cudaMallocAsync(&p->t_remlo, n_remlo * 4, c->stream));
+        p->t_remlo_cap = n_remlo;
+      }
       if (p->t_ea_cap < n_ea) {
         pool_free(c, p->t_ea);
         p->t_ea = nullptr;
@@ -955,7 +1025,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
         CU(cudaMallocAsync(&p->t_ebp, n_ebp * 4, c->stream));
         p->t_ebp_cap = n_ebp;
       }
-      std::fill(p->t_key, p->t_key + 4, -1);   // valid again only once the tables below are built
+      std::fill(p->t_key, p->t_key + 5, -1);   // valid again only once the tables below are built
     }
     ea = p->t_ea;
     ebp = p->t_ebp;
@@ -986,7 +1056,9 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     uint32_t* hs = static_cast<uint32_t*>(c->pinned);
     hs[0] = 0xFF800000u;   // fkey(+inf)
     hs[1] = 0u;
+    hs[4] = hs[5] = 0u;    // pruning work counter (64-bit at gs + 4)
     CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(gs + 4, hs + 4, 8, cudaMemcpyHostToDevice, c->stream));
     if (!tables_cached) {
       // two-level split of each side: lo = trailing parameters with <= 64 combinations
       auto lo_split = [&](int p_lo, int p_hi, int* sa, int64_t* nlo) {
@@ -1030,7 +1102,40 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       void (*tin)(TableArgs) = B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
       tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads * 4 * ebw, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
-      std::copy(key, key + 4, p->t_key);
+      if (prune) {
+        double* ext;
+        TRY(ws_t(c, S_SORT_TMP, (size_t)KH * n_ib, &ext));
+        ta.n_ib = n_ib;
+        k_table_ebext<<<grid_for(c, (int64_t)KH * n_ib, 128), 128, 0, c->stream>>>(ta, ext);
+        TRY(check_launch(c));
+        k_table_remlo<<<grid_for(c, (int64_t)n_ob * kOB * n_ib, 128), 128, 0, c->stream>>>(ta, ck, ext, p->t_remlo);
+        TRY(check_launch(c));
+        // best-first order of the work items: by the smallest whole-item lower bound
+        std::vector<float> rl(n_remlo);
+        CU(cudaMemcpyAsync(rl.data(), p->t_remlo, n_remlo * 4, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        const int items = n_ob * n_ib;
+        std::vector<std::pair<float, int>> keyed(items);
+        for (int w = 0; w < items; ++w) {
+          const int ob = w / n_ib, ib = w % n_ib;
+          float mn = INFINITY;
+          for (int r = 0; r < kOB; ++r) mn = std::min(mn, rl[(((size_t)ob * kOB + r) * n_ib + ib) * ck.n]);
+          keyed[w] = {mn, w};
+        }
+        std::sort(keyed.begin(), keyed.end());
+        std::vector<int> order(items);
+        for (int w = 0; w < items; ++w) order[w] = keyed[w].second;
+        if (p->t_order_cap < (size_t)items) {
+          pool_free(c, p->t_order);
+          p->t_order = nullptr;
+          p->t_order_cap = 0;
+          CU(cudaMallocAsync(&p->t_order, (size_t)items * 4, c->stream));
+          p->t_order_cap = items;
+        }
+        CU(cudaMemcpyAsync(p->t_order, order.data(), (size_t)items * 4, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));   // `order` is a host temporary
+      }
+      std::copy(key, key + 5, p->t_key);
     }
 
     SweepArgs sa;
@@ -1055,10 +1160,19 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     sa.g_cval = cval;
     sa.cap = (uint32_t)std::min<int64_t>(c->cand_cap, UINT32_MAX);
     sa.check_rules = p->ds.R > 0;
+    sa.prune = prune ? 1 : 0;
+    sa.n_ck = ck.n;
+    for (int q = 0; q < ck.n; ++q) sa.ck_group[q] = ck_group[q];
+    sa.remlo = p->t_remlo;
+    // fp32 rounding of T = acc + (cst + remlo): a few ulps of the largest partial sum
+    sa.prune_eps = (float)(16.0 * std::ldexp(1.0, -23) * (B.mag + 1.0));
+    sa.item_order = p->t_order;
+    sa.g_work = reinterpret_cast<unsigned long long*>(gs + 4);
     sa.sp = p->ds;
     const size_t smem = sweep_smem(p->he.k);
     if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);
-    void (*kern)(SweepArgs) = B.G == 3 ? k_sweep<3> : (B.G == 2 ? k_sweep<2> : k_sweep<1>);
+    void (*kern)(SweepArgs) = prune ? (B.G == 3 ? k_sweep<3, true> : (B.G == 2 ? k_sweep<2, true> : k_sweep<1, true>))
+                                    : (B.G == 3 ? k_sweep<3, false> : (B.G == 2 ? k_sweep<2, false> : k_sweep<1, false>));
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));
@@ -1070,8 +1184,15 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     TRY(check_launch(c));
     if (c->prof) CU(cudaEventRecord(c->ev[2], c->stream));
     CU(cudaMemcpyAsync(hs, gs, 8, cudaMemcpyDeviceToHost, c->stream));
+    if (prune) CU(cudaMemcpyAsync(hs + 4, gs + 4, 8, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     const uint32_t theta_key = hs[0], count = hs[1];
+    local.evaluated_frac = 1.0;
+    if (prune) {
+      uint64_t work;
+      std::memcpy(&work, hs + 4, 8);
+      local.evaluated_frac = (double)work / ((double)n_ob * n_ib * ngroups);
+    }
     local.group = B.G;
     local.raw_candidates = count;
     local.delta = B.delta;

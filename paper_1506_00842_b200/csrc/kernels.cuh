@@ -72,6 +72,7 @@ __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
 constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
 constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
+constexpr int kMaxCk = 16;      // pruning checkpoints per work item
 
 struct SweepArgs {
   int k;                        // members
@@ -91,6 +92,15 @@ struct SweepArgs {
   float* g_cval;
   uint32_t cap;
   int check_rules;
+  // optional exact pruning (MLT_OPT_PRUNE): at group ck_group[c] a work item is
+  // abandoned when every configuration's partial sum + cst + a lower bound of
+  // the remaining units (remlo, per outer) exceeds the threshold by prune_eps
+  int prune, n_ck;
+  int ck_group[kMaxCk];
+  const float* remlo;           // [outer - o_lo][inner block][n_ck] lower bound of the units still to come
+  float prune_eps;
+  const int* item_order;        // pruning: work items best-first (ascending lower bound)
+  unsigned long long* g_work;   // pruning: groups evaluated, summed over work items
   DSpace sp;
 };
 
@@ -106,10 +116,12 @@ struct TableArgs {
   int radix[kMaxP];
   int foff[kMaxP + 1];          // offset of parameter p's digits in a row of F
   const double* w1;             // [k][h][d]
-  double* F;                    // [k*kH][foff[d]]
+  const int* unit_of;           // [k*kH] original unit (m*kH + j) of each table position
+  double* F;                    // [k*kH][foff[d]]  (position order)
   const double* ca;             // [k*kH]
   const double* cb;             // [k*kH]  (0 for dummy units)
   const double* wprime;         // [k*kH]  w2*std/k (0 for dummy units)
+  int n_ib;                     // inner blocks of kInnerBlock inners
   int64_t o_lo, o_card, c_in, c_in_pad;   // o_card = number of outer configurations
   // two-level split of each table: entry = const * P_hi[index / nlo] * P_lo[index % nlo]
   const double *PoH, *PoL, *PiH, *PiL;    // [k*kH][n_hi] / [k*kH][n_lo]
@@ -122,10 +134,16 @@ struct TableArgs {
 __global__ void k_table_factors(TableArgs t);
 __global__ void k_table_partial(TableArgs t, int p_lo, int p_hi, int64_t base, int64_t count, double* P);
 __global__ void k_table_outer(TableArgs t);
+struct CkList {
+  int n;
+  int unit[kMaxCk];             // first table position still to come at checkpoint c
+};
+__global__ void k_table_ebext(TableArgs t, double* ext);
+__global__ void k_table_remlo(TableArgs t, CkList ck, const double* ext, float* remlo);
 template <int G>
 __global__ void k_table_inner(TableArgs t);
 
-template <int G>
+template <int G, bool PRUNE>
 __global__ void k_sweep(SweepArgs a);
 size_t sweep_smem(int k);
 

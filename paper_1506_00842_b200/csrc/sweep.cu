@@ -31,7 +31,8 @@ __global__ void k_table_factors(TableArgs t) {
   const int fs = t.foff[t.d];
   const int64_t total = (int64_t)KH * fs;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int mj = (int)(q / fs), r = (int)(q % fs);
+    const int pos = (int)(q / fs), r = (int)(q % fs);
+    const int mj = t.unit_of[pos];
     const int m = mj / kH, j = mj % kH;
     int p = 0;
     while (t.foff[p + 1] <= r) ++p;
@@ -100,6 +101,71 @@ __global__ void k_table_outer(TableArgs t) {
       out = (float)(t.ca[mj] * __ldg(t.PoH + (size_t)mj * t.o_nhi + a) * __ldg(t.PoL + (size_t)mj * t.o_nlo + b));
     }
     t.ea[q] = out;
+  }
+}
+
+// Extremes of the inner part per (table position, inner block): over the
+// block's inners, exp(-(B + c)) = exp(-c) * P_hi * P_lo in fp64 — its maximum
+// for w' > 0 (sigmoid smallest), its minimum for w' < 0 — widened by 1e-12
+// relative so fp64 rounding cannot make the bound optimistic.
+__global__ void k_table_ebext(TableArgs t, double* ext) {
+  const int KH = t.k * kH;
+  const int64_t total = (int64_t)KH * t.n_ib;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int pos = (int)(q / t.n_ib), ib = (int)(q % t.n_ib);
+    const double wp = t.wprime[pos];
+    double e = 0.0;
+    if (wp != 0.0) {
+      const double base = t.cb[pos] * wp;      // exp(-c)
+      double mx = 0.0, mn = INFINITY;
+      const int64_t i0 = (int64_t)ib * kInnerBlock;
+      const int64_t i1 = i0 + kInnerBlock < t.c_in ? i0 + kInnerBlock : t.c_in;
+      for (int64_t i = i0; i < i1; ++i) {
+        const double v = base * __ldg(t.PiH + (size_t)pos * t.i_nhi + i / t.i_nlo) *
+                         __ldg(t.PiL + (size_t)pos * t.i_nlo + i % t.i_nlo);
+        mx = fmax(mx, v);
+        mn = fmin(mn, v);
+      }
+      e = wp > 0 ? mx * (1.0 + 1e-12) : mn * (1.0 - 1e-12);
+    }
+    ext[q] = e;
+  }
+}
+
+// Lower bounds of the units still to come, per (outer row, inner block) and checkpoint:
+//   remlo[o][ib][c] = sum_{pos >= ck.unit[c]} min over the block's inners of w'*sigmoid(z)
+// = w' / (1 + Ea64(o) * ext(pos, ib)) in fp64 (dummy units contribute exactly 1),
+// rounded down with a safety margin so it stays a bound.
+__global__ void k_table_remlo(TableArgs t, CkList ck, const double* ext, float* remlo) {
+  const int n_ck = ck.n;
+  const int KH = t.k * kH;
+  const int64_t rows = (int64_t)t.n_ob * kOB * t.n_ib;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = q / t.n_ib;
+    const int ib = (int)(q % t.n_ib);
+    const int64_t o = t.o_lo + row;
+    float* out = remlo + q * n_ck;
+    if (o >= t.o_card) {
+      for (int c = 0; c < n_ck; ++c) out[c] = __int_as_float(0x7f800000);   // no configuration: prune freely
+      continue;
+    }
+    const int64_t a = o / t.o_nlo - t.o_hi_base, b = o % t.o_nlo;
+    double acc = 0.0;
+    int c = n_ck - 1;
+    for (int pos = KH - 1; pos >= 0 && c >= 0; --pos) {
+      const double wp = t.wprime[pos];
+      double lo = 1.0;
+      if (wp != 0.0) {
+        const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) * __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
+        lo = wp / (1.0 + ea * ext[(size_t)pos * t.n_ib + ib]);
+      }
+      acc += lo;
+      while (c >= 0 && pos == ck.unit[c]) {
+        const double v = acc - 1e-9 * (1.0 + fabs(acc));
+        out[c] = __double2float_rd(v);
+        --c;
+      }
+    }
   }
 }
 
@@ -282,7 +348,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // and every per-thread exp(-B')/w' register feeds 16. acc[s][q] holds the
 // f32x2 pair of outers (2q, 2q+1) for inner s.
 // ---------------------------------------------------------------------------
-template <int G>
+template <int G, bool PRUNE>
 __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int KH = a.k * kH;
@@ -305,9 +371,26 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   const int n_items = a.n_ob * a.n_ib;
   constexpr int kV = kInner * kOB;   // configurations per thread per work item (32)
 
+  __shared__ float s_cr[kOB * kMaxCk];   // pruning: cst + remaining-unit lower bound per outer, checkpoint
   for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const int ob = w / a.n_ib, ib = w - ob * a.n_ib;
+    // pruning visits work items best-first (ascending lower bound of their
+    // mean log time), so the threshold reaches its final value within the first wave
+    const int wi = PRUNE ? __ldg(a.item_order + w) : w;
+    const int ob = wi / a.n_ib, ib = wi - ob * a.n_ib;
     __syncthreads();
+    if (PRUNE) {
+      for (int q = tid; q < kOB * a.n_ck; q += kThreads) {
+        const int r = q / a.n_ck, c = q - r * a.n_ck;
+        s_cr[q] = a.cst + __ldg(a.remlo + (((size_t)ob * kOB + r) * a.n_ib + ib) * a.n_ck + c);
+      }
+      __syncthreads();
+      // checkpoint 0 (no unit evaluated): the item's lower bound alone decides
+      const float thf = fkey_inv(*reinterpret_cast<volatile uint32_t*>(&s_th)) + a.prune_eps;
+      bool above = true;
+#pragma unroll
+      for (int r = 0; r < kOB; ++r) above = above && s_cr[r * a.n_ck] > thf;
+      if (__syncthreads_and(above)) continue;
+    }
     {  // stage exp(-A') of this outer block: [KH][kOB] floats, contiguous in global
       const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)ob * KH * kOB);
       float4* dst = reinterpret_cast<float4*>(s_ea);
@@ -321,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     __syncthreads();
 
     const int64_t ibase = (int64_t)ib * kInnerBlock + tid;     // inner s is ibase + s*kThreads
+    bool pruned = false;
     f2 acc[kInner][kOB / 2];
 #pragma unroll
     for (int s = 0; s < kInner; ++s)
@@ -379,8 +463,28 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       // are in flight from L2 while the current group computes, with no copies.
       float ebA[kInner][G], uA[G], ebB[kInner][G], uB[G];
       load_group<G>(pe, pu, ebA, uA);
+      int ck = PRUNE ? 1 : 0;     // checkpoint 0 was decided before staging
 #pragma unroll 1
       for (int gi = 0; gi < ngroups; gi += 2) {
+        if (PRUNE && ck < a.n_ck && gi == a.ck_group[ck]) {
+          // every configuration of the work item provably above the threshold?
+          const float thf = fkey_inv(*reinterpret_cast<volatile uint32_t*>(&s_th)) + a.prune_eps;
+          bool above = true;
+#pragma unroll
+          for (int s2 = 0; s2 < kInner; ++s2)
+#pragma unroll
+            for (int q = 0; q < kOB / 2; ++q) {
+              float lo, hi;
+              upk(acc[s2][q], lo, hi);
+              above = above && (lo + s_cr[(2 * q) * a.n_ck + ck] > thf) && (hi + s_cr[(2 * q + 1) * a.n_ck + ck] > thf);
+            }
+          ++ck;
+          if (__syncthreads_and(above)) {
+            pruned = true;
+            if (tid == 0) atomicAdd(a.g_work, (unsigned long long)gi);
+            break;
+          }
+        }
         const bool has_b = gi + 1 < ngroups;
         load_group<G>(has_b ? pe + gstride : pe, has_b ? pu + G : pu, ebB, uB);
         group_step<G>(acc, E, ebA, uA);
@@ -393,6 +497,9 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
         E += 2 * G * kOB;
       }
     }
+
+    if (PRUNE && pruned) continue;   // uniform: no configuration of this item can be kept
+    if (PRUNE && tid == 0) atomicAdd(a.g_work, (unsigned long long)ngroups);
 
     // ---- candidates: bit (s*kOB + r) <-> inner s, outer r -----------------------
     float v[kV];
@@ -547,8 +654,11 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
 template __global__ void k_table_inner<1>(TableArgs t);
 template __global__ void k_table_inner<2>(TableArgs t);
 template __global__ void k_table_inner<3>(TableArgs t);
-template __global__ void k_sweep<1>(SweepArgs a);
-template __global__ void k_sweep<2>(SweepArgs a);
-template __global__ void k_sweep<3>(SweepArgs a);
+template __global__ void k_sweep<1, false>(SweepArgs a);
+template __global__ void k_sweep<2, false>(SweepArgs a);
+template __global__ void k_sweep<3, false>(SweepArgs a);
+template __global__ void k_sweep<1, true>(SweepArgs a);
+template __global__ void k_sweep<2, true>(SweepArgs a);
+template __global__ void k_sweep<3, true>(SweepArgs a);
 
 }  // namespace mlt

@@ -67,6 +67,17 @@ class TuningReport:
         return len(self.stage1_samples) + len(self.stage2_samples)
 
 
+MLT_OPT_PRUNE = N.MLT_OPT_PRUNE
+
+
+def set_sweep_pruning(on: bool, device=None) -> None:
+    """Exact bound-based pruning in the device sweep (mlt_ctx_set_option
+    MLT_OPT_PRUNE): a work item stops once every configuration in it provably
+    exceeds the running threshold. Results are identical either way; off by
+    default, so every configuration of the space is evaluated."""
+    N.check(N.lib().mlt_ctx_set_option(N.ctx(device), MLT_OPT_PRUNE, 1 if on else 0), "mlt_ctx_set_option")
+
+
 def top_m_arrays(ensemble, space, m: int, begin: int = 0, end: int | None = None, indices=None,
                  device=None, with_stats: bool = False):
     """Device top-m over the slice [begin, end) of `space` (or over an index

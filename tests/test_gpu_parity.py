@@ -33,7 +33,7 @@ def _defaults(gpu_ok):
     N = _lib()
     c = N.ctx(0)
     yield
-    for key in (N.MLT_OPT_PATH, N.MLT_OPT_GROUP, N.MLT_OPT_CAND_CAP):
+    for key in (N.MLT_OPT_PATH, N.MLT_OPT_GROUP, N.MLT_OPT_CAND_CAP, N.MLT_OPT_PRUNE):
         N.lib().mlt_ctx_set_option(c, key, -1)
 
 
@@ -125,6 +125,66 @@ def test_top_m_synthetic_full_space_1e8():
     assert st["path"] == 0
     assert np.array_equal(idx, g["m200_i"])
     np.testing.assert_allclose(pred, g["m200_p"], rtol=PRED_RTOL)
+
+
+@pytest.mark.parametrize("case,m", TOPM_CASES)
+def test_pruned_sweep_matches_reference(case, m):
+    """MLT_OPT_PRUNE: bound-based early exit, best-first item order — the same top-m."""
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    set_opt(N.MLT_OPT_PRUNE, 1)
+    g = golden(f"topm_{case}.npz")
+    idx, pred, st = top_m_arrays(product_ensemble(case), product_space(CASE_SPACE[case]), m, with_stats=True)
+    assert np.array_equal(idx, g[f"m{m}_i"]), (st, idx[:10], g[f"m{m}_i"][:10])
+    np.testing.assert_allclose(pred, g[f"m{m}_p"], rtol=PRED_RTOL)
+
+
+def test_pruned_sweep_synthetic_1e8_and_slices():
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    set_opt(N.MLT_OPT_PRUNE, 1)
+    g = golden("topm_synth_k16.npz")
+    ens, sp = product_ensemble("synth_k16"), product_space("synthetic-1e8")
+    idx, pred, st = top_m_arrays(ens, sp, 200, with_stats=True)
+    assert st["path"] == 0 and st["evaluated_frac"] < 0.8
+    assert np.array_equal(idx, g["m200_i"])
+    for lo, hi in [(0, 1 << 21), (98566144, 100663296), (37000000, 37000000 + (1 << 21))]:
+        idx, _ = top_m_arrays(ens, sp, 200, begin=lo, end=hi)
+        assert np.array_equal(idx, g[f"slice_{lo}_{hi}_i"]), (lo, hi)
+    for m in (1, 57, 1024):                               # m edge cases against the unpruned sweep
+        set_opt(N.MLT_OPT_PRUNE, 1)
+        a = top_m_arrays(ens, sp, m, begin=5_000_000, end=25_000_000)
+        set_opt(N.MLT_OPT_PRUNE, 0)
+        b_ = top_m_arrays(ens, sp, m, begin=5_000_000, end=25_000_000)
+        assert np.array_equal(a[0], b_[0]) and np.array_equal(a[1], b_[1]), m
+
+
+def test_pruned_random_ensembles_and_rules():
+    """Pruning on seeded random ensembles (saturated and flat sigmoids) and with
+    every static rule kind: identical to the unpruned band path."""
+    import paper_1506_00842_b200 as b
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    sp = product_space("stereo")
+    rng = np.random.default_rng(23)
+    for trial in range(4):
+        k = int(rng.integers(1, 9))
+        scale = [0.3, 1.0, 3.0, 8.0][trial]
+        nets = [b.Network(rng.normal(size=(30, 11)) * scale, rng.normal(size=30) * scale,
+                          rng.normal(size=30), float(rng.normal()), float(rng.normal()), float(rng.uniform(0.2, 2)))
+                for _ in range(k)]
+        ens = b.Ensemble(nets, b.Encoder.from_space(sp), sp.name)
+        res = []
+        for pr in (0, 1):
+            set_opt(N.MLT_OPT_PRUNE, pr)
+            res.append(top_m_arrays(ens, sp, 100))
+        assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1]), trial
+    set_opt(N.MLT_OPT_PRUNE, 1)
+    g = golden("topm_conv-rules_k11.npz")
+    ens = product_ensemble("conv_k11")
+    ens = b.Ensemble(list(ens.members), ens.encoder, "conv-rules")
+    idx, _ = top_m_arrays(ens, product_space("conv-rules"), 200)
+    assert np.array_equal(idx, g["m200_i"])
 
 
 @pytest.mark.parametrize("lo,hi", [(0, 1 << 21), (98566144, 100663296), (37000000, 37000000 + (1 << 21))])

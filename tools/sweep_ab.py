@@ -17,6 +17,8 @@ sp = space_from_json(json.loads((G / "spaces.json").read_text())[name])
 ens = model_from_json(json.loads((G / f"model_{case}.json").read_text()))
 c = N.ctx(0)
 N.check(N.lib().mlt_ctx_set_profiling(c, 1))
+if os.environ.get("MLT_PRUNE") == "1":
+    N.check(N.lib().mlt_ctx_set_option(c, 4, 1))
 ps, pe = N.packed(sp, "space"), N.packed(ens, "ensemble")
 plan = N.C.c_void_p()
 N.check(N.lib().mlt_plan_create(c, N.C.byref(ps.c), N.C.byref(pe.c), N.C.byref(plan)))
@@ -30,6 +32,6 @@ for r in range(reps + 2):
         tot.append(st.total_ms)
 g = np.load(G / f"topm_{case}.npz")
 ok = bool(np.array_equal(oi[:on.value], g["m200_i"])) if "m200_i" in g.files else None
-print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "sweep_ms_min": min(sw),
+print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "prune": os.environ.get("MLT_PRUNE") == "1", "sweep_ms_min": min(sw),
                   "sweep_ms_med": float(np.median(sw)), "total_ms_med": float(np.median(tot)),
-                  "parity": ok, "group": st.group, "cands": st.candidates, "raw": st.raw_candidates, "delta": st.delta}))
+                  "parity": ok, "group": st.group, "cands": st.candidates, "evaluated_frac": st.evaluated_frac, "raw": st.raw_candidates, "delta": st.delta}))
