@@ -186,6 +186,12 @@ def train_bench(space_name, with_cpu=True):
         out["cpu_reference_s_per_member"] = cpu_member
         out["cpu_reference_s_all_members_sequential"] = cpu_member * k
         out["speedup_vs_sequential_cpu"] = cpu_member * k / dev_s
+        # train_ensemble(jobs=cores) runs members in separate processes (model.py:334-339):
+        # with one BLAS thread each its wall time is about ceil(k / cores) member times
+        cores = len(os.sched_getaffinity(0))
+        par = cpu_member * -(-k // cores)
+        out["cpu_reference_s_all_members_parallel_estimate"] = par
+        out["speedup_vs_parallel_cpu_estimate"] = par / dev_s
     return out
 
 
