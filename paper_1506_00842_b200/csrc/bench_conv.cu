@@ -14,8 +14,8 @@
 //                    each thread also streams 8 input rows once for 4 vertically adjacent outputs
 //
 // Every variant sums the 25 taps in the same (dy, dx) order in fp32 and
-// divides by 25, so all 32 variants produce bit-identical images, equal to
-// the numpy float32 golden of tests/ (clamp-to-edge borders).
+// divides by 25 (correctly rounded), so all 32 variants produce bit-identical
+// images, equal to the numpy float32 golden of tests/ (clamp-to-edge borders).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -48,6 +48,15 @@ __device__ __forceinline__ float fetch(const ConvArgs& a, int y, int x) {
   return __ldg(a.in + (size_t)yy * a.pitch + xx);
 }
 
+// s / 25 correctly rounded with two FMAs: exhaustively equal to the IEEE
+// division for every finite float except -0 (tools/check_div25.cu), and a tap
+// sum that starts from +0 is never -0.
+__device__ __forceinline__ float div25(float s) {
+  const float inv = 1.0f / 25.0f;
+  const float q0 = __fmul_rn(s, inv);
+  return __fmaf_rn(__fmaf_rn(-q0, 25.0f, s), inv, q0);
+}
+
 template <bool IMG, bool LOCAL, bool PAD, bool INTER, bool UNROLL>
 __global__ void k_conv5(ConvArgs a) {
   extern __shared__ float tile[];
@@ -58,10 +67,19 @@ __global__ void k_conv5(ConvArgs a) {
   const int tw = bw + 4;
   if (LOCAL) {
     const int th = bh + 4;
-    for (int q = ty * wgx + tx; q < tw * th; q += wgx * wgy) {
-      const int r = q / tw, c = q - r * tw;
-      // rows/cols past the image's 2-pixel halo feed no valid output: clamp them in range
+    // flat, evenly split over the CTA; (r, c) advanced incrementally (no division).
+    // Rows/cols past the image's 2-pixel halo feed no valid output: clamp them in range.
+    const int nt = wgx * wgy, step_r = nt / tw, step_c = nt - step_r * tw;
+    int q = ty * wgx + tx;
+    int r = q / tw, c = q - r * tw;
+    for (; q < tw * th; q += nt) {
       tile[q] = fetch<IMG, PAD>(a, min(Y0 - 2 + r, a.H + 1), min(X0 - 2 + c, a.W + 1));
+      r += step_r;
+      c += step_c;
+      if (c >= tw) {
+        c -= tw;
+        ++r;
+      }
     }
     __syncthreads();
   }
@@ -94,7 +112,7 @@ __global__ void k_conv5(ConvArgs a) {
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a.out[(size_t)(y + k) * a.W + x] = acc[k] / 25.0f;
+        for (int k = 0; k < 4; ++k) a.out[(size_t)(y + k) * a.W + x] = div25(acc[k]);
       }
     }
   }
@@ -120,7 +138,7 @@ __global__ void k_conv5(ConvArgs a) {
           for (int dx = -2; dx <= 2; ++dx)
             s += LOCAL ? tile[(ly + 2 + dy) * tw + (lx + 2 + dx)] : fetch<IMG, PAD>(a, y + dy, x + dx);
       }
-      a.out[(size_t)y * a.W + x] = s / 25.0f;
+      a.out[(size_t)y * a.W + x] = div25(s);
     }
   }
 }
