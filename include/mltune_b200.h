@@ -134,6 +134,9 @@ MLT_API int64_t mlt_ctx_launches(mlt_ctx* ctx);
  *                     units exceed the threshold stops early (same top-m; fewer
  *                     configurations fully evaluated). 0 (default) = evaluate all.   */
 #define MLT_OPT_PRUNE 4
+/*   MLT_OPT_CHUNK     configurations per sweep chunk (default 2^27): longer slices are swept
+ *                     chunk by chunk and the per-chunk top-m merged (bounded memory).   */
+#define MLT_OPT_CHUNK 5
 MLT_API int mlt_ctx_set_option(mlt_ctx* ctx, int key, int64_t value);
 
 /* A1: values[n][P] = decode(idx[n]).                 paramspace.py:184-193 */

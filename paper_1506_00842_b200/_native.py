@@ -21,7 +21,7 @@ from . import errors
 _LIB_PATH = Path(os.environ.get("MLTUNE_B200_LIB", Path(__file__).resolve().parent / "libmltune_b200.so"))
 
 MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
-MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE = 1, 2, 3, 4
+MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE, MLT_OPT_CHUNK = 1, 2, 3, 4, 5
 RULE_KIND = {"max-product": 0, "max-weighted-sum": 1, "forbidden-combination": 2}
 
 _i32p = C.POINTER(C.c_int32)

@@ -59,6 +59,7 @@ struct mlt_ctx {
   bool prof = false;
   int64_t launches = 0;
   int opt_path = -1, opt_group = -1, opt_prune = 0;
+  int64_t chunk = int64_t(1) << 27;   // configurations per sweep chunk (MLT_OPT_CHUNK)
   int64_t cand_cap = 1 << 20;
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
   std::vector<size_t> sizes = std::vector<size_t>(32, 0);
@@ -750,6 +751,7 @@ int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
     case MLT_OPT_GROUP: c->opt_group = (int)value; return MLT_OK;
     case MLT_OPT_CAND_CAP: c->cand_cap = value < 0 ? (1 << 20) : std::max<int64_t>(value, 1); return MLT_OK;
     case MLT_OPT_PRUNE: c->opt_prune = value == 1 ? 1 : 0; return MLT_OK;
+    case MLT_OPT_CHUNK: c->chunk = value < 0 ? (int64_t(1) << 27) : std::max<int64_t>(value, 4096); return MLT_OK;
     default: return fail(MLT_EINVAL, "unknown option %d", key);
   }
 }
@@ -1284,10 +1286,56 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
   return MLT_OK;
 }
 
+// Slices longer than kChunk configurations are swept chunk by chunk (bounded
+// table and materialisation memory for spaces far beyond 10^8) and the
+// per-chunk top-m lists merged by (prediction, index): exact, because every
+// element of the global top-m is in its own chunk's top-m.
+static int plan_top_m_range(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* out_idx, double* out_pred,
+                            int64_t* out_n, mlt_sweep_stats* st) {
+  const int64_t kChunk = p->ctx->chunk;
+  if (end - begin <= kChunk || m < 1 || begin < 0 || end > p->hs.card_i || begin > end)
+    return plan_top_m_impl(p, m, begin, end, nullptr, 0, out_idx, out_pred, out_n, st);
+  std::vector<std::pair<double, int64_t>> all;
+  std::vector<int64_t> ci(m);
+  std::vector<double> cp(m);
+  mlt_sweep_stats tot;
+  std::memset(&tot, 0, sizeof tot);
+  tot.evaluated_frac = 0.0;
+  for (int64_t lo = begin; lo < end; lo += kChunk) {
+    const int64_t hi = std::min(end, lo + kChunk);
+    int64_t n = 0;
+    mlt_sweep_stats cs;
+    std::memset(&cs, 0, sizeof cs);
+    TRY(plan_top_m_impl(p, m, lo, hi, nullptr, 0, ci.data(), cp.data(), &n, &cs));
+    for (int64_t q = 0; q < n; ++q) all.emplace_back(cp[q], ci[q]);
+    tot.configs += cs.configs;
+    tot.candidates += cs.candidates;
+    tot.raw_candidates += cs.raw_candidates;
+    tot.path = std::max(tot.path, cs.path);
+    tot.group = cs.group;
+    tot.split = cs.split;
+    tot.delta = std::max(tot.delta, cs.delta);
+    tot.sweep_ms += cs.sweep_ms;
+    tot.total_ms += cs.total_ms;
+    tot.launches += cs.launches;
+    tot.evaluated_frac += cs.evaluated_frac * (double)(hi - lo);
+  }
+  std::sort(all.begin(), all.end());
+  const int64_t take = std::min<int64_t>(m, (int64_t)all.size());
+  for (int64_t q = 0; q < take; ++q) {
+    out_pred[q] = all[q].first;
+    out_idx[q] = all[q].second;
+  }
+  *out_n = take;
+  tot.evaluated_frac /= (double)(end - begin);
+  if (st) *st = tot;
+  return MLT_OK;
+}
+
 int mlt_plan_top_m(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* out_idx, double* out_pred,
                    int64_t* out_n, mlt_sweep_stats* st) {
   if (!p) return fail(MLT_EINVAL, "plan is NULL");
-  return plan_top_m_impl(p, m, begin, end, nullptr, 0, out_idx, out_pred, out_n, st);
+  return plan_top_m_range(p, m, begin, end, out_idx, out_pred, out_n, st);
 }
 
 int mlt_top_m(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, int64_t m, int64_t begin, int64_t end,
@@ -1297,7 +1345,8 @@ int mlt_top_m(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, int64
   if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
   mlt_plan* p = nullptr;
   TRY(mlt_plan_create(c, space, ens, &p));
-  const int rc = plan_top_m_impl(p, m, begin, end, idx_list, n_list, out_idx, out_pred, out_n, st);
+  const int rc = idx_list ? plan_top_m_impl(p, m, begin, end, idx_list, n_list, out_idx, out_pred, out_n, st)
+                          : plan_top_m_range(p, m, begin, end, out_idx, out_pred, out_n, st);
   mlt_plan_destroy(p);
   return rc;
 }

@@ -33,7 +33,7 @@ def _defaults(gpu_ok):
     N = _lib()
     c = N.ctx(0)
     yield
-    for key in (N.MLT_OPT_PATH, N.MLT_OPT_GROUP, N.MLT_OPT_CAND_CAP, N.MLT_OPT_PRUNE):
+    for key in (N.MLT_OPT_PATH, N.MLT_OPT_GROUP, N.MLT_OPT_CAND_CAP, N.MLT_OPT_PRUNE, N.MLT_OPT_CHUNK):
         N.lib().mlt_ctx_set_option(c, key, -1)
 
 
@@ -157,6 +157,29 @@ def test_pruned_sweep_synthetic_1e8_and_slices():
         set_opt(N.MLT_OPT_PRUNE, 0)
         b_ = top_m_arrays(ens, sp, m, begin=5_000_000, end=25_000_000)
         assert np.array_equal(a[0], b_[0]) and np.array_equal(a[1], b_[1]), m
+
+
+@pytest.mark.parametrize("prune", [0, 1])
+def test_chunked_sweep_equals_single(prune):
+    """Slices longer than MLT_OPT_CHUNK are swept chunk by chunk and merged:
+    the 10^8 space in 2^24-configuration chunks gives the reference top-200,
+    and the exact path is chunked too (m > 1024 on a 2^22 slice, 2^20 chunks)."""
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    set_opt(N.MLT_OPT_PRUNE, prune)
+    set_opt(N.MLT_OPT_CHUNK, 1 << 24)
+    g = golden("topm_synth_k16.npz")
+    ens, sp = product_ensemble("synth_k16"), product_space("synthetic-1e8")
+    idx, pred, st = top_m_arrays(ens, sp, 200, with_stats=True)
+    assert np.array_equal(idx, g["m200_i"]) and st["configs"] == sp.cardinality()
+    lo, hi = 37_000_000, 37_000_000 + (1 << 21)
+    idx, _ = top_m_arrays(ens, sp, 200, begin=lo, end=hi)
+    assert np.array_equal(idx, g[f"slice_{lo}_{hi}_i"])
+    set_opt(N.MLT_OPT_CHUNK, 1 << 20)
+    a = top_m_arrays(ens, sp, 1500, begin=3_000_000, end=3_000_000 + (1 << 22))
+    set_opt(N.MLT_OPT_CHUNK, -1)
+    b_ = top_m_arrays(ens, sp, 1500, begin=3_000_000, end=3_000_000 + (1 << 22))
+    assert np.array_equal(a[0], b_[0]) and np.array_equal(a[1], b_[1])
 
 
 def test_pruned_random_ensembles_and_rules():
