@@ -1059,8 +1059,9 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     hs[0] = 0xFF800000u;   // fkey(+inf)
     hs[1] = 0u;
     hs[4] = hs[5] = 0u;    // pruning work counter (64-bit at gs + 4)
+    hs[6] = 0u;            // pruning: next work item
     CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(gs + 4, hs + 4, 8, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(gs + 4, hs + 4, 12, cudaMemcpyHostToDevice, c->stream));
     if (!tables_cached) {
       // two-level split of each side: lo = trailing parameters with <= 64 combinations
       auto lo_split = [&](int p_lo, int p_hi, int* sa, int64_t* nlo) {
@@ -1170,6 +1171,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     sa.prune_eps = (float)(16.0 * std::ldexp(1.0, -23) * (B.mag + 1.0));
     sa.item_order = p->t_order;
     sa.g_work = reinterpret_cast<unsigned long long*>(gs + 4);
+    sa.g_next = reinterpret_cast<int*>(gs + 6);
     sa.sp = p->ds;
     const size_t smem = sweep_smem(p->he.k);
     if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);

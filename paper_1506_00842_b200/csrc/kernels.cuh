@@ -101,6 +101,7 @@ struct SweepArgs {
   float prune_eps;
   const int* item_order;        // pruning: work items best-first (ascending lower bound)
   unsigned long long* g_work;   // pruning: groups evaluated, summed over work items
+  int* g_next;                  // pruning: next work item (dynamic distribution)
   DSpace sp;
 };
 

@@ -372,7 +372,17 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   constexpr int kV = kInner * kOB;   // configurations per thread per work item (32)
 
   __shared__ float s_cr[kOB * kMaxCk];   // pruning: cst + remaining-unit lower bound per outer, checkpoint
-  for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+  // pruning makes work items uneven: they are handed out dynamically then
+  __shared__ int s_next;
+  if (PRUNE && tid == 0) s_next = atomicAdd(a.g_next, 1);
+  for (int w = PRUNE ? -1 : blockIdx.x; ; w = PRUNE ? w : w + gridDim.x) {
+    if (PRUNE) {
+      __syncthreads();
+      w = s_next;
+      __syncthreads();
+      if (tid == 0 && w < n_items) s_next = atomicAdd(a.g_next, 1);
+    }
+    if (w >= n_items) break;
     // pruning visits work items best-first (ascending lower bound of their
     // mean log time), so the threshold reaches its final value within the first wave
     const int wi = PRUNE ? __ldg(a.item_order + w) : w;
