@@ -478,7 +478,8 @@ def main():
             "parity_top200_vs_reference": ok,
             "pruned_sweep": pruned,
             "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "ms_per_step_median": 1e3 * statistics.median(e2e_times),
+                    "d2h_bytes_per_step": int(d2h), "h2d_from": "pinned staging buffer (library)",
+                    "ms_per_step_median": 1e3 * statistics.median(e2e_times),
                     "ms_per_step_max": 1e3 * max(e2e_times)},
         }
         if world == 1 and not args.no_cpu_baseline:

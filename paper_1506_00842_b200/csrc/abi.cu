@@ -64,6 +64,8 @@ struct mlt_ctx {
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
   std::vector<size_t> sizes = std::vector<size_t>(32, 0);
   void* pinned = nullptr;       // small pinned staging for scalars
+  void* stage = nullptr;        // pinned staging for plan uploads (weights, value tables)
+  size_t stage_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -103,6 +105,26 @@ int ws_t(mlt_ctx* c, int slot, size_t count, T** out) {
 // round trips or device-wide synchronisation.
 void pool_free(mlt_ctx* c, void* ptr) {
   if (ptr) cudaFreeAsync(ptr, c->stream);
+}
+
+// Host -> device upload through the context's pinned staging buffer (the
+// caller's arrays are pageable); the stream is synchronised before the buffer
+// is reused, so every upload of a plan comes from pinned memory.
+int upload_pinned(mlt_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return MLT_OK;
+  if (c->stage_cap < bytes) {
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->stage) CU(cudaFreeHost(c->stage));
+    c->stage = nullptr;
+    c->stage_cap = 0;
+    CU(cudaMallocHost(&c->stage, bytes + bytes / 2));
+    c->stage_cap = bytes + bytes / 2;
+  } else {
+    CU(cudaStreamSynchronize(c->stream));    // the previous upload from the buffer has landed
+  }
+  std::memcpy(c->stage, src, bytes);
+  CU(cudaMemcpyAsync(dst, c->stage, bytes, cudaMemcpyHostToDevice, c->stream));
+  return MLT_OK;
 }
 
 int check_launch(mlt_ctx* c) {
@@ -602,7 +624,7 @@ int plan_upload(mlt_plan* p) {
     off += h.radix[q];
   }
   CU(cudaMallocAsync(&p->d_values, h.values.size() * 8, c->stream));
-  CU(cudaMemcpyAsync(p->d_values, h.values.data(), h.values.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  TRY(upload_pinned(c, p->d_values, h.values.data(), h.values.size() * 8));
   d.values = p->d_values;
   for (int r = 0; r < d.R; ++r) {
     d.rkind[r] = h.rkind[r];
@@ -626,7 +648,7 @@ int plan_upload(mlt_plan* p) {
   de.h = e.h;
   for (int q = 0; q < e.d; ++q) de.counts[q] = e.counts[q];
   CU(cudaMallocAsync(&p->d_ens, e.packed.size() * 8, c->stream));
-  CU(cudaMemcpyAsync(p->d_ens, e.packed.data(), e.packed.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  TRY(upload_pinned(c, p->d_ens, e.packed.data(), e.packed.size() * 8));
   const size_t nw = (size_t)e.k * e.h * e.d, nh = (size_t)e.k * e.h;
   de.w1 = p->d_ens;
   de.b1 = p->d_ens + nw;
@@ -723,6 +745,7 @@ int mlt_ctx_destroy(mlt_ctx* c) {
   for (void* p : c->slots)
     if (p) cudaFree(p);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->stage) cudaFreeHost(c->stage);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->own) cudaStreamDestroy(c->own);
