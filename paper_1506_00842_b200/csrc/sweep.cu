@@ -342,11 +342,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ---------------------------------------------------------------------------
 // the sweep
 //
-// CTA = 256 threads; a work item is kOB = 16 outer x kInnerBlock = 512 inner
-// configurations. Thread t owns inners {t, t + 256} of the block and all 16
+// One persistent CTA of kThreads = 1024 threads per SM (64 registers, 32
+// warps); a work item is kOB = 8 outer x kInnerBlock = 2048 inner
+// configurations. Thread t owns inners {t, t + 1024} of the block and all 8
 // outers, so every broadcast LDS.128 of exp(-A') feeds 2 x 4 configurations
-// and every per-thread exp(-B')/w' register feeds 16. acc[s][q] holds the
-// f32x2 pair of outers (2q, 2q+1) for inner s.
+// and every per-thread exp(-B')/w' register feeds 8. acc[s][q] holds the
+// f32x2 pair of outers (2q, 2q+1) for inner s. (Tile constants: kernels.cuh,
+// overridable for A/B builds with tools/build_variants.sh.)
 // ---------------------------------------------------------------------------
 template <int G, bool PRUNE>
 __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
