@@ -17,6 +17,7 @@
  *   mlt_surrogate_times   SurrogateRunner.true_times / measured_times  measurement.py:212-238
  *   mlt_surrogate_best    exhaustive_search over a surrogate tuner.py:191-224
  *   mlt_{conv,stereo,ray}bench_*  the paper's benchmark kernels behind runner.measure (measurement.py:250-258)
+ *   mlt_host_permutations the per-epoch rng.permutation draws of _fit     model.py:218 (host helper, no GPU)
  *
  * Conventions
  *   - Plain C types only; every pointer argument is HOST memory owned by the
@@ -30,7 +31,8 @@
  *     caller's via mlt_ctx_set_stream). One context per device; a context is
  *     not re-entrant (the reference runner contract is sequential too).
  *   - There is no CPU fallback: without a usable sm_100 device every compute
- *     entry point fails with MLT_ECUDA.
+ *     entry point fails with MLT_ECUDA (mlt_host_permutations is host-only:
+ *     it reproduces the reference's RNG stream, it computes nothing of the path).
  */
 #ifndef MLTUNE_B200_H
 #define MLTUNE_B200_H
