@@ -354,16 +354,8 @@ def main():
         N.check(N.lib().mlt_plan_top_m(plan, M_TOP, lo, hi, N.ptr(out_i, N.C.c_int64), N.ptr(out_p, N.C.c_double),
                                        N.C.byref(out_n), N.C.byref(st)))
         if world > 1:
-            gi = torch.full((M_TOP,), -1, dtype=torch.int64)
-            gp = torch.full((M_TOP,), float("inf"), dtype=torch.float64)
             n = out_n.value
-            gi[:n] = torch.from_numpy(out_i[:n])
-            gp[:n] = torch.from_numpy(out_p[:n])
-            dev = "cuda" if args.backend == "nccl" else "cpu"
-            ai = torch.empty(world * M_TOP, dtype=torch.int64, device=dev)
-            ap_ = torch.empty(world * M_TOP, dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(ai, gi.to(dev))
-            dist.all_gather_into_tensor(ap_, gp.to(dev))
+            ai, ap_ = D.gather_top_lists(out_i[:n], out_p[:n], M_TOP)     # one collective per step
             return D._device_merge(ai.cuda(), ap_.cuda(), M_TOP)
         return out_i[: out_n.value], out_p[: out_n.value]
 

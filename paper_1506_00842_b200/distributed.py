@@ -42,9 +42,31 @@ def _device_merge(all_idx, all_pred, m):
     return out_idx[:n], out_pred[:n]
 
 
+def gather_top_lists(idx, pred, m: int, group=None):
+    """All-gather every rank's (index, prediction) top-m list in ONE collective:
+    a per-rank int64 record [m indices | m prediction bit patterns], padded with
+    index -1 / +inf. Returns the concatenated (indices, predictions) tensors
+    (on the GPU for NCCL, on the CPU for gloo)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    rec = torch.empty(2 * m, dtype=torch.int64)
+    rec[:m] = PAD_IDX
+    rec[m:] = torch.tensor([float("inf")], dtype=torch.float64).view(torch.int64)
+    n = len(idx)
+    rec[:n] = torch.from_numpy(np.asarray(idx, dtype=np.int64))
+    rec[m:m + n] = torch.from_numpy(np.asarray(pred, dtype=np.float64).view(np.int64))
+    rec = rec.to(dev)
+    out = torch.empty(world * 2 * m, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(out, rec, group=group)
+    out = out.view(world, 2, m)
+    return out[:, 0, :].reshape(-1).contiguous(), out[:, 1, :].reshape(-1).contiguous().view(torch.float64)
+
+
 def top_m_arrays_sharded(ensemble, space, m: int, group=None, local_fn=None, merge_fn=None):
     """Sharded top-m over the whole space; identical result on every rank."""
-    import torch
     import torch.distributed as dist
     if m < 1:
         raise ValueError("m must be >= 1")
@@ -52,17 +74,7 @@ def top_m_arrays_sharded(ensemble, space, m: int, group=None, local_fn=None, mer
     world = dist.get_world_size(group)
     lo, hi = shard_bounds(space.cardinality(), rank, world)
     idx, pred = (local_fn or _device_local)(ensemble, space, m, lo, hi)
-    nccl = dist.get_backend(group) == "nccl"
-    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
-    li = torch.full((m,), PAD_IDX, dtype=torch.int64)
-    lp = torch.full((m,), float("inf"), dtype=torch.float64)
-    li[: len(idx)] = torch.from_numpy(np.asarray(idx, dtype=np.int64))
-    lp[: len(pred)] = torch.from_numpy(np.asarray(pred, dtype=np.float64))
-    li, lp = li.to(dev), lp.to(dev)
-    gi = torch.empty(world * m, dtype=torch.int64, device=dev)
-    gp = torch.empty(world * m, dtype=torch.float64, device=dev)
-    dist.all_gather_into_tensor(gi, li, group=group)
-    dist.all_gather_into_tensor(gp, lp, group=group)
+    gi, gp = gather_top_lists(idx, pred, m, group)
     if merge_fn is not None:
         return merge_fn(gi.cpu().numpy(), gp.cpu().numpy(), m)
     if not gi.is_cuda:          # CPU-side collective (gloo): the merge still runs on this rank's B200
