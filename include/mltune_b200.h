@@ -18,6 +18,7 @@
  *   mlt_surrogate_best    exhaustive_search over a surrogate tuner.py:191-224
  *   mlt_{conv,stereo,ray}bench_*  the paper's benchmark kernels behind runner.measure (measurement.py:250-258)
  *   mlt_host_permutations the per-epoch rng.permutation draws of _fit     model.py:218 (host helper, no GPU)
+ *   mlt_format_predictions the `mltune predict` CSV rows                   cli.py:346-351 (host helper, no GPU)
  *
  * Conventions
  *   - Plain C types only; every pointer argument is HOST memory owned by the
@@ -221,6 +222,12 @@ MLT_API int mlt_train_members(mlt_ctx* ctx, const mlt_train_desc* desc, double* 
  * on `threads` host threads (0 = all); no GPU involved. */
 MLT_API int mlt_host_permutations(void* const* bitgens, int32_t n_gen, const int32_t* n, int32_t count,
                                   int32_t* out, int32_t threads);
+
+/* Host helper for the `mltune predict` CSV (cli.py:346-351): writes n lines
+ * "<idx>,<pred %.17g>\n" into out (capacity cap bytes), *used = bytes written;
+ * MLT_EINVAL if they do not fit. Runs on `threads` host threads (0 = all). */
+MLT_API int mlt_format_predictions(const int64_t* idx, const double* pred, int64_t n, char* out, int64_t cap,
+                                   int64_t* used, int32_t threads);
 
 /* ---------------------------------------------------------------------------
  * A12: the analytic surrogate device (SurrogateSpec / SurrogateRunner,

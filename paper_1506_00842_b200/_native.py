@@ -90,6 +90,7 @@ _SIGNATURES = [
     ("mlt_merge_top_m", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _i64p, _f64p, _i64p]),
     ("mlt_train_members", C.c_int, [C.c_void_p, C.POINTER(MltTrainDesc), _f64p, _f64p, _f64p, _f64p, _f64p,
                                      _f64p, _i32p]),
+    ("mlt_format_predictions", C.c_int, [_i64p, _f64p, C.c_int64, C.c_char_p, C.c_int64, _i64p, C.c_int32]),
     ("mlt_host_permutations", C.c_int, [C.POINTER(C.c_void_p), C.c_int32, _i32p, C.c_int32, _i32p, C.c_int32]),
     ("mlt_surrogate_times", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltSurrogate), _i64p, C.c_int64,
                                       C.c_int32, _f64p, _u8p]),

@@ -10,8 +10,8 @@ this package so the reference's CLI files interoperate with the device path:
   SurrogateSpec records;
 * the prediction CSV of `mltune predict` (cli.py:330-353,
   `config_index,predicted_seconds`), produced here from device predictions
-  in large chunks with vectorised formatting (the reference formats one row
-  per Python call, its next host bottleneck after the sweep).
+  in large chunks with native multi-threaded formatting (the reference
+  formats one row per Python call, its next host bottleneck after the sweep).
 
 Model JSON lives in model.py (save_model / load_model).
 """
@@ -26,6 +26,7 @@ from pathlib import Path
 
 import numpy as np
 
+from . import _native as N
 from . import errors
 from .measurement import ALL_STATUSES, STATUS_VALID, Outcome, Sample, SampleSet
 from .space import BUILTIN_SPACE_NAMES, ValidityRule, builtin_space
@@ -236,13 +237,21 @@ def load_surrogate_spec(path) -> SurrogateSpec:
 # ---- prediction CSV (mltune predict) -------------------------------------------------
 
 def format_prediction_rows(indices, preds) -> str:
-    """`index,prediction` lines with the prediction as '.17g' (cli.py:346-351)."""
-    idx = np.asarray(indices, dtype=np.int64)
-    p = np.asarray(preds, dtype=np.float64)
-    if not np.isfinite(p).all():
-        return "".join(f"{int(i)},{fmt17(v)}\n" for i, v in zip(idx.tolist(), p.tolist()))
-    body = np.char.add(np.char.add(idx.astype(str), ","), np.char.mod("%.17g", p))
-    return "\n".join(body.tolist()) + ("\n" if idx.size else "")
+    """`index,prediction` lines with the prediction as '.17g' (cli.py:346-351),
+    formatted natively on host threads (mlt_format_predictions)."""
+    idx = np.ascontiguousarray(indices, dtype=np.int64)
+    p = np.ascontiguousarray(preds, dtype=np.float64)
+    if idx.shape != p.shape:
+        raise ValueError("indices and predictions differ in length")
+    n = idx.shape[0]
+    if n == 0:
+        return ""
+    cap = n * 48
+    buf = N.C.create_string_buffer(cap)
+    used = N.C.c_int64(0)
+    N.check(N.lib().mlt_format_predictions(N.ptr(idx, N.C.c_int64), N.ptr(p, N.C.c_double), n, buf, cap,
+                                           N.C.byref(used), 0), "mlt_format_predictions")
+    return buf.raw[:used.value].decode("ascii")
 
 
 def write_predictions_csv(ensemble, path, indices=None, chunk: int = 1 << 20, device=None) -> int:

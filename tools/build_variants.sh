@@ -15,7 +15,7 @@ for spec in "$@"; do
   defs="-DMLT_THREADS=$thr -DMLT_INNER=$inner -DMLT_OB=$ob -DMLT_MINB=$minb"
   for d in ${extra//,/ }; do defs="$defs -D$d"; done
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-    -Xcompiler -fvisibility=hidden -I$ROOT/include $defs -Xptxas -v -o $out/libmltune_b200.so $SRC/abi.cu $SRC/host_rng.cu \
+    -Xcompiler -fvisibility=hidden -I$ROOT/include $defs -Xptxas -v -o $out/libmltune_b200.so $SRC/abi.cu $SRC/host_format.cu $SRC/host_rng.cu \
     $SRC/predict.cu $SRC/select.cu $SRC/surrogate.cu $SRC/sweep.cu $SRC/train.cu $BENCH_OBJS 2> $out/ptxas.txt &
 done
 wait
