@@ -30,33 +30,36 @@ def main():
     ap.add_argument("--m", type=int, nargs="+", default=[10, 50, 200])
     ap.add_argument("--k", type=int, default=11)
     ap.add_argument("--cpu-member", action="store_true", help="time one member of the reference CPU trainer")
+    ap.add_argument("--space", default="convolution", choices=["convolution", "raycasting", "stereo", "synthetic-1e8"])
+    ap.add_argument("--no-sequential", action="store_true", help="skip the one-autotune-at-a-time comparison")
     a = ap.parse_args()
-    sp = space_from_json(json.loads((G / "spaces.json").read_text())["convolution"])
-    runner = b.B200SurrogateRunner(json.loads((G / "surrogates.json").read_text())["convolution"], sp,
+    sp = space_from_json(json.loads((G / "spaces.json").read_text())[a.space])
+    runner = b.B200SurrogateRunner(json.loads((G / "surrogates.json").read_text())[a.space], sp,
                                    runner_id="gpu-a")
     EV.slowdown_grid(sp, runner, [200], [10], 1, 99, k=3, train_cfg=b.TrainConfig(epochs=5))   # warm-up
     t0 = time.perf_counter()
     cells = EV.slowdown_grid(sp, runner, a.n, a.m, a.repeats, 7, k=a.k)
     batched = time.perf_counter() - t0
     runs = len(a.n) * len(a.m) * a.repeats
-    # the same runs, one autotune call after another (device path, unbatched)
-    t0 = time.perf_counter()
-    seq_slow = {}
-    _, opt = b.exhaustive_search(sp, runner)
-    for ci, n in enumerate(a.n):
-        for cj, m in enumerate(a.m):
-            cid = ci * len(a.m) + cj
-            for rep in range(a.repeats):
-                r = b.autotune(sp, runner, b.TunerConfig(n_train=n, m_candidates=m, k_bag=a.k,
-                                                         seed=derive_seed(7, cid, rep)))
-                seq_slow.setdefault(cid, []).append(r.best_time / opt)
-    sequential = time.perf_counter() - t0
-    same = all(abs(c.mean_slowdown - float(np.mean(seq_slow[i]))) <= 1e-12 * c.mean_slowdown
-               for i, c in enumerate(cells))
-    out = {"experiment": "slowdown_grid, convolution space, gpu-a device surrogate",
+    out = {"experiment": f"slowdown_grid, {a.space} space, device surrogate (golden spec)",
            "grid": {"n": a.n, "m": a.m, "repeats": a.repeats, "k": a.k, "runs": runs, "members": runs * a.k},
-           "batched_wall_s": batched, "sequential_device_wall_s": sequential, "identical_results": same,
+           "batched_wall_s": batched,
            "cells": [{"n": c.n_train, "m": c.m_candidates, "mean_slowdown": c.mean_slowdown} for c in cells]}
+    if not a.no_sequential:
+        # the same runs, one autotune call after another (device path, unbatched)
+        t0 = time.perf_counter()
+        seq_slow = {}
+        _, opt = b.exhaustive_search(sp, runner)
+        for ci, n in enumerate(a.n):
+            for cj, m in enumerate(a.m):
+                cid = ci * len(a.m) + cj
+                for rep in range(a.repeats):
+                    r = b.autotune(sp, runner, b.TunerConfig(n_train=n, m_candidates=m, k_bag=a.k,
+                                                             seed=derive_seed(7, cid, rep)))
+                    seq_slow.setdefault(cid, []).append(r.best_time / opt)
+        out["sequential_device_wall_s"] = time.perf_counter() - t0
+        out["identical_results"] = all(abs(c.mean_slowdown - float(np.mean(seq_slow[i]))) <= 1e-12 * c.mean_slowdown
+                                       for i, c in enumerate(cells))
     if a.cpu_member:
         from oracle.model import OTrainCfg, fit
         from oracle.space import space_from_doc
