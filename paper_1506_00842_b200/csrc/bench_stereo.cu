@@ -18,7 +18,9 @@
 //   local_left/right   that image's CTA tile (+ window halo, + D-1 columns for the right image)
 //                      staged in shared memory (tiles > 227 KB -> invalid-launch)
 //   unroll_disparity   unroll factor of the disparity loop (1, 2, 4, 8)
-//   unroll_diff_x/y    unroll factors of the window loops (1, 2, 4)
+//   unroll_diff_x/y    unroll factors of the window loops (1, 2, 4); unroll_diff_x = 4 with
+//                      both tiles in shared memory (9 x 9 window) compares 4 pixels per
+//                      VABSDIFF4 with the left window rows held in registers
 //
 // 16 memory-placement combinations x 36 unroll combinations = 576 template
 // instances (bench_stereo_kern.cuh, compiled in bench_stereo_p0..p7.cu); ppt
@@ -172,8 +174,9 @@ MLT_API int mlt_stereobench_run(mlt_stereobench* b, const int32_t* knobs, int32_
   const int64_t bw = (int64_t)wgx * pptx, bh = (int64_t)wgy * ppty;
   const int64_t gx = (b->W + bw - 1) / bw, gy = (b->H + bh - 1) / bh;
   const int64_t th = bh + 2 * b->R;
+  // (+16 bytes: the packed path reads up to one aligned word past the last row)
   const size_t smem = (size_t)(((flags >> 1) & 1) ? (bw + 2 * b->R) * th : 0) +
-                      (size_t)((flags & 1) ? (bw + 2 * b->R + b->D - 1) * th : 0);
+                      (size_t)((flags & 1) ? (bw + 2 * b->R + b->D - 1) * th : 0) + 16;
   if ((int64_t)wgx * wgy > 1024 || wgy > 1024 || smem > bench::kMaxSmem || gy > 65535) {
     *status = 1;
     return MLT_OK;

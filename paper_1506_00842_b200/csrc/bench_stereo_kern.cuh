@@ -14,6 +14,18 @@ __device__ __forceinline__ unsigned fetch_u8(const uint8_t* img, cudaTextureObje
   return __ldg(img + (size_t)yy * W + xx);
 }
 
+// Three 4-byte words of a shared-memory row starting at byte `p` (any
+// alignment): four aligned 32-bit loads and three funnel shifts.
+__device__ __forceinline__ void ld12(const uint8_t* p, unsigned& w0, unsigned& w1, unsigned& w2) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const unsigned* w = reinterpret_cast<const unsigned*>(a & ~uintptr_t(3));
+  const unsigned sh = (unsigned)(a & 3) * 8;
+  const unsigned x0 = w[0], x1 = w[1], x2 = w[2], x3 = w[3];
+  w0 = __funnelshift_r(x0, x1, sh);
+  w1 = __funnelshift_r(x1, x2, sh);
+  w2 = __funnelshift_r(x2, x3, sh);
+}
+
 template <bool IL, bool IR, bool LL, bool LR, int UD, int UX, int UY>
 __global__ void k_stereo(StereoArgs a) {
   extern __shared__ uint8_t smem[];
@@ -51,6 +63,38 @@ __global__ void k_stereo(StereoArgs a) {
       if (x >= a.W) break;
       unsigned best = 0xffffffffu;
       int bd = 0;
+      if (LL && LR && UX == 4 && R == 4) {
+        // unroll_diff_x = 4 with both tiles in shared memory (9 x 9 window):
+        // each window row is 9 bytes = 2 packed words + 1 byte, compared with
+        // VABSDIFF4 (4 pixels per instruction); the left rows are loaded once
+        // per pixel, the right rows once per (disparity, row). Integer sums:
+        // the same values as the byte-wise loop.
+        unsigned lw[9][3];
+#pragma unroll
+        for (int r = 0; r < 9; ++r) {
+          ld12(tl + (ly + r) * twl + lx, lw[r][0], lw[r][1], lw[r][2]);
+          lw[r][2] &= 0xffu;
+        }
+        const uint8_t* rbase = tr + ly * twr + lx + D - 1;
+#pragma unroll UD
+        for (int d = 0; d < D; ++d) {
+          unsigned s = 0;
+#pragma unroll      // fully: the left words stay in registers (unroll_diff_y acts on the byte path)
+          for (int r = 0; r < 9; ++r) {
+            unsigned r0, r1, r2;
+            ld12(rbase + r * twr - d, r0, r1, r2);
+            s = __vsadu4(lw[r][0], r0) + s;
+            s = __vsadu4(lw[r][1], r1) + s;
+            s = __vsadu4(lw[r][2], r2 & 0xffu) + s;
+          }
+          if (s < best) {
+            best = s;
+            bd = d;
+          }
+        }
+        a.out[(size_t)y * a.W + x] = (uint8_t)bd;
+        continue;
+      }
 #pragma unroll UD
       for (int d = 0; d < D; ++d) {
         unsigned s = 0;
