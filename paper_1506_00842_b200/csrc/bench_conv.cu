@@ -7,7 +7,8 @@
 //   ppt_x, ppt_y     output pixels per thread in x / y
 //   use_image        input read through a texture object (point sampling, clamp addressing)
 //   use_local        the CTA's input tile + 2-pixel halo staged in shared memory
-//                    (tile > 227 KB -> invalid-launch)
+//                    (tile > 227 KB -> invalid-launch); with padding and no image
+//                    memory the tile arrives by TMA (cp.async.bulk.tensor + mbarrier)
 //   padding          input pre-padded by 2 replicated pixels: no clamping in the kernel
 //   interleaved      a thread's pixels are strided by the CTA width (coalesced) instead of contiguous
 //   unroll           the 5x5 filter loops fully unrolled; with contiguous pixels (interleaved = 0)
@@ -16,6 +17,8 @@
 // Every variant sums the 25 taps in the same (dy, dx) order in fp32 and
 // divides by 25 (correctly rounded), so all 32 variants produce bit-identical
 // images, equal to the numpy float32 golden of tests/ (clamp-to-edge borders).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -58,31 +61,8 @@ __device__ __forceinline__ float div25(float s) {
 }
 
 template <bool IMG, bool LOCAL, bool PAD, bool INTER, bool UNROLL>
-__global__ void k_conv5(ConvArgs a) {
-  extern __shared__ float tile[];
-  const int wgx = blockDim.x, wgy = blockDim.y;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int bw = wgx * a.pptx, bh = wgy * a.ppty;           // output pixels per CTA
-  const int X0 = blockIdx.x * bw, Y0 = blockIdx.y * bh;
-  const int tw = bw + 4;
-  if (LOCAL) {
-    const int th = bh + 4;
-    // flat, evenly split over the CTA; (r, c) advanced incrementally (no division).
-    // Rows/cols past the image's 2-pixel halo feed no valid output: clamp them in range.
-    const int nt = wgx * wgy, step_r = nt / tw, step_c = nt - step_r * tw;
-    int q = ty * wgx + tx;
-    int r = q / tw, c = q - r * tw;
-    for (; q < tw * th; q += nt) {
-      tile[q] = fetch<IMG, PAD>(a, min(Y0 - 2 + r, a.H + 1), min(X0 - 2 + c, a.W + 1));
-      r += step_r;
-      c += step_c;
-      if (c >= tw) {
-        c -= tw;
-        ++r;
-      }
-    }
-    __syncthreads();
-  }
+__device__ __forceinline__ void conv_compute(const ConvArgs& a, const float* tile, int tw, int X0, int Y0, int bw,
+                                             int bh, int tx, int ty, int wgx, int wgy) {
   int iy0 = 0;
   if (UNROLL && !INTER) {
     // Unrolled + contiguous rows: 4 vertically adjacent outputs of a column
@@ -141,6 +121,90 @@ __global__ void k_conv5(ConvArgs a) {
       a.out[(size_t)y * a.W + x] = div25(s);
     }
   }
+}
+
+
+template <bool IMG, bool LOCAL, bool PAD, bool INTER, bool UNROLL>
+__global__ void k_conv5(ConvArgs a) {
+  extern __shared__ float tile[];
+  const int wgx = blockDim.x, wgy = blockDim.y;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int bw = wgx * a.pptx, bh = wgy * a.ppty;           // output pixels per CTA
+  const int X0 = blockIdx.x * bw, Y0 = blockIdx.y * bh;
+  const int tw = bw + 4;
+  if (LOCAL) {
+    const int th = bh + 4;
+    // flat, evenly split over the CTA; (r, c) advanced incrementally (no division).
+    // Rows/cols past the image's 2-pixel halo feed no valid output: clamp them in range.
+    const int nt = wgx * wgy, step_r = nt / tw, step_c = nt - step_r * tw;
+    int q = ty * wgx + tx;
+    int r = q / tw, c = q - r * tw;
+    for (; q < tw * th; q += nt) {
+      tile[q] = fetch<IMG, PAD>(a, min(Y0 - 2 + r, a.H + 1), min(X0 - 2 + c, a.W + 1));
+      r += step_r;
+      c += step_c;
+      if (c >= tw) {
+        c -= tw;
+        ++r;
+      }
+    }
+    __syncthreads();
+  }
+  conv_compute<IMG, LOCAL, PAD, INTER, UNROLL>(a, tile, tw, X0, Y0, bw, bh, tx, ty, wgx, wgy);
+}
+
+// use_local + padding (no image memory), on a row pitch that is a multiple of
+// 16 bytes: the CTA's tile + halo arrives by TMA (cp.async.bulk.tensor.2d,
+// one elected thread, mbarrier completion) from the pre-padded image instead
+// of per-thread loads; boxes of up to 256 rows stack into the row-major tile.
+// The compute part is k_conv5's, so the output is bit-identical.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(map), "r"(x), "r"(y), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <bool INTER, bool UNROLL>
+__global__ void k_conv5_tma(ConvArgs a, const __grid_constant__ CUtensorMap map, int box_rows) {
+  extern __shared__ __align__(128) float tile[];
+  __shared__ __align__(8) uint64_t bar;
+  const int wgx = blockDim.x, wgy = blockDim.y;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int bw = wgx * a.pptx, bh = wgy * a.ppty;
+  const int X0 = blockIdx.x * bw, Y0 = blockIdx.y * bh;
+  const int tw = bw + 4, th = bh + 4;
+  const int nbox = (th + box_rows - 1) / box_rows;
+  if (tx == 0 && ty == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar, (unsigned)(nbox * box_rows * tw * 4));
+    // padded coordinates: tile column 0 = padded column X0 (= image column X0 - 2)
+    for (int bx = 0; bx < nbox; ++bx) tma_load_2d(tile + (size_t)bx * box_rows * tw, &map, X0, Y0 + bx * box_rows, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  conv_compute<false, true, true, INTER, UNROLL>(a, tile, tw, X0, Y0, bw, bh, tx, ty, wgx, wgy);
 }
 
 typedef void (*ConvKernel)(ConvArgs);
@@ -270,6 +334,50 @@ MLT_API int mlt_convbench_run(mlt_convbench* b, const int32_t* knobs, int32_t re
   if ((int64_t)wgx * wgy > 1024 || wgy > 1024 || smem > bench::kMaxSmem || gy > 65535) {
     *status = 1;                                     // cannot launch on this device
     return MLT_OK;
+  }
+  // use_local + padding without image memory: TMA-staged tile when the
+  // tensor-map constraints hold (16-byte row pitch and box width, box <= 256 wide)
+  const int tw = (int)bw + 4, th = (int)bh + 4;
+  if (!img && local && pad && (b->W % 4) == 0 && (tw % 4) == 0 && tw <= 256) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }
+    const int box_rows = th < 256 ? th : 256;
+    const int nbox = (th + box_rows - 1) / box_rows;
+    const size_t tsmem = (size_t)nbox * box_rows * tw * 4;
+    if (encode && tsmem <= bench::kMaxSmem && (int64_t)wgx * wgy <= 1024 && gy <= 65535) {
+      CUtensorMap map;
+      const cuuint64_t gdim[2] = {(cuuint64_t)b->W + 4, (cuuint64_t)b->H + 4};
+      const cuuint64_t gstride[1] = {(cuuint64_t)(b->W + 4) * 4};
+      const cuuint32_t box[2] = {(cuuint32_t)tw, (cuuint32_t)box_rows};
+      const cuuint32_t estride[2] = {1, 1};
+      if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, b->pad, gdim, gstride, box, estride,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+        void (*tk)(ConvArgs, const CUtensorMap, int) =
+            inter ? (unroll ? k_conv5_tma<true, true> : k_conv5_tma<true, false>)
+                  : (unroll ? k_conv5_tma<false, true> : k_conv5_tma<false, false>);
+        if (tsmem > 48 * 1024) CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+        ConvArgs ta;
+        ta.W = b->W;
+        ta.H = b->H;
+        ta.in = b->pad;
+        ta.pitch = b->W + 4;
+        ta.tex = b->tex_pad;
+        ta.out = b->out;
+        ta.pptx = pptx;
+        ta.ppty = ppty;
+        return b->timer.run(g_cerr, reps, [&]() {
+          tk<<<dim3((unsigned)gx, (unsigned)gy), dim3(wgx, wgy), tsmem, b->stream>>>(ta, map, box_rows);
+          return cudaGetLastError();
+        }, seconds, status);
+      }
+    }
   }
   const int sel = (img << 4) | (local << 3) | (pad << 2) | (inter << 1) | (int)unroll;
   ConvKernel k = kConvKernels[sel];

@@ -62,7 +62,11 @@ def test_conv_4096_input_and_default_image(gpu_ok):
     # unroll + contiguous rows: the 4-row register-blocked path (and its row tails)
     for cfg in ((32, 8, 1, 4, 0, 0, 1, 1, 1), (32, 4, 1, 4, 0, 1, 1, 0, 1), (32, 8, 1, 8, 0, 0, 0, 0, 1),
                 (16, 16, 2, 4, 1, 1, 0, 0, 1), (32, 4, 4, 4, 1, 0, 1, 0, 1), (64, 2, 1, 16, 0, 1, 0, 0, 1),
-                (32, 8, 1, 6, 0, 1, 1, 0, 1)):
+                (32, 8, 1, 6, 0, 1, 1, 0, 1),
+                # use_local + padding on a 16-byte pitch: the TMA-staged tile, incl. tiles taller than one
+                # 256-row box and boxes hanging past the padded image
+                (32, 32, 1, 16, 0, 1, 1, 1, 1), (8, 64, 4, 8, 0, 1, 1, 0, 0), (252, 1, 1, 100, 0, 1, 1, 0, 1),
+                (64, 4, 2, 2, 0, 1, 1, 1, 0)):
         t, ok = r.run(cfg, 3)
         assert ok and np.array_equal(r.output(), gold), cfg
     r.close()
