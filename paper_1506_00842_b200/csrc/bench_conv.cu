@@ -64,7 +64,64 @@ template <bool IMG, bool LOCAL, bool PAD, bool INTER, bool UNROLL>
 __device__ __forceinline__ void conv_compute(const ConvArgs& a, const float* tile, int tw, int X0, int Y0, int bw,
                                              int bh, int tx, int ty, int wgx, int wgy) {
   int iy0 = 0;
-  if (UNROLL && !INTER) {
+  if (UNROLL && !INTER && LOCAL && (a.pptx & 3) == 0 && (tw & 3) == 0) {
+    // 4 x 4 register block per step: 8 input rows x 8 columns (two aligned
+    // 16-byte shared loads per row) feed 16 outputs, each still summing its
+    // 25 taps in (dy, dx) order.
+    for (; iy0 + 4 <= a.ppty; iy0 += 4) {
+      const int ly = ty * a.ppty + iy0;
+      const int y = Y0 + ly;
+      if (y + 3 >= a.H) break;
+      for (int ix = 0; ix < a.pptx; ix += 4) {
+        const int lx = tx * a.pptx + ix;
+        const int x = X0 + lx;
+        if (x + 3 >= a.W) {     // right edge: the per-column path below finishes these
+          if (x < a.W) {
+            for (int c = 0; c < 4 && x + c < a.W; ++c)
+              for (int k = 0; k < 4; ++k) {
+                float sum = 0.0f;
+#pragma unroll
+                for (int dy = 0; dy < 5; ++dy)
+#pragma unroll
+                  for (int dx = 0; dx < 5; ++dx) sum += tile[(ly + k + dy) * tw + (lx + c + dx)];
+                a.out[(size_t)(y + k) * a.W + x + c] = div25(sum);
+              }
+          }
+          break;
+        }
+        float acc[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[k][c] = 0.0f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float4 u0 = *reinterpret_cast<const float4*>(tile + (ly + r) * tw + lx);
+          const float4 u1 = *reinterpret_cast<const float4*>(tile + (ly + r) * tw + lx + 4);
+          const float t[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (r - k >= 0 && r - k <= 4) {
+#pragma unroll
+              for (int dx = 0; dx < 5; ++dx)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[k][c] += t[c + dx];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float* o = a.out + (size_t)(y + k) * a.W + x;
+          if ((a.W & 3) == 0) {
+            *reinterpret_cast<float4*>(o) = make_float4(div25(acc[k][0]), div25(acc[k][1]), div25(acc[k][2]),
+                                                         div25(acc[k][3]));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) o[c] = div25(acc[k][c]);
+          }
+        }
+      }
+    }
+  } else if (UNROLL && !INTER) {
     // Unrolled + contiguous rows: 4 vertically adjacent outputs of a column
     // stream the 8 input rows they cover once (8 x 5 loads for 4 outputs
     // instead of 4 x 25); each output still adds its 25 taps in (dy, dx)

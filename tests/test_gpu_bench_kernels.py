@@ -66,7 +66,10 @@ def test_conv_4096_input_and_default_image(gpu_ok):
                 # use_local + padding on a 16-byte pitch: the TMA-staged tile, incl. tiles taller than one
                 # 256-row box and boxes hanging past the padded image
                 (32, 32, 1, 16, 0, 1, 1, 1, 1), (8, 64, 4, 8, 0, 1, 1, 0, 0), (252, 1, 1, 100, 0, 1, 1, 0, 1),
-                (64, 4, 2, 2, 0, 1, 1, 1, 0)):
+                (64, 4, 2, 2, 0, 1, 1, 1, 0),
+                # 4 x 4 register blocks with 16-byte shared loads (TMA, manual and texture-staged tiles)
+                (16, 8, 4, 4, 0, 1, 1, 0, 1), (16, 8, 8, 4, 0, 1, 0, 0, 1), (8, 8, 4, 8, 1, 1, 0, 0, 1),
+                (32, 2, 4, 16, 0, 1, 1, 0, 1)):
         t, ok = r.run(cfg, 3)
         assert ok and np.array_equal(r.output(), gold), cfg
     r.close()
