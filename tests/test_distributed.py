@@ -116,7 +116,20 @@ def _ex_worker(rank, world, port, q):
             p = int(np.argmin(tt))
             return int(idx[p]), float(tt[p]), int(ok.sum()), 0
 
-        q.put((rank,) + tuple(exhaustive_best_sharded(None, SpaceView(), local_fn=local)))
+        res = exhaustive_best_sharded(None, SpaceView(), local_fn=local)
+
+        class MeasuredRunner:             # a hardware-style runner: measured_times, no fused search
+            default_repetitions = 1
+
+            def measured_times(self, idx, reps=1):
+                return ora.measured_times(np.asarray(idx), reps)
+
+        class RuleFreeSpace(SpaceView):
+            rules = ()
+
+        res2 = exhaustive_best_sharded(MeasuredRunner(), RuleFreeSpace())
+        assert res2 == res, (res, res2)
+        q.put((rank,) + tuple(res))
     finally:
         dist.destroy_process_group()
 
