@@ -1218,7 +1218,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     if (prune) {
       uint64_t work;
       std::memcpy(&work, hs + 4, 8);
-      local.evaluated_frac = (double)work / ((double)n_ob * n_ib * ngroups);
+      local.evaluated_frac = (double)work / ((double)n_ob * n_ib * ngroups * (kThreads / 32));   // warp-groups
     }
     local.group = B.G;
     local.raw_candidates = count;

@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_bval + kSB);
   float4* s_eb = reinterpret_cast<float4*>(s_hist + 256);        // [kEbStages][W][kThreads]
   __shared__ int s_n, s_tot;
+  __shared__ unsigned int s_work;   // pruning: groups evaluated by the warps of this item
   __shared__ uint32_t s_th, s_sel[2], s_wsum[kThreads / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -410,13 +411,15 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     }
     if (tid == 0) {
       s_tot = 0;
+      s_work = 0;
       const uint32_t g = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
       if (g < s_th) s_th = g;
     }
     __syncthreads();
 
     const int64_t ibase = (int64_t)ib * kInnerBlock + tid;     // inner s is ibase + s*kThreads
-    bool pruned = false;
+    bool pruned = false;   // this WARP's configurations are all provably above the threshold
+    int done = ngroups;    // groups this warp evaluated
     f2 acc[kInner][kOB / 2];
 #pragma unroll
     for (int s = 0; s < kInner; ++s)
@@ -479,8 +482,13 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
 #pragma unroll 1
       for (int gi = 0; gi < ngroups; gi += 2) {
         if (PRUNE && ck < a.n_ck && gi == a.ck_group[ck]) {
-          // every configuration of the work item provably above the threshold?
-          const float thf = fkey_inv(*reinterpret_cast<volatile uint32_t*>(&s_th)) + a.prune_eps;
+          // Every configuration of this warp provably above the threshold? The
+          // decision is per warp (no block barrier): a warp whose 32 x kV
+          // configurations are excluded stops and leaves its issue slots to
+          // the others. The global threshold is read live: other CTAs lower it.
+          const uint32_t tk = min(*reinterpret_cast<volatile uint32_t*>(&s_th),
+                                  *reinterpret_cast<volatile uint32_t*>(a.g_theta));
+          const float thf = fkey_inv(tk) + a.prune_eps;
           bool above = true;
 #pragma unroll
           for (int s2 = 0; s2 < kInner; ++s2)
@@ -491,9 +499,9 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
               above = above && (lo + s_cr[(2 * q) * a.n_ck + ck] > thf) && (hi + s_cr[(2 * q + 1) * a.n_ck + ck] > thf);
             }
           ++ck;
-          if (__syncthreads_and(above)) {
+          if (__all_sync(0xffffffffu, above)) {
             pruned = true;
-            if (tid == 0) atomicAdd(a.g_work, (unsigned long long)gi);
+            done = gi;
             break;
           }
         }
@@ -510,8 +518,12 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       }
     }
 
-    if (PRUNE && pruned) continue;   // uniform: no configuration of this item can be kept
-    if (PRUNE && tid == 0) atomicAdd(a.g_work, (unsigned long long)ngroups);
+    if (PRUNE) {
+      if (lane == 0) atomicAdd(&s_work, (unsigned int)done);
+      const bool all_pruned = __syncthreads_and(pruned);
+      if (tid == 0) atomicAdd(a.g_work, (unsigned long long)s_work);
+      if (all_pruned) continue;   // no configuration of this item can be kept
+    }
 
     // ---- candidates: bit (s*kOB + r) <-> inner s, outer r -----------------------
     float v[kV];
@@ -535,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
         const int64_t i = ibase + (b / kOB) * kThreads;
         const int64_t idx = cfg_index(b);
         const bool in = i < a.c_in && idx >= a.begin && idx < a.end;
-        if (in && !(v[b] > thf)) mask |= 1u << b;   // NaN passes (never silently dropped)
+        if (in && !(PRUNE && pruned) && !(v[b] > thf)) mask |= 1u << b;   // NaN passes (never silently dropped)
       }
     }
     if (a.check_rules && mask) {

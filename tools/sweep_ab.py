@@ -1,6 +1,6 @@
 """A/B timing of sweep-kernel builds: MLTUNE_B200_LIB=<so> python tools/sweep_ab.py [workload] [reps]
 Prints one JSON line: sweep kernel ms (CUDA events inside the library), step ms, parity."""
-import json, os, sys, time
+import json, os, sys
 from pathlib import Path
 import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
