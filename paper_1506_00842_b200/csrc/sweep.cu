@@ -402,7 +402,13 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       bool above = true;
 #pragma unroll
       for (int r = 0; r < kOB; ++r) above = above && s_cr[r * a.n_ck] > thf;
-      if (__syncthreads_and(above)) continue;
+      if (__syncthreads_and(above)) {
+        // Items come in ascending order of exactly this bound (min over the rows
+        // of cst + remlo[checkpoint 0], rounded monotonically) and θ only falls:
+        // every later item fails the same test, so stop handing items out.
+        if (tid == 0) atomicMax(a.g_next, n_items);
+        break;
+      }
     }
     {  // stage exp(-A') of this outer block: [KH][kOB] floats, contiguous in global
       const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)ob * KH * kOB);
