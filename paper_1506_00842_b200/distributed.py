@@ -89,7 +89,7 @@ def top_m_predicted(ensemble, space, m: int, sweep_cap=None, seed: int = 0, grou
     if sweep_cap is not None and space.cardinality() > sweep_cap:
         return single(ensemble, space, m, sweep_cap, seed)
     idx, pred = top_m_arrays_sharded(ensemble, space, m, group)
-    return [(space.config_at(int(i)), float(p)) for i, p in zip(idx, pred)]
+    return list(zip(space.configs_at(idx), np.asarray(pred, dtype=np.float64).tolist()))
 
 
 def exhaustive_best_sharded(runner, space, group=None, repetitions=None, local_fn=None):

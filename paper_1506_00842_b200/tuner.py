@@ -117,7 +117,7 @@ def top_m_predicted(ensemble, space, m: int, sweep_cap: int | None = None, seed:
         idx, pred = top_m_arrays(ensemble, space, m, indices=subset)
     else:
         idx, pred = top_m_arrays(ensemble, space, m)
-    return [(space.config_at(int(i)), float(p)) for i, p in zip(idx, pred)]
+    return list(zip(space.configs_at(idx), pred.tolist()))
 
 
 def measure_configs(space, runner, configs, repetitions: int | None = None) -> list:

@@ -194,3 +194,22 @@ def test_iter_random_indices_prefix_stable(name):
     assert head == sp.sample_indices(300, 17).tolist()
     assert list(itertools.islice(sp.iter_random_indices(17), 120)) == head[:120]
     assert len(set(head)) == 300
+
+
+def test_configs_at_matches_config_at():
+    """The column-wise decode equals config_at (paramspace.py:184-193) on every
+    golden space, on a 62-binary-parameter space and past int64 values."""
+    import paper_1506_00842_b200 as b
+    rng = np.random.default_rng(3)
+    spaces = [product_space(n) for n in ("bench512", "synthetic-1e8", "convolution", "stereo", "raycasting")]
+    spaces.append(b.ParamSpace("p62", tuple(b.ParamDef(f"p{i}", (0, 1)) for i in range(62))))
+    spaces.append(b.ParamSpace("huge-values", (b.ParamDef("a", (1, 2 ** 70)), b.ParamDef("b", (3, 4, 5)))))
+    for sp in spaces:
+        card = sp.cardinality()
+        idx = np.unique(np.concatenate([rng.integers(0, card, 64), [0, card - 1]]))
+        got = sp.configs_at(idx)
+        assert got == [sp.config_at(int(i)) for i in idx], sp.name
+        assert all(type(v) is int for v in got[0])
+    assert spaces[0].configs_at([]) == []
+    with pytest.raises(IndexError):
+        spaces[0].configs_at([spaces[0].cardinality()])
