@@ -172,6 +172,17 @@ MLT_API int mlt_top_m(mlt_ctx* ctx, const mlt_space* space, const mlt_ensemble* 
               int64_t begin, int64_t end, const int64_t* idx_list, int64_t n_list,
               int64_t* out_idx, double* out_pred, int64_t* out_n, mlt_sweep_stats* stats);
 
+/* Single-process multi-GPU mlt_top_m (SURVEY §8(b) mlt_sweep_topn_multi,
+ * replacing tuner.py:95-131 on a node): the slice [begin, end) -- or the
+ * n_list indices of idx_list -- is cut into n_ctx contiguous shards, context
+ * i sweeps shard i on its own device (one host thread each, concurrently) and
+ * the per-shard lists are merged by (prediction, index). Contexts must be
+ * distinct (a context is not re-entrant); several may share a device.
+ * stats: counts summed, times the max over contexts. */
+MLT_API int mlt_top_m_multi(mlt_ctx* const* ctxs, int32_t n_ctx, const mlt_space* space, const mlt_ensemble* ens,
+                    int64_t m, int64_t begin, int64_t end, const int64_t* idx_list, int64_t n_list,
+                    int64_t* out_idx, double* out_pred, int64_t* out_n, mlt_sweep_stats* stats);
+
 /* Resident variant for repeated sweeps of one (space, ensemble): uploads the
  * descriptors once; mlt_plan_top_m then does the whole step on the device. */
 typedef struct mlt_plan mlt_plan;

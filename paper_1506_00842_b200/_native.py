@@ -83,6 +83,9 @@ _SIGNATURES = [
     ("mlt_member_outputs", C.c_int, [C.c_void_p, C.POINTER(MltEnsemble), _f64p, C.c_int64, _f64p]),
     ("mlt_top_m", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltEnsemble), C.c_int64, C.c_int64,
                             C.c_int64, _i64p, C.c_int64, _i64p, _f64p, _i64p, C.POINTER(MltSweepStats)]),
+    ("mlt_top_m_multi", C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(MltSpace), C.POINTER(MltEnsemble),
+                                  C.c_int64, C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, _f64p, _i64p,
+                                  C.POINTER(MltSweepStats)]),
     ("mlt_plan_create", C.c_int, [C.c_void_p, C.POINTER(MltSpace), C.POINTER(MltEnsemble), C.POINTER(C.c_void_p)]),
     ("mlt_plan_top_m", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, _i64p, _f64p, _i64p,
                                  C.POINTER(MltSweepStats)]),
@@ -186,6 +189,19 @@ def ctx(device: int | None = None) -> C.c_void_p:
         check(lib().mlt_ctx_create(dev, C.byref(h)), "mlt_ctx_create")
         _ctxs[dev] = h
     return _ctxs[dev]
+
+
+def extra_ctx(device: int, slot: int) -> C.c_void_p:
+    """An additional context on `device` (slot >= 1; slot 0 is ctx(device)):
+    contexts are not re-entrant, so concurrent work on one device needs one each."""
+    if slot == 0:
+        return ctx(device)
+    key = (int(device), int(slot))
+    if key not in _ctxs:
+        h = C.c_void_p()
+        check(lib().mlt_ctx_create(int(device), C.byref(h)), "mlt_ctx_create")
+        _ctxs[key] = h
+    return _ctxs[key]
 
 
 def ptr(a: np.ndarray, ctype):

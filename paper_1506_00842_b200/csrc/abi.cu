@@ -12,6 +12,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -1374,6 +1375,86 @@ int mlt_top_m(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, int64
                           : plan_top_m_range(p, m, begin, end, out_idx, out_pred, out_n, st);
   mlt_plan_destroy(p);
   return rc;
+}
+
+// Single-process multi-GPU top-m (SURVEY §8(b) `mlt_sweep_topn_multi`): the
+// slice (or the index list) is cut into n_ctx contiguous shards, one host
+// thread per context sweeps its shard on its own device concurrently, and the
+// per-shard top-m lists (exact over their shard) are merged on the host by
+// (prediction, index) -- the union's top-m is the global top-m. No collective:
+// the only exchange is n_ctx x m (index, prediction) pairs.
+int mlt_top_m_multi(mlt_ctx* const* ctxs, int32_t n_ctx, const mlt_space* space, const mlt_ensemble* ens,
+                    int64_t m, int64_t begin, int64_t end, const int64_t* idx_list, int64_t n_list,
+                    int64_t* out_idx, double* out_pred, int64_t* out_n, mlt_sweep_stats* st) {
+  if (!ctxs || n_ctx < 1) return fail(MLT_EINVAL, "need at least one context");
+  for (int i = 0; i < n_ctx; ++i) {
+    if (!ctxs[i]) return fail(MLT_EINVAL, "context %d is NULL", i);
+    for (int j = 0; j < i; ++j)
+      if (ctxs[j] == ctxs[i]) return fail(MLT_EINVAL, "context %d is passed twice (contexts are not re-entrant)", i);
+  }
+  if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
+  if (!out_idx || !out_pred || !out_n) return fail(MLT_EINVAL, "output pointer is NULL");
+  if (idx_list ? n_list < 0 : (begin < 0 || begin > end)) return fail(MLT_EINVAL, "bad slice or list length");
+  struct Shard {
+    int64_t lo = 0, hi = 0, n = 0;
+    std::vector<int64_t> idx;
+    std::vector<double> pred;
+    mlt_sweep_stats st;
+    int rc = MLT_OK;
+    std::string err;
+  };
+  std::vector<Shard> sh(n_ctx);
+  const int64_t total = idx_list ? n_list : end - begin;
+  const int64_t q = total / n_ctx, r = total % n_ctx;
+  for (int i = 0; i < n_ctx; ++i) {
+    sh[i].lo = i * q + std::min<int64_t>(i, r);
+    sh[i].hi = sh[i].lo + q + (i < r ? 1 : 0);
+  }
+  auto work = [&](int i) {
+    Shard& s = sh[i];
+    std::memset(&s.st, 0, sizeof s.st);
+    if (s.hi == s.lo) return;
+    s.idx.resize(m);
+    s.pred.resize(m);
+    s.rc = idx_list ? mlt_top_m(ctxs[i], space, ens, m, begin, end, idx_list + s.lo, s.hi - s.lo, s.idx.data(),
+                                s.pred.data(), &s.n, &s.st)
+                    : mlt_top_m(ctxs[i], space, ens, m, begin + s.lo, begin + s.hi, nullptr, 0, s.idx.data(),
+                                s.pred.data(), &s.n, &s.st);
+    if (s.rc != MLT_OK) s.err = g_err;   // the worker's thread-local message
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < n_ctx; ++i) th.emplace_back(work, i);
+  work(0);
+  for (auto& t : th) t.join();
+  for (int i = 0; i < n_ctx; ++i)
+    if (sh[i].rc != MLT_OK) return fail(sh[i].rc, "shard %d (device %d): %s", i, ctxs[i]->dev, sh[i].err.c_str());
+  std::vector<std::pair<double, int64_t>> all;
+  mlt_sweep_stats tot;
+  std::memset(&tot, 0, sizeof tot);
+  for (auto& s : sh) {
+    for (int64_t k = 0; k < s.n; ++k) all.emplace_back(s.pred[k], s.idx[k]);
+    tot.configs += s.st.configs;
+    tot.candidates += s.st.candidates;
+    tot.raw_candidates += s.st.raw_candidates;
+    tot.path = std::max(tot.path, s.st.path);
+    tot.group = std::max(tot.group, s.st.group);
+    tot.split = std::max(tot.split, s.st.split);
+    tot.delta = std::max(tot.delta, s.st.delta);
+    tot.sweep_ms = std::max(tot.sweep_ms, s.st.sweep_ms);   // the devices run concurrently
+    tot.total_ms = std::max(tot.total_ms, s.st.total_ms);
+    tot.launches += s.st.launches;
+    tot.evaluated_frac += s.st.evaluated_frac * (double)(s.hi - s.lo);
+  }
+  tot.evaluated_frac = total > 0 ? tot.evaluated_frac / (double)total : 1.0;
+  std::sort(all.begin(), all.end());
+  const int64_t take = std::min<int64_t>(m, (int64_t)all.size());
+  for (int64_t k = 0; k < take; ++k) {
+    out_pred[k] = all[k].first;
+    out_idx[k] = all[k].second;
+  }
+  *out_n = take;
+  if (st) *st = tot;
+  return MLT_OK;
 }
 
 int mlt_merge_top_m(mlt_ctx* c, const int64_t* dev_idx, const double* dev_pred, int64_t n, int64_t m,

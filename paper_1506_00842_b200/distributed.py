@@ -92,6 +92,43 @@ def top_m_predicted(ensemble, space, m: int, sweep_cap=None, seed: int = 0, grou
     return list(zip(space.configs_at(idx), np.asarray(pred, dtype=np.float64).tolist()))
 
 
+def top_m_arrays_multi_device(ensemble, space, m: int, devices, begin: int = 0, end: int | None = None,
+                              indices=None, with_stats: bool = False):
+    """Single-process multi-GPU top-m (`mlt_top_m_multi`): one shard per entry
+    of `devices`, swept concurrently from host threads inside the library,
+    merged by (prediction, index). The result equals `tuner.top_m_arrays` over
+    the same slice / index list. A device listed twice gets a second context."""
+    from . import _native as N
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    devs = [int(d) for d in devices]
+    if not devs:
+        raise ValueError("need at least one device")
+    seen = {}
+    ctxs = []
+    for d in devs:
+        ctxs.append(N.extra_ctx(d, seen.get(d, 0)))
+        seen[d] = seen.get(d, 0) + 1
+    arr = (N.C.c_void_p * len(ctxs))(*[c.value for c in ctxs])
+    ps, pe = N.packed(space, "space"), N.packed(ensemble, "ensemble")
+    end = ps.card if end is None else int(end)
+    out_idx = np.empty(m, dtype=np.int64)
+    out_pred = np.empty(m, dtype=np.float64)
+    out_n = N.C.c_int64(0)
+    st = N.MltSweepStats()
+    if indices is not None:
+        lst = np.ascontiguousarray(indices, dtype=np.int64)
+        lp, ln = N.ptr(lst, N.C.c_int64), lst.shape[0]
+    else:
+        lp, ln = None, 0
+    N.check(N.lib().mlt_top_m_multi(arr, len(ctxs), N.C.byref(ps.c), N.C.byref(pe.c), int(m), int(begin), end,
+                                    lp, ln, N.ptr(out_idx, N.C.c_int64), N.ptr(out_pred, N.C.c_double),
+                                    N.C.byref(out_n), N.C.byref(st)), "mlt_top_m_multi")
+    n = out_n.value
+    res = (out_idx[:n].copy(), out_pred[:n].copy())
+    return res + (st.as_dict(),) if with_stats else res
+
+
 def exhaustive_best_sharded(runner, space, group=None, repetitions=None, local_fn=None):
     """Exhaustive search (tuner.py:191-224) over the ranks of `group`: rank r
     runs the fused device search (`runner.exhaustive_best`) on its slice, one
