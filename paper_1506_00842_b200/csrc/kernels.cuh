@@ -72,7 +72,7 @@ __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
 constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
 constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
-constexpr int kMaxCk = 16;      // pruning checkpoints per work item
+constexpr int kMaxCk = 32;      // pruning checkpoints per work item
 
 struct SweepArgs {
   int k;                        // members

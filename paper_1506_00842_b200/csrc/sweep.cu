@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   const int n_items = a.n_ob * a.n_ib;
   constexpr int kV = kInner * kOB;   // configurations per thread per work item (32)
 
-  __shared__ float s_cr[kOB * kMaxCk];   // pruning: cst + remaining-unit lower bound per outer, checkpoint
+  __shared__ __align__(16) float s_cr[kOB * kMaxCk];   // pruning: cst + remaining-unit lower bound per outer, checkpoint
   // pruning makes work items uneven: they are handed out dynamically then
   __shared__ int s_next;
   if (PRUNE && tid == 0) s_next = atomicAdd(a.g_next, 1);
@@ -392,8 +392,8 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     const int ob = wi / a.n_ib, ib = wi - ob * a.n_ib;
     __syncthreads();
     if (PRUNE) {
-      for (int q = tid; q < kOB * a.n_ck; q += kThreads) {
-        const int r = q / a.n_ck, c = q - r * a.n_ck;
+      for (int q = tid; q < kOB * a.n_ck; q += kThreads) {   // s_cr[checkpoint][outer]
+        const int c = q / kOB, r = q - c * kOB;
         s_cr[q] = a.cst + __ldg(a.remlo + (((size_t)ob * kOB + r) * a.n_ib + ib) * a.n_ck + c);
       }
       __syncthreads();
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       const float thf = fkey_inv(*reinterpret_cast<volatile uint32_t*>(&s_th)) + a.prune_eps;
       bool above = true;
 #pragma unroll
-      for (int r = 0; r < kOB; ++r) above = above && s_cr[r * a.n_ck] > thf;
+      for (int r = 0; r < kOB; ++r) above = above && s_cr[r] > thf;
       if (__syncthreads_and(above)) {
         // Items come in ascending order of exactly this bound (min over the rows
         // of cst + remlo[checkpoint 0], rounded monotonically) and θ only falls:
@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       float ebA[kInner][G], uA[G], ebB[kInner][G], uB[G];
       load_group<G>(pe, pu, ebA, uA);
       int ck = PRUNE ? 1 : 0;     // checkpoint 0 was decided before staging
+      uint32_t gth = PRUNE ? *reinterpret_cast<volatile uint32_t*>(a.g_theta) : 0u;
 #pragma unroll 1
       for (int gi = 0; gi < ngroups; gi += 2) {
         if (PRUNE && ck < a.n_ck && gi == a.ck_group[ck]) {
@@ -492,9 +493,16 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
           // decision is per warp (no block barrier): a warp whose 32 x kV
           // configurations are excluded stops and leaves its issue slots to
           // the others. The global threshold is read live: other CTAs lower it.
-          const uint32_t tk = min(*reinterpret_cast<volatile uint32_t*>(&s_th),
-                                  *reinterpret_cast<volatile uint32_t*>(a.g_theta));
+          // (the global value was loaded at the previous checkpoint: its L2
+          // latency hides behind the groups in between)
+          const uint32_t tk = min(*reinterpret_cast<volatile uint32_t*>(&s_th), gth);
+          gth = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
           const float thf = fkey_inv(tk) + a.prune_eps;
+          static_assert(kOB % 4 == 0, "checkpoint bounds are read as float4");
+          float cr[kOB];   // this checkpoint's bounds of the outers: broadcast LDS.128s
+#pragma unroll
+          for (int r = 0; r < kOB; r += 4)
+            *reinterpret_cast<float4*>(cr + r) = *reinterpret_cast<const float4*>(s_cr + ck * kOB + r);
           bool above = true;
 #pragma unroll
           for (int s2 = 0; s2 < kInner; ++s2)
@@ -502,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
             for (int q = 0; q < kOB / 2; ++q) {
               float lo, hi;
               upk(acc[s2][q], lo, hi);
-              above = above && (lo + s_cr[(2 * q) * a.n_ck + ck] > thf) && (hi + s_cr[(2 * q + 1) * a.n_ck + ck] > thf);
+              above = above && (lo + cr[2 * q] > thf) && (hi + cr[2 * q + 1] > thf);
             }
           ++ck;
           if (__all_sync(0xffffffffu, above)) {
