@@ -1135,25 +1135,19 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
         double* ext;
         TRY(ws_t(c, S_SORT_TMP, (size_t)KH * n_ib, &ext));
         ta.n_ib = n_ib;
-        k_table_ebext<<<grid_for(c, (int64_t)KH * n_ib, 128), 128, 0, c->stream>>>(ta, ext);
+        k_table_ebext<<<grid_for(c, (int64_t)KH * n_ib * 32, 256), 256, 0, c->stream>>>(ta, ext);
         TRY(check_launch(c));
-        k_table_remlo<<<grid_for(c, (int64_t)n_ob * kOB * n_ib, 128), 128, 0, c->stream>>>(ta, ck, ext, p->t_remlo);
+        double* seg;
+        const int64_t rows_ib = (int64_t)n_ob * kOB * n_ib;
+        CU(cudaMallocAsync(&seg, (size_t)rows_ib * ck.n * 8, c->stream));
+        k_table_remseg<<<grid_for(c, rows_ib * ck.n, 256), 256, 0, c->stream>>>(ta, ck, ext, seg);
         TRY(check_launch(c));
-        // best-first order of the work items: by the smallest whole-item lower bound
-        std::vector<float> rl(n_remlo);
-        CU(cudaMemcpyAsync(rl.data(), p->t_remlo, n_remlo * 4, cudaMemcpyDeviceToHost, c->stream));
-        CU(cudaStreamSynchronize(c->stream));
+        k_table_remlo<<<grid_for(c, rows_ib, 256), 256, 0, c->stream>>>(ta, ck, seg, p->t_remlo);
+        TRY(check_launch(c));
+        CU(cudaFreeAsync(seg, c->stream));
+        // best-first order of the work items: by the smallest whole-item lower
+        // bound, sorted on the device (a stable radix sort: ties keep index order)
         const int items = n_ob * n_ib;
-        std::vector<std::pair<float, int>> keyed(items);
-        for (int w = 0; w < items; ++w) {
-          const int ob = w / n_ib, ib = w % n_ib;
-          float mn = INFINITY;
-          for (int r = 0; r < kOB; ++r) mn = std::min(mn, rl[(((size_t)ob * kOB + r) * n_ib + ib) * ck.n]);
-          keyed[w] = {mn, w};
-        }
-        std::sort(keyed.begin(), keyed.end());
-        std::vector<int> order(items);
-        for (int w = 0; w < items; ++w) order[w] = keyed[w].second;
         if (p->t_order_cap < (size_t)items) {
           pool_free(c, p->t_order);
           p->t_order = nullptr;
@@ -1161,8 +1155,20 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
           CU(cudaMallocAsync(&p->t_order, (size_t)items * 4, c->stream));
           p->t_order_cap = items;
         }
-        CU(cudaMemcpyAsync(p->t_order, order.data(), (size_t)items * 4, cudaMemcpyHostToDevice, c->stream));
-        CU(cudaStreamSynchronize(c->stream));   // `order` is a host temporary
+        float *kin, *kout;
+        int* vin;
+        void* tmp = nullptr;
+        size_t tmp_bytes = 0;
+        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const float*)nullptr, (float*)nullptr,
+                                           (const int*)nullptr, (int*)nullptr, items, 0, 32, c->stream));
+        CU(cudaMallocAsync(&kin, (size_t)items * 4, c->stream));
+        CU(cudaMallocAsync(&kout, (size_t)items * 4, c->stream));
+        CU(cudaMallocAsync(&vin, (size_t)items * 4, c->stream));
+        CU(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), c->stream));
+        k_item_keys<<<grid_for(c, items, 256), 256, 0, c->stream>>>(p->t_remlo, ck.n, n_ib, items, kin, vin);
+        TRY(check_launch(c));
+        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, p->t_order, items, 0, 32, c->stream));
+        for (void* q : {(void*)kin, (void*)kout, (void*)vin, tmp}) CU(cudaFreeAsync(q, c->stream));
       }
       std::copy(key, key + 5, p->t_key);
     }

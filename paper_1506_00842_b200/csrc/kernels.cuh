@@ -140,7 +140,9 @@ struct CkList {
   int unit[kMaxCk];             // first table position still to come at checkpoint c
 };
 __global__ void k_table_ebext(TableArgs t, double* ext);
-__global__ void k_table_remlo(TableArgs t, CkList ck, const double* ext, float* remlo);
+__global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, float* keys, int* vals);
+__global__ void k_table_remseg(TableArgs t, CkList ck, const double* ext, double* seg);
+__global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* remlo);
 template <int G>
 __global__ void k_table_inner(TableArgs t);
 

@@ -104,14 +104,24 @@ __global__ void k_table_outer(TableArgs t) {
   }
 }
 
+// x / d for non-negative operands, in 32 bits when both fit (a 64-bit
+// division is a ~60-instruction sequence; these index splits run per thread)
+__device__ __forceinline__ int64_t udiv(int64_t x, int64_t d) {
+  return ((uint64_t)x | (uint64_t)d) <= 0xffffffffull ? (int64_t)((uint32_t)x / (uint32_t)d) : x / d;
+}
+
 // Extremes of the inner part per (table position, inner block): over the
 // block's inners, exp(-(B + c)) = exp(-c) * P_hi * P_lo in fp64 — its maximum
 // for w' > 0 (sigmoid smallest), its minimum for w' < 0 — widened by 1e-12
 // relative so fp64 rounding cannot make the bound optimistic.
 __global__ void k_table_ebext(TableArgs t, double* ext) {
+  // one warp per (position, inner block): lanes stride over the block's
+  // inners; max / min are exact, so the reduction order does not matter
   const int KH = t.k * kH;
   const int64_t total = (int64_t)KH * t.n_ib;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < total; q += wstride) {
     const int pos = (int)(q / t.n_ib), ib = (int)(q % t.n_ib);
     const double wp = t.wprime[pos];
     double e = 0.0;
@@ -120,15 +130,35 @@ __global__ void k_table_ebext(TableArgs t, double* ext) {
       double mx = 0.0, mn = INFINITY;
       const int64_t i0 = (int64_t)ib * kInnerBlock;
       const int64_t i1 = i0 + kInnerBlock < t.c_in ? i0 + kInnerBlock : t.c_in;
-      for (int64_t i = i0; i < i1; ++i) {
-        const double v = base * __ldg(t.PiH + (size_t)pos * t.i_nhi + i / t.i_nlo) *
-                         __ldg(t.PiL + (size_t)pos * t.i_nlo + i % t.i_nlo);
+      for (int64_t i = i0 + lane; i < i1; i += 32) {
+        const int64_t ih = udiv(i, t.i_nlo);
+        const double v = base * __ldg(t.PiH + (size_t)pos * t.i_nhi + ih) *
+                         __ldg(t.PiL + (size_t)pos * t.i_nlo + (i - ih * t.i_nlo));
         mx = fmax(mx, v);
         mn = fmin(mn, v);
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      }
       e = wp > 0 ? mx * (1.0 + 1e-12) : mn * (1.0 - 1e-12);
     }
-    ext[q] = e;
+    if (lane == 0) ext[q] = e;
+  }
+}
+
+// Sort key of each work item for the best-first order of the pruned sweep:
+// the smallest checkpoint-0 bound over its outer rows (exactly what the
+// kernel's checkpoint-0 test compares, so the early stop there is sound).
+__global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, float* keys, int* vals) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < items; w += gridDim.x * blockDim.x) {
+    const int ob = w / n_ib, ib = w - ob * n_ib;
+    float mn = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int r = 0; r < kOB; ++r) mn = fminf(mn, __ldg(remlo + (((size_t)ob * kOB + r) * n_ib + ib) * n_ck));
+    keys[w] = mn;
+    vals[w] = w;
   }
 }
 
@@ -136,35 +166,54 @@ __global__ void k_table_ebext(TableArgs t, double* ext) {
 //   remlo[o][ib][c] = sum_{pos >= ck.unit[c]} min over the block's inners of w'*sigmoid(z)
 // = w' / (1 + Ea64(o) * ext(pos, ib)) in fp64 (dummy units contribute exactly 1),
 // rounded down with a safety margin so it stays a bound.
-__global__ void k_table_remlo(TableArgs t, CkList ck, const double* ext, float* remlo) {
+// Two passes. k_table_remseg: one thread per (outer row, checkpoint interval,
+// inner block), inner block fastest (coalesced ext loads, broadcast outer
+// factors), sums the units between checkpoints c and c + 1 into
+// seg[c][row * n_ib + ib] (fp64). k_table_remlo: one thread per (row, inner
+// block) suffix-sums its intervals and rounds each checkpoint's bound down
+// with a 1e-9 margin (which dwarfs the fp64 summation-order error of <= 480
+// terms).
+__global__ void k_table_remseg(TableArgs t, CkList ck, const double* ext, double* seg) {
   const int n_ck = ck.n;
   const int KH = t.k * kH;
-  const int64_t rows = (int64_t)t.n_ob * kOB * t.n_ib;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = q / t.n_ib;
-    const int ib = (int)(q % t.n_ib);
+  const int64_t rows_ib = (int64_t)t.n_ob * kOB * t.n_ib;
+  const int64_t total = rows_ib * n_ck;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q1 = udiv(q, t.n_ib);
+    const int ib = (int)(q - q1 * t.n_ib);
+    const int64_t row = udiv(q1, n_ck);
+    const int c = (int)(q1 - row * n_ck);
     const int64_t o = t.o_lo + row;
-    float* out = remlo + q * n_ck;
-    if (o >= t.o_card) {
-      for (int c = 0; c < n_ck; ++c) out[c] = __int_as_float(0x7f800000);   // no configuration: prune freely
-      continue;
-    }
-    const int64_t a = o / t.o_nlo - t.o_hi_base, b = o % t.o_nlo;
     double acc = 0.0;
-    int c = n_ck - 1;
-    for (int pos = KH - 1; pos >= 0 && c >= 0; --pos) {
-      const double wp = t.wprime[pos];
-      double lo = 1.0;
-      if (wp != 0.0) {
-        const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) * __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
-        lo = wp / (1.0 + ea * ext[(size_t)pos * t.n_ib + ib]);
+    if (o < t.o_card) {
+      const int64_t oh = udiv(o, t.o_nlo);
+      const int64_t a = oh - t.o_hi_base, b = o - oh * t.o_nlo;
+      const int u1 = c + 1 < n_ck ? ck.unit[c + 1] : KH;
+      for (int pos = ck.unit[c]; pos < u1; ++pos) {
+        const double wp = t.wprime[pos];
+        double lo = 1.0;
+        if (wp != 0.0) {
+          const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) * __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
+          lo = wp / (1.0 + ea * __ldg(ext + (size_t)pos * t.n_ib + ib));
+        }
+        acc += lo;
       }
-      acc += lo;
-      while (c >= 0 && pos == ck.unit[c]) {
-        const double v = acc - 1e-9 * (1.0 + fabs(acc));
-        out[c] = __double2float_rd(v);
-        --c;
-      }
+    }
+    seg[(size_t)c * rows_ib + row * t.n_ib + ib] = acc;
+  }
+}
+
+__global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* remlo) {
+  const int n_ck = ck.n;
+  const int64_t rows_ib = (int64_t)t.n_ob * kOB * t.n_ib;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows_ib; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = t.o_lo + q / t.n_ib;
+    float* out = remlo + q * n_ck;
+    double acc = 0.0;
+    for (int c = n_ck - 1; c >= 0; --c) {
+      acc += seg[(size_t)c * rows_ib + q];
+      out[c] = o < t.o_card ? __double2float_rd(acc - 1e-9 * (1.0 + fabs(acc)))
+                            : __int_as_float(0x7f800000);   // no configuration: prune freely
     }
   }
 }
