@@ -374,11 +374,19 @@ __device__ __forceinline__ void lower_threshold(const SweepArgs& a, uint32_t* s_
 }
 
 // the per-thread factor ring: [stage][w][thread] float4 (conflict-free LDS.128)
-constexpr size_t eb_ring_bytes() { return (size_t)kEbStages * ebw_of(3) * kThreads * 16; }
+__host__ __device__ constexpr size_t eb_ring_bytes() { return (size_t)kEbStages * ebw_of(3) * kThreads * 16; }
+
+// byte offset of the second exp(-A') tile buffer (the next item's tile lands
+// there by cp.async while the current item computes)
+__host__ __device__ inline size_t ea2_offset(int k) {
+  const size_t KH = (size_t)k * kH;
+  const size_t b = KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4 + eb_ring_bytes();
+  return (b + 15) & ~(size_t)15;
+}
 
 size_t sweep_smem(int k) {
   const size_t KH = (size_t)k * kH;
-  return KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4 + eb_ring_bytes();
+  return ea2_offset(k) + KH * kOB * 4;   // ... + the second exp(-A') buffer
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -409,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   float* s_bval = reinterpret_cast<float*>(s_bidx + kSB);
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_bval + kSB);
   float4* s_eb = reinterpret_cast<float4*>(s_hist + 256);        // [kEbStages][W][kThreads]
+  float* s_ea2 = reinterpret_cast<float*>(smraw + ea2_offset(a.k));   // [KH][kOB], the other tile buffer
   __shared__ int s_n, s_tot;
   __shared__ unsigned int s_work;   // pruning: groups evaluated by the warps of this item
   __shared__ uint32_t s_th, s_sel[2], s_wsum[kThreads / 32];
@@ -427,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   // pruning makes work items uneven: they are handed out dynamically then
   __shared__ int s_next;
   if (PRUNE && tid == 0) s_next = atomicAdd(a.g_next, 1);
+  int pf_ob = -1, pf_buf = 0, cur = 0;   // prefetched outer block, its buffer; the buffer in use
   for (int w = PRUNE ? -1 : blockIdx.x; ; w = PRUNE ? w : w + gridDim.x) {
     if (PRUNE) {
       __syncthreads();
@@ -459,7 +469,13 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
         break;
       }
     }
-    {  // stage exp(-A') of this outer block: [KH][kOB] floats, contiguous in global
+    if (pf_ob == ob) {
+      // this outer block's exp(-A') tile was prefetched during the previous item
+      cur = pf_buf;
+      cp_async_wait<0>();   // (visible to every thread after the barrier below)
+    } else {  // stage it now: [KH][kOB] floats, contiguous in global
+      cp_async_wait<0>();   // no prefetch may still be landing in the buffer
+      cur = 0;
       const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)ob * KH * kOB);
       float4* dst = reinterpret_cast<float4*>(s_ea);
       for (int q = tid; q < KH * kOB / 4; q += kThreads) dst[q] = __ldg(src + q);
@@ -471,6 +487,29 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       if (g < s_th) s_th = g;
     }
     __syncthreads();
+
+    const float* s_cur = cur ? s_ea2 : s_ea;
+    // Prefetch the next item's tile into the other buffer (cp.async, no wait):
+    // full sweep 5.00 -> 4.92 ms on the 10^8 case. Not in the pruned sweep,
+    // where the next item is often rejected at checkpoint 0 (2.483 -> 2.496 ms).
+    if (!PRUNE) {
+      const int wn = w + (int)gridDim.x;
+      pf_ob = -1;
+      if (wn < n_items) {
+        const int obn = wn / a.n_ib;
+        if (obn == ob) {
+          pf_ob = ob;
+          pf_buf = cur;
+        } else {
+          const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)obn * KH * kOB);
+          float* dst = cur ? s_ea : s_ea2;
+          for (int q = tid; q < KH * kOB / 4; q += kThreads) cp_async16(dst + 4 * q, src + q);
+          cp_async_commit();
+          pf_ob = obn;
+          pf_buf = cur ^ 1;
+        }
+      }
+    }
 
     const int64_t ibase = (int64_t)ib * kInnerBlock + tid;     // inner s is ibase + s*kThreads
     bool pruned = false;   // this WARP's configurations are all provably above the threshold
@@ -485,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     const size_t gstride = (size_t)kThreads * W;   // float4s per group
     const float4* pe = reinterpret_cast<const float4*>(a.ebp) + ((size_t)ib * ngroups * kThreads + tid) * W;
     const float* pu = s_u;                   // 1/w' of the current group
-    const float* E = s_ea;                   // exp(-A') rows of the current group
+    const float* E = s_cur;                  // exp(-A') rows of the current group
     if (kEbStages > 0) {
       // Each thread streams ITS OWN factors through a private cp.async ring
       // kEbStages groups ahead: the L2 latency hides behind kEbStages-1 groups
@@ -729,6 +768,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     }
   }
   __syncthreads();
+  cp_async_wait<0>();   // a prefetch for an item this CTA never ran
   {  // final flush of this CTA's candidates, against the freshest global threshold
     const uint32_t g = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
     const float thf = fkey_inv(min(s_th, g));
