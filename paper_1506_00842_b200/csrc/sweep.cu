@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
         __syncthreads();
       }
       const float thf = fkey_inv(s_th);
-      constexpr int kPer = kSB / kThreads;
+      constexpr int kPer = (kSB + kThreads - 1) / kThreads;   // any block size (768: 3 slots per thread)
       int64_t ki[kPer];
       float kv[kPer];
       uint32_t keep = 0;
