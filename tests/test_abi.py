@@ -70,3 +70,9 @@ def test_null_and_bad_arguments_are_rejected_without_a_device():
     assert lib.mlt_ctx_set_option(None, 1, 0) == N.MLT_EINVAL
     assert lib.mlt_top_m(None, None, None, 1, 0, 1, None, 0, None, None, None, None) == N.MLT_EINVAL
     assert lib.mlt_ctx_launches(None) == -1
+    # multi-context top-m: no contexts, a NULL context, m < 1 -- all refused before any device work
+    assert lib.mlt_top_m_multi(None, 1, None, None, 1, 0, 1, None, 0, None, None, None, None) == N.MLT_EINVAL
+    arr = (N.C.c_void_p * 2)(None, None)
+    assert lib.mlt_top_m_multi(arr, 0, None, None, 1, 0, 1, None, 0, None, None, None, None) == N.MLT_EINVAL
+    assert lib.mlt_top_m_multi(arr, 2, None, None, 1, 0, 1, None, 0, None, None, None, None) == N.MLT_EINVAL
+    assert b"NULL" in lib.mlt_last_error()
