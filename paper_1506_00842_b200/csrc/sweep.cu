@@ -86,6 +86,12 @@ __global__ void k_table_partial(TableArgs t, int p_lo, int p_hi, int64_t base, i
   }
 }
 
+// x / d for non-negative operands, in 32 bits when both fit (a 64-bit
+// division is a ~60-instruction sequence; these index splits run per thread)
+__device__ __forceinline__ int64_t udiv(int64_t x, int64_t d) {
+  return ((uint64_t)x | (uint64_t)d) <= 0xffffffffull ? (int64_t)((uint32_t)x / (uint32_t)d) : x / d;
+}
+
 // Outer table Ea[ob][mj][r], one thread per element in output order.
 // Row o = o_lo + ob*kOB + r = (o / nlo) * nlo + o % nlo over the outer split.
 __global__ void k_table_outer(TableArgs t) {
@@ -93,21 +99,17 @@ __global__ void k_table_outer(TableArgs t) {
   const int64_t total = (int64_t)t.n_ob * KH * kOB;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(q % kOB);
-    const int mj = (int)((q / kOB) % KH);
-    const int64_t o = t.o_lo + (q / ((int64_t)kOB * KH)) * kOB + r;
+    const int64_t q8 = q / kOB, ob = udiv(q8, KH);
+    const int mj = (int)(q8 - ob * KH);
+    const int64_t o = t.o_lo + ob * kOB + r;
     float out = 1.0f;
     if (o < t.o_card && t.wprime[mj] != 0.0) {
-      const int64_t a = o / t.o_nlo - t.o_hi_base, b = o % t.o_nlo;
+      const int64_t oh = udiv(o, t.o_nlo);
+      const int64_t a = oh - t.o_hi_base, b = o - oh * t.o_nlo;
       out = (float)(t.ca[mj] * __ldg(t.PoH + (size_t)mj * t.o_nhi + a) * __ldg(t.PoL + (size_t)mj * t.o_nlo + b));
     }
     t.ea[q] = out;
   }
-}
-
-// x / d for non-negative operands, in 32 bits when both fit (a 64-bit
-// division is a ~60-instruction sequence; these index splits run per thread)
-__device__ __forceinline__ int64_t udiv(int64_t x, int64_t d) {
-  return ((uint64_t)x | (uint64_t)d) <= 0xffffffffull ? (int64_t)((uint32_t)x / (uint32_t)d) : x / d;
 }
 
 // Extremes of the inner part per (table position, inner block): over the
@@ -230,14 +232,14 @@ __global__ void k_table_inner(TableArgs t) {
     const int slot = (int)(q % WF);
     const int th = (int)((q / WF) % kThreads);
     const int64_t rest = q / ((int64_t)WF * kThreads);
-    const int gi = (int)(rest % ngroups);
-    const int64_t ib = rest / ngroups;
+    const int64_t ib = udiv(rest, ngroups);
+    const int gi = (int)(rest - ib * ngroups);
     const int x = slot / kInner, s = slot % kInner;
     const int mj = gi * G + x;
     const int64_t i = ib * kInnerBlock + (int64_t)s * kThreads + th;
     float out = 0.0f;
     if (x < G && i < t.c_in) {
-      const int64_t a = i / t.i_nlo, b = i % t.i_nlo;     // cb = 0 for dummy units
+      const int64_t a = udiv(i, t.i_nlo), b = i - a * t.i_nlo;     // cb = 0 for dummy units
       out = (float)(t.cb[mj] * __ldg(t.PiH + (size_t)mj * t.i_nhi + a) * __ldg(t.PiL + (size_t)mj * t.i_nlo + b));
     }
     t.ebp[q] = out;
