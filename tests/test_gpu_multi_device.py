@@ -69,3 +69,24 @@ def test_multi_context_errors(gpu_ok):
                                  N.ptr(oi, N.C.c_int64), N.ptr(op, N.C.c_double), N.C.byref(on), None)
     assert rc == N.MLT_EINVAL
     assert b"twice" in N.lib().mlt_last_error()
+
+
+def test_multi_context_with_pruning_and_chunks(gpu_ok):
+    """Each context may run its shard with exact pruning and chunked sweeps:
+    the merged top-m is still the reference's golden list."""
+    from paper_1506_00842_b200 import _native as N
+    from paper_1506_00842_b200.distributed import top_m_arrays_multi_device
+    sp, ens = product_space("synthetic-1e8"), product_ensemble("synth_k16")
+    g = golden("topm_synth_k16.npz")
+    ctxs = [N.extra_ctx(0, s) for s in range(3)]
+    try:
+        for c in ctxs:
+            N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_PRUNE, 1))
+            N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_CHUNK, 1 << 24))
+        idx, pred, st = top_m_arrays_multi_device(ens, sp, 200, [0, 0, 0], with_stats=True)
+        assert np.array_equal(idx, g["m200_i"])
+        assert st["evaluated_frac"] < 1.0
+    finally:
+        for c in ctxs:
+            N.lib().mlt_ctx_set_option(c, N.MLT_OPT_PRUNE, -1)
+            N.lib().mlt_ctx_set_option(c, N.MLT_OPT_CHUNK, -1)
