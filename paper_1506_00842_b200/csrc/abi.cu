@@ -65,8 +65,9 @@ struct mlt_ctx {
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
   std::vector<size_t> sizes = std::vector<size_t>(32, 0);
   void* pinned = nullptr;       // small pinned staging for scalars
-  void* stage = nullptr;        // pinned staging for plan uploads (weights, value tables)
+  void* stage = nullptr;        // pinned staging ring for plan uploads (weights, value tables)
   size_t stage_cap = 0;
+  size_t stage_off = 0;         // next free byte of the ring
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -112,19 +113,28 @@ void pool_free(mlt_ctx* c, void* ptr) {
 // caller's arrays are pageable); the stream is synchronised before the buffer
 // is reused, so every upload of a plan comes from pinned memory.
 int upload_pinned(mlt_ctx* c, void* dst, const void* src, size_t bytes) {
+  // Successive uploads take successive slots of the ring, so a plan's several
+  // uploads queue without host waits; the stream is synchronised only when
+  // the ring wraps (every earlier copy out of it has then landed) or grows.
   if (bytes == 0) return MLT_OK;
-  if (c->stage_cap < bytes) {
+  const size_t need = (bytes + 255) & ~(size_t)255;
+  if (c->stage_cap < need) {
     CU(cudaStreamSynchronize(c->stream));
     if (c->stage) CU(cudaFreeHost(c->stage));
     c->stage = nullptr;
     c->stage_cap = 0;
-    CU(cudaMallocHost(&c->stage, bytes + bytes / 2));
-    c->stage_cap = bytes + bytes / 2;
-  } else {
-    CU(cudaStreamSynchronize(c->stream));    // the previous upload from the buffer has landed
+    const size_t cap = std::max<size_t>(need * 2, (size_t)4 << 20);
+    CU(cudaMallocHost(&c->stage, cap));
+    c->stage_cap = cap;
+    c->stage_off = 0;
+  } else if (c->stage_off + need > c->stage_cap) {
+    CU(cudaStreamSynchronize(c->stream));
+    c->stage_off = 0;
   }
-  std::memcpy(c->stage, src, bytes);
-  CU(cudaMemcpyAsync(dst, c->stage, bytes, cudaMemcpyHostToDevice, c->stream));
+  char* slot = static_cast<char*>(c->stage) + c->stage_off;
+  c->stage_off += need;
+  std::memcpy(slot, src, bytes);
+  CU(cudaMemcpyAsync(dst, slot, bytes, cudaMemcpyHostToDevice, c->stream));
   return MLT_OK;
 }
 
@@ -533,8 +543,8 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   mlt_ctx* c = p->ctx;
   CU(cudaMallocAsync(&b.d_tab, tab.size() * 8, c->stream));
   CU(cudaMallocAsync(&b.d_u, (size_t)KH * 4, c->stream));
-  CU(cudaMemcpyAsync(b.d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
-  CU(cudaMemcpyAsync(b.d_u, u.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
+  TRY(upload_pinned(c, b.d_tab, tab.data(), tab.size() * 8));
+  TRY(upload_pinned(c, b.d_u, u.data(), (size_t)KH * 4));
   b.ok = true;
   return MLT_OK;
 }
@@ -592,7 +602,7 @@ int plan_factors(mlt_plan* p) {
     for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = mj;
     std::stable_sort(p->unit_of.begin(), p->unit_of.end(), [&](int x, int y) { return range[x] > range[y]; });
     CU(cudaMallocAsync(&p->d_unit_of, (size_t)KH * 4, c->stream));
-    CU(cudaMemcpyAsync(p->d_unit_of, p->unit_of.data(), (size_t)KH * 4, cudaMemcpyHostToDevice, c->stream));
+    TRY(upload_pinned(c, p->d_unit_of, p->unit_of.data(), (size_t)KH * 4));
   }
   CU(cudaMallocAsync(&p->d_F, (size_t)KH * p->foff[s.P] * 8, c->stream));
   TableArgs ta;
@@ -635,8 +645,8 @@ int plan_upload(mlt_plan* p) {
   CU(cudaMallocAsync(&p->d_rpos, std::max<size_t>(1, h.rpos.size()) * 4, c->stream));
   CU(cudaMallocAsync(&p->d_rcoeff, std::max<size_t>(1, h.rcoeff.size()) * 8, c->stream));
   if (!h.rpos.empty()) {
-    CU(cudaMemcpyAsync(p->d_rpos, h.rpos.data(), h.rpos.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(p->d_rcoeff, h.rcoeff.data(), h.rcoeff.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    TRY(upload_pinned(c, p->d_rpos, h.rpos.data(), h.rpos.size() * 4));
+    TRY(upload_pinned(c, p->d_rcoeff, h.rcoeff.data(), h.rcoeff.size() * 8));
   }
   d.rpos = p->d_rpos;
   d.rcoeff = p->d_rcoeff;
