@@ -109,9 +109,9 @@ void pool_free(mlt_ctx* c, void* ptr) {
   if (ptr) cudaFreeAsync(ptr, c->stream);
 }
 
-// Host -> device upload through the context's pinned staging buffer (the
-// caller's arrays are pageable); the stream is synchronised before the buffer
-// is reused, so every upload of a plan comes from pinned memory.
+// Host -> device upload through the context's pinned staging ring (the
+// caller's arrays are pageable), so every upload of a plan comes from pinned
+// memory and is truly asynchronous.
 int upload_pinned(mlt_ctx* c, void* dst, const void* src, size_t bytes) {
   // Successive uploads take successive slots of the ring, so a plan's several
   // uploads queue without host waits; the stream is synchronised only when
@@ -953,16 +953,14 @@ int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens,
     delete p;
     return rc;
   }
-  CU(cudaStreamSynchronize(c->stream));
-  *out = p;
+  *out = p;   // no host wait: uploads come from the pinned ring, and all use is stream-ordered
   return MLT_OK;
 }
 
 int mlt_plan_destroy(mlt_plan* p) {
   if (!p) return MLT_OK;
   cudaSetDevice(p->ctx->dev);
-  cudaStreamSynchronize(p->ctx->stream);
-  plan_free(p);
+  plan_free(p);   // stream-ordered frees: no host wait
   delete p;
   return MLT_OK;
 }
