@@ -65,6 +65,8 @@ struct mlt_ctx {
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
   std::vector<size_t> sizes = std::vector<size_t>(32, 0);
   void* pinned = nullptr;       // small pinned staging for scalars
+  void* res_pin = nullptr;      // pinned landing zone of a step's top-m (prediction, index) lists
+  size_t res_cap = 0;
   void* stage = nullptr;        // pinned staging ring for plan uploads (weights, value tables)
   size_t stage_cap = 0;
   size_t stage_off = 0;         // next free byte of the ring
@@ -757,6 +759,7 @@ int mlt_ctx_destroy(mlt_ctx* c) {
     if (p) cudaFree(p);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->stage) cudaFreeHost(c->stage);
+  if (c->res_pin) cudaFreeHost(c->res_pin);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->own) cudaStreamDestroy(c->own);
@@ -1227,14 +1230,59 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     kern<<<grid, kThreads, smem, c->stream>>>(sa);
     TRY(check_launch(c));
     if (c->prof) CU(cudaEventRecord(c->ev[2], c->stream));
-    CU(cudaMemcpyAsync(hs, gs, 8, cudaMemcpyDeviceToHost, c->stream));
-    if (prune) CU(cudaMemcpyAsync(hs + 4, gs + 4, 8, cudaMemcpyDeviceToHost, c->stream));
+    // Snapshot the sweep's counters (the band stage reuses gs[2..4]) and launch
+    // the band stage right behind the sweep, without a host round trip: its
+    // buffers are sized for the candidate capacity and its kernels read the
+    // candidate count on the device. One host wait at the end of the step.
+    CU(cudaMemcpyAsync(hs + 8, gs, 8, cudaMemcpyDeviceToHost, c->stream));            // theta, count
+    if (prune) CU(cudaMemcpyAsync(hs + 10, gs + 4, 8, cudaMemcpyDeviceToHost, c->stream));   // work
+    const uint32_t cap = (uint32_t)std::min<int64_t>(c->cand_cap, UINT32_MAX);
+    const size_t cap1 = std::max<size_t>(cap, 1);
+    double *pa, *pb, *tp;
+    int64_t *ia, *ib, *ti;
+    float* fv;
+    TRY(ws_t(c, S_OUT_A, cap1, &pa));
+    TRY(ws_t(c, S_OUT_B, cap1, &pb));
+    TRY(ws_t(c, S_OUT_C, cap1, &ia));
+    TRY(ws_t(c, S_OUT_D, cap1, &ib));
+    TRY(ws_t(c, S_FEAT, cap1, &fv));
+    TRY(ws_t(c, S_TOPI, (size_t)m, &ti));
+    TRY(ws_t(c, S_TOPP, (size_t)m, &tp));
+    // 1) exact global tau_m over the candidates, keep f32 <= tau_m + 2*delta
+    //    (a count beyond the capacity: no survivors, the host falls back below)
+    k_band_filter<<<1, 1024, 0, c->stream>>>(cidx, cval, gs + 1, cap, (int)m, sa.band, ia, fv, gs + 2);
+    TRY(check_launch(c));
+    // 2) fp64 rescoring of the survivors, one warp each (grid-stride over the
+    //    device count; survivors are few, ~m, so 32 CTAs of 8 warps)
+    const size_t smem64 = predict64_smem(p->de);
+    if (smem64 > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem64);
+    CU(cudaFuncSetAttribute(k_rescore_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
+    k_rescore_warp<<<32, 256, smem64, c->stream>>>(p->de, ia, gs + 2, pa);
+    TRY(check_launch(c));
+    // 3) sort by (prediction, index) in one CTA when small
+    const int ssmem = 16 * kSmallSort;
+    CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3);
+    TRY(check_launch(c));
+    if (c->res_cap < (size_t)m * 16) {
+      if (c->res_pin) CU(cudaFreeHost(c->res_pin));
+      c->res_pin = nullptr;
+      c->res_cap = 0;
+      CU(cudaMallocHost(&c->res_pin, (size_t)m * 16));
+      c->res_cap = (size_t)m * 16;
+    }
+    double* rp = static_cast<double*>(c->res_pin);
+    int64_t* ri = reinterpret_cast<int64_t*>(rp + m);
+    CU(cudaMemcpyAsync(rp, tp, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));   // valid when the
+    CU(cudaMemcpyAsync(ri, ti, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));   // one-CTA sort ran
+    CU(cudaMemcpyAsync(hs, gs, 32, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
-    const uint32_t theta_key = hs[0], count = hs[1];
+    const uint32_t theta_key = hs[8], count = hs[9];
+    (void)theta_key;
     local.evaluated_frac = 1.0;
     if (prune) {
       uint64_t work;
-      std::memcpy(&work, hs + 4, 8);
+      std::memcpy(&work, hs + 10, 8);
       local.evaluated_frac = (double)work / ((double)n_ob * n_ib * ngroups * (kThreads / 32));   // warp-groups
     }
     local.group = B.G;
@@ -1243,46 +1291,18 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     if ((int64_t)count > c->cand_cap) {
       band = false;   // crowded guard band: fall back to the exact materialising path
     } else {
-      local.candidates = count;
-      // decode the final threshold on the host (same ordered-key map as the device)
-      uint32_t b = (theta_key & 0x80000000u) ? (theta_key & 0x7fffffffu) : ~theta_key;
-      float theta;
-      std::memcpy(&theta, &b, 4);
-      (void)theta;
-      const uint32_t cnt1 = std::max<uint32_t>(count, 1);
-      double *pa, *pb, *tp;
-      int64_t *ia, *ib, *ti;
-      float* fv;
-      TRY(ws_t(c, S_OUT_A, cnt1, &pa));
-      TRY(ws_t(c, S_OUT_B, cnt1, &pb));
-      TRY(ws_t(c, S_OUT_C, cnt1, &ia));
-      TRY(ws_t(c, S_OUT_D, cnt1, &ib));
-      TRY(ws_t(c, S_FEAT, cnt1, &fv));
-      TRY(ws_t(c, S_TOPI, (size_t)m, &ti));
-      TRY(ws_t(c, S_TOPP, (size_t)m, &tp));
-      // 1) exact global tau_m over the candidates, keep f32 <= tau_m + 2*delta
-      k_band_filter<<<1, 1024, 0, c->stream>>>(cidx, cval, count, (int)m, sa.band, ia, fv, gs + 2);
-      TRY(check_launch(c));
-      // 2) fp64 rescoring of the survivors, one warp each
-      const size_t smem64 = predict64_smem(p->de);
-      if (smem64 > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem64);
-      CU(cudaFuncSetAttribute(k_rescore_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
-      // survivors are few (~m); a fixed 32 x 8-warp grid avoids staging the
-      // weights into hundreds of idle CTAs (grid-stride over the device count)
-      const int rgrid = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)count + 7) / 8, 32));
-      k_rescore_warp<<<rgrid, 256, smem64, c->stream>>>(p->de, ia, gs + 2, pa);
-      TRY(check_launch(c));
-      // 3) sort by (prediction, index) in one CTA when small
-      const int ssmem = 16 * kSmallSort;
-      CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
-      k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3);
-      TRY(check_launch(c));
-      CU(cudaMemcpyAsync(hs, gs, 32, cudaMemcpyDeviceToHost, c->stream));
-      CU(cudaStreamSynchronize(c->stream));
       const uint32_t n2 = hs[2], big = hs[3], take = hs[4];
       local.candidates = n2;
-      if (!big) {
-        TRY(emit_top(c, tp, ti, take, m, out_idx, out_pred, out_n));
+      if (!big) {   // the lists already landed in pinned memory with the counters
+        const int64_t tk = std::min<int64_t>(m, take);
+        int64_t cnt = 0;
+        for (int64_t t = 0; t < tk; ++t) {
+          if (ri[t] == INT64_MAX || ri[t] < 0) break;
+          out_idx[cnt] = ri[t];
+          out_pred[cnt] = rp[t];
+          ++cnt;
+        }
+        *out_n = cnt;
       } else {
         double* pcur = pa;
         int64_t* icur = ia;

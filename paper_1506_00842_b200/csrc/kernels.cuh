@@ -40,8 +40,8 @@ __global__ void k_surr_best_final(const SurrPart* part, int n, SurrPart* out);
 
 // ---- final guard-band stage (select.cu) ------------------------------------
 constexpr int kSmallSort = 4096;  // survivors sorted in one CTA's shared memory
-__global__ void k_band_filter(const int64_t* cidx, const float* cval, uint32_t count, int m, float band,
-                              int64_t* out_idx, float* out_val, uint32_t* out_n);
+__global__ void k_band_filter(const int64_t* cidx, const float* cval, const uint32_t* count_ptr, uint32_t cap, int m,
+                              float band, int64_t* out_idx, float* out_val, uint32_t* out_n);
 __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint32_t* n_ptr, int m, double* out_pred,
                              int64_t* out_idx, uint32_t* status);
 

@@ -13,10 +13,16 @@
 namespace mlt {
 
 __global__ void __launch_bounds__(1024) k_band_filter(const int64_t* __restrict__ cidx, const float* __restrict__ cval,
-                                                      uint32_t count, int m, float band, int64_t* __restrict__ out_idx,
+                                                      const uint32_t* __restrict__ count_ptr, uint32_t cap, int m,
+                                                      float band, int64_t* __restrict__ out_idx,
                                                       float* __restrict__ out_val, uint32_t* __restrict__ out_n) {
   __shared__ uint32_t s_hist[256], s_sel[2], s_n;
   const int tid = threadIdx.x;
+  const uint32_t count = *count_ptr;   // written by the sweep (stream order)
+  if (count > cap) {                   // the buffer overflowed: the caller takes the exact path
+    if (tid == 0) *out_n = 0;
+    return;
+  }
   float theta = __int_as_float(0x7f800000);   // +inf: keep everything when count < m
   if (count >= (uint32_t)m) {
     const uint32_t key = block_select(
