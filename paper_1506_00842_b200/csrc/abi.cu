@@ -1682,13 +1682,45 @@ int mlt_surrogate_best(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* 
   size_t smem = 0;
   TRY(upload_surrogate(c, spec, reps, tpos, tdig, tfac, &ds, &smem));
   const int threads = 256;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((end - begin + threads - 1) / threads, (int64_t)c->sms * 8));
+  const double thr = std::isnan(threshold) ? -HUGE_VAL : threshold;
+  const int T = spec->n_terms;
+  // noise-free, <= 64 terms, <= 16 parameters: the odometer / hit-mask kernel
+  const bool runs = T <= 64 && hs.P <= 16 && (reps == 0 || !(ds.sigma > 0.0));
+  const int run = 256;
+  const int64_t units = runs ? (end - begin + run - 1) / run : end - begin;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + threads - 1) / threads, (int64_t)c->sms * 8));
   SurrPart* part;
   TRY(ws_t(c, S_PART, (size_t)grid + 1, &part));
-  if (smem > 48 * 1024) CU(cudaFuncSetAttribute(k_surr_best, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_surr_best<<<grid, threads, smem, c->stream>>>(dsp, dl, ds, begin, end, std::isnan(threshold) ? -HUGE_VAL : threshold,
-                                                  part);
-  TRY(check_launch(c));
+  uint64_t* gmask = nullptr;
+  if (runs) {
+    const int nm = dsp.voff[hs.P - 1] + dsp.radix[hs.P - 1];   // the kernel's mask offsets are dsp.voff
+    std::vector<uint64_t> masks(2 * (size_t)std::max(nm, 1), 0);
+    uint64_t b_ones = 0;
+    for (int t = 0; t < T; ++t) {
+      const int p1 = tpos[2 * t], d1 = tdig[2 * t], p2 = tpos[2 * t + 1], d2 = tdig[2 * t + 1];
+      if (d1 < 0) continue;                             // a value outside the list: never hits
+      const uint64_t bit = 1ull << t;
+      if (p2 < 0) {
+        masks[dsp.voff[p1] + d1] |= bit;
+        b_ones |= bit;
+      } else if (d2 >= 0) {
+        masks[dsp.voff[p1] + d1] |= bit;
+        masks[nm + dsp.voff[p2] + d2] |= bit;
+      }
+    }
+    CU(cudaMallocAsync(&gmask, masks.size() * 8, c->stream));
+    TRY(upload_pinned(c, gmask, masks.data(), masks.size() * 8));
+    const size_t smem_r = (size_t)T * 8 + (size_t)2 * nm * 8;
+    if (smem_r > 48 * 1024)
+      CU(cudaFuncSetAttribute(k_surr_best_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+    k_surr_best_runs<<<grid, threads, smem_r, c->stream>>>(dsp, dl, ds, gmask, nm, b_ones, begin, end, run, thr, part);
+    TRY(check_launch(c));
+    CU(cudaFreeAsync(gmask, c->stream));
+  } else {
+    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(k_surr_best, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_surr_best<<<grid, threads, smem, c->stream>>>(dsp, dl, ds, begin, end, thr, part);
+    TRY(check_launch(c));
+  }
   k_surr_best_final<<<1, 1024, 0, c->stream>>>(part, grid, part + grid);
   TRY(check_launch(c));
   SurrPart r;

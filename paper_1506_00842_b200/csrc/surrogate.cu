@@ -138,6 +138,111 @@ __global__ void k_surr_best(DSpace sp, DSpace lr, DSurr su, int64_t begin, int64
   }
 }
 
+// Noise-free search without rules (the ground truth of the tuner's slowdown):
+// each thread walks a run of consecutive indices with an odometer over the
+// digits held in registers, and tracks which terms hit as two 64-bit masks
+// (bit q of A: term q's first (parameter, digit) matches; of B: its second,
+// or always for one-parameter terms), updated by XOR when a digit changes.
+// The time is base times the hit factors in ascending term order -- the same
+// multiplications, in the same order, as surr_time, so it is bit-identical.
+constexpr int PMAX = 16;   // parameters handled by k_surr_best_runs (digits in registers)
+__global__ void __launch_bounds__(256) k_surr_best_runs(DSpace sp, DSpace lr, DSurr su, const uint64_t* __restrict__ gmask,
+                                                        int nm, uint64_t b_ones, int64_t begin, int64_t end, int run,
+                                                        double thr, SurrPart* __restrict__ part) {
+  extern __shared__ double s_fac[];                 // [T] factors, then A masks [nm], B masks [nm]
+  uint64_t* sA = reinterpret_cast<uint64_t*>(s_fac + su.T);
+  uint64_t* sB = sA + nm;
+  for (int t = threadIdx.x; t < su.T; t += blockDim.x) s_fac[t] = su.tfac[t];
+  for (int q = threadIdx.x; q < 2 * nm; q += blockDim.x) sA[q] = gmask[q];
+  __syncthreads();
+  const int P = sp.P;
+  const bool rules = sp.R > 0 || lr.R > 0;
+  double bt = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+  int64_t bi = INT64_MAX;
+  unsigned long long nv = 0, nb = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * run;
+  for (int64_t r0 = begin + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * run; r0 < end; r0 += stride) {
+    const int64_t r1 = r0 + run < end ? r0 + run : end;
+    int dig[PMAX];    // registers (static indices only)
+    int dl[kMaxP];    // the same digits for the rule checks (dynamic indices: local memory)
+    uint64_t x = (uint64_t)r0;
+#pragma unroll
+    for (int p = PMAX - 1; p >= 0; --p) {
+      dig[p] = 0;
+      if (p < P) {
+        const uint64_t q = x / (uint64_t)sp.radix[p];
+        dig[p] = (int)(x - q * (uint64_t)sp.radix[p]);
+        x = q;
+      }
+      if (rules) dl[p] = dig[p];
+    }
+    uint64_t A = 0, B = b_ones;
+#pragma unroll
+    for (int p = 0; p < PMAX; ++p)
+      if (p < P) {
+        A |= sA[sp.voff[p] + dig[p]];
+        B |= sB[sp.voff[p] + dig[p]];
+      }
+    for (int64_t i = r0; i < r1; ++i) {
+      if (!rules || (rules_ok(sp, dl) && rules_ok(lr, dl))) {
+        uint64_t h = A & B;
+        double t = su.base;
+        while (h) {
+          t = __dmul_rn(t, s_fac[__ffsll((long long)h) - 1]);
+          h &= h - 1;
+        }
+        ++nv;
+        nb += (t < thr);
+        if (key_less(t, i, bt, bi)) {
+          bt = t;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int p = PMAX - 1; p >= 0; --p) {   // odometer: next index, last parameter fastest
+        if (p < P) {
+          const int o = dig[p];
+          int nw = o + 1;
+          const bool wrap = nw == sp.radix[p];
+          if (wrap) nw = 0;
+          A ^= sA[sp.voff[p] + o] ^ sA[sp.voff[p] + nw];
+          B ^= sB[sp.voff[p] + o] ^ sB[sp.voff[p] + nw];
+          dig[p] = nw;
+          if (rules) dl[p] = nw;
+          if (!wrap) break;
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ot = __shfl_down_sync(0xffffffffu, bt, o);
+    const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+    nv += __shfl_down_sync(0xffffffffu, nv, o);
+    nb += __shfl_down_sync(0xffffffffu, nb, o);
+    if (key_less(ot, oi, bt, bi)) {
+      bt = ot;
+      bi = oi;
+    }
+  }
+  __shared__ SurrPart w[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) w[wid] = SurrPart{bt, bi, (int64_t)nv, (int64_t)nb};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    SurrPart r = w[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
+      if (key_less(w[q].t, w[q].i, r.t, r.i)) {
+        r.t = w[q].t;
+        r.i = w[q].i;
+      }
+      r.n_valid += w[q].n_valid;
+      r.n_below += w[q].n_below;
+    }
+    part[blockIdx.x] = r;
+  }
+}
+
+
 __global__ void k_surr_best_final(const SurrPart* __restrict__ part, int n, SurrPart* __restrict__ out) {
   __shared__ SurrPart w[1024];
   SurrPart r{__longlong_as_double(0x7ff0000000000000ll), INT64_MAX, 0, 0};

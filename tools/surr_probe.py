@@ -11,4 +11,11 @@ r = b.B200SurrogateRunner(json.loads((G / "surrogates.json").read_text())["synth
 r.exhaustive_best(0, 1 << 16)
 t0 = time.perf_counter()
 res = r.exhaustive_best()
-print(json.dumps({"best": res, "wall_s": time.perf_counter() - t0}))
+out = {"best": res, "wall_s": time.perf_counter() - t0}
+doc = dict(json.loads((G / "surrogates.json").read_text())["synthetic-1e8"], noise_cv=0.0)
+r0 = b.B200SurrogateRunner(doc, sp)   # noise-free: the odometer / hit-mask kernel
+r0.exhaustive_best(0, 1 << 16)
+t0 = time.perf_counter()
+out["noise_free_best"] = r0.exhaustive_best()
+out["noise_free_wall_s"] = time.perf_counter() - t0
+print(json.dumps(out))
