@@ -1684,8 +1684,8 @@ int mlt_surrogate_best(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* 
   const int threads = 256;
   const double thr = std::isnan(threshold) ? -HUGE_VAL : threshold;
   const int T = spec->n_terms;
-  // noise-free, <= 64 terms, <= 16 parameters: the odometer / hit-mask kernel
-  const bool runs = T <= 64 && hs.P <= 16 && (reps == 0 || !(ds.sigma > 0.0));
+  // <= 64 terms, <= 16 parameters: the odometer / hit-mask kernel
+  const bool runs = T <= 64 && hs.P <= 16;
   const int run = 256;
   const int64_t units = runs ? (end - begin + run - 1) / run : end - begin;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + threads - 1) / threads, (int64_t)c->sms * 8));

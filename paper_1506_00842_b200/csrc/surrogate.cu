@@ -138,7 +138,7 @@ __global__ void k_surr_best(DSpace sp, DSpace lr, DSurr su, int64_t begin, int64
   }
 }
 
-// Noise-free search without rules (the ground truth of the tuner's slowdown):
+// Exhaustive search (the ground truth of the tuner's slowdown), <= 64 terms:
 // each thread walks a run of consecutive indices with an odometer over the
 // digits held in registers, and tracks which terms hit as two 64-bit masks
 // (bit q of A: term q's first (parameter, digit) matches; of B: its second,
@@ -190,6 +190,11 @@ __global__ void __launch_bounds__(256) k_surr_best_runs(DSpace sp, DSpace lr, DS
         while (h) {
           t = __dmul_rn(t, s_fac[__ffsll((long long)h) - 1]);
           h &= h - 1;
+        }
+        if (su.reps > 0 && su.sigma > 0.0) {   // measured times: exactly surr_time's noise
+          double z = unit_normal(su.seed, (uint64_t)i, 0);
+          for (int r = 1; r < su.reps; ++r) z = fmin(z, unit_normal(su.seed, (uint64_t)i, r));
+          t = __dmul_rn(t, exp(__dmul_rn(su.sigma, z)));
         }
         ++nv;
         nb += (t < thr);
