@@ -1593,6 +1593,29 @@ int read_surrogate(const mlt_space* space, const mlt_surrogate* sp, const HostSp
 }
 
 // never-hitting terms keep their position but an impossible digit (-2 never equals a digit)
+// Term-hit masks of the surrogate kernels (k_surr_best_runs, k_surr_times_masks):
+// A[voff[p] + v] has bit t when term t's first (parameter, digit) is (p, v);
+// B likewise for its second; one-parameter terms always pass B (b_ones).
+// Terms whose value is not in the list never hit. Needs T <= 64.
+void term_masks(const DSpace& d, int P, int T, const std::vector<int>& tpos, const std::vector<int>& tdig,
+                std::vector<uint64_t>* masks, uint64_t* b_ones, int* nm) {
+  *nm = d.voff[P - 1] + d.radix[P - 1];
+  masks->assign(2 * (size_t)std::max(*nm, 1), 0);
+  *b_ones = 0;
+  for (int t = 0; t < T; ++t) {
+    const int p1 = tpos[2 * t], d1 = tdig[2 * t], p2 = tpos[2 * t + 1], d2 = tdig[2 * t + 1];
+    if (d1 < 0) continue;
+    const uint64_t bit = 1ull << t;
+    if (p2 < 0) {
+      (*masks)[d.voff[p1] + d1] |= bit;
+      *b_ones |= bit;
+    } else if (d2 >= 0) {
+      (*masks)[d.voff[p1] + d1] |= bit;
+      (*masks)[*nm + d.voff[p2] + d2] |= bit;
+    }
+  }
+}
+
 int upload_surrogate(mlt_ctx* c, const mlt_surrogate* sp, int reps, std::vector<int>& tpos, std::vector<int>& tdig,
                      const std::vector<double>& tfac, DSurr* d, size_t* smem) {
   const int T = sp->n_terms;
@@ -1649,8 +1672,24 @@ int mlt_surrogate_times(mlt_ctx* c, const mlt_space* space, const mlt_surrogate*
   TRY(ws_t(c, S_OUT_A, n, &dt));
   TRY(ws_t(c, S_OUT_C, n, &dok));
   CU(cudaMemcpyAsync(di, idx, n * 8, cudaMemcpyHostToDevice, c->stream));
-  if (smem > 48 * 1024) CU(cudaFuncSetAttribute(k_surr_times, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_surr_times<<<grid_for(c, n, 256), 256, smem, c->stream>>>(dl, ds, di, n, dt, dok);
+  const int T = spec->n_terms;
+  uint64_t* gmask = nullptr;
+  if (T <= 64 && hs.P <= 16) {
+    int nm = 0;
+    std::vector<uint64_t> masks;
+    uint64_t b_ones = 0;
+    term_masks(dl, hs.P, T, tpos, tdig, &masks, &b_ones, &nm);
+    CU(cudaMallocAsync(&gmask, masks.size() * 8, c->stream));
+    TRY(upload_pinned(c, gmask, masks.data(), masks.size() * 8));
+    const size_t smem_m = (size_t)T * 8 + (size_t)2 * nm * 8;
+    if (smem_m > 48 * 1024)
+      CU(cudaFuncSetAttribute(k_surr_times_masks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_m));
+    k_surr_times_masks<<<grid_for(c, n, 256), 256, smem_m, c->stream>>>(dl, ds, gmask, nm, b_ones, di, n, dt, dok);
+    CU(cudaFreeAsync(gmask, c->stream));
+  } else {
+    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(k_surr_times, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_surr_times<<<grid_for(c, n, 256), 256, smem, c->stream>>>(dl, ds, di, n, dt, dok);
+  }
   TRY(check_launch(c));
   CU(cudaMemcpyAsync(times, dt, n * 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, c->stream));
@@ -1693,21 +1732,10 @@ int mlt_surrogate_best(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* 
   TRY(ws_t(c, S_PART, (size_t)grid + 1, &part));
   uint64_t* gmask = nullptr;
   if (runs) {
-    const int nm = dsp.voff[hs.P - 1] + dsp.radix[hs.P - 1];   // the kernel's mask offsets are dsp.voff
-    std::vector<uint64_t> masks(2 * (size_t)std::max(nm, 1), 0);
+    int nm = 0;
+    std::vector<uint64_t> masks;
     uint64_t b_ones = 0;
-    for (int t = 0; t < T; ++t) {
-      const int p1 = tpos[2 * t], d1 = tdig[2 * t], p2 = tpos[2 * t + 1], d2 = tdig[2 * t + 1];
-      if (d1 < 0) continue;                             // a value outside the list: never hits
-      const uint64_t bit = 1ull << t;
-      if (p2 < 0) {
-        masks[dsp.voff[p1] + d1] |= bit;
-        b_ones |= bit;
-      } else if (d2 >= 0) {
-        masks[dsp.voff[p1] + d1] |= bit;
-        masks[nm + dsp.voff[p2] + d2] |= bit;
-      }
-    }
+    term_masks(dsp, hs.P, T, tpos, tdig, &masks, &b_ones, &nm);
     CU(cudaMallocAsync(&gmask, masks.size() * 8, c->stream));
     TRY(upload_pinned(c, gmask, masks.data(), masks.size() * 8));
     const size_t smem_r = (size_t)T * 8 + (size_t)2 * nm * 8;

@@ -38,6 +38,8 @@ __global__ void k_surr_times(DSpace lr, DSurr su, const int64_t* idx, int64_t n,
 __global__ void k_surr_best(DSpace sp, DSpace lr, DSurr su, int64_t begin, int64_t end, double thr, SurrPart* part);
 __global__ void k_surr_best_runs(DSpace sp, DSpace lr, DSurr su, const uint64_t* gmask, int nm, uint64_t b_ones, int64_t begin,
                                  int64_t end, int run, double thr, SurrPart* part);
+__global__ void k_surr_times_masks(DSpace lr, DSurr su, const uint64_t* gmask, int nm, uint64_t b_ones,
+                                   const int64_t* idx, int64_t n, double* times, uint8_t* ok);
 __global__ void k_surr_best_final(const SurrPart* part, int n, SurrPart* out);
 
 // ---- final guard-band stage (select.cu) ------------------------------------

@@ -248,6 +248,55 @@ __global__ void __launch_bounds__(256) k_surr_best_runs(DSpace sp, DSpace lr, DS
 }
 
 
+// k_surr_times with the term-hit masks of k_surr_best_runs (<= 64 terms,
+// <= 16 parameters): digits decoded into registers, the same products in the
+// same term order, the same noise.
+__global__ void __launch_bounds__(256) k_surr_times_masks(DSpace lr, DSurr su, const uint64_t* __restrict__ gmask,
+                                                          int nm, uint64_t b_ones, const int64_t* __restrict__ idx,
+                                                          int64_t n, double* __restrict__ times,
+                                                          uint8_t* __restrict__ ok) {
+  extern __shared__ double s_fac[];
+  uint64_t* sA = reinterpret_cast<uint64_t*>(s_fac + su.T);
+  uint64_t* sB = sA + nm;
+  for (int t = threadIdx.x; t < su.T; t += blockDim.x) s_fac[t] = su.tfac[t];
+  for (int q = threadIdx.x; q < 2 * nm; q += blockDim.x) sA[q] = gmask[q];
+  __syncthreads();
+  const int P = lr.P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t x0 = (uint64_t)idx[i];
+    int dl[kMaxP];
+    uint64_t x = x0, A = 0, B = b_ones;
+#pragma unroll
+    for (int p = PMAX - 1; p >= 0; --p) {
+      if (p < P) {
+        const uint64_t q = x / (uint64_t)lr.radix[p];
+        const int d = (int)(x - q * (uint64_t)lr.radix[p]);
+        x = q;
+        A |= sA[lr.voff[p] + d];
+        B |= sB[lr.voff[p] + d];
+        dl[p] = d;
+      }
+    }
+    const bool good = lr.R == 0 || rules_ok(lr, dl);
+    ok[i] = good;
+    double t = __longlong_as_double(0x7ff8000000000000ll);
+    if (good) {
+      uint64_t h = A & B;
+      t = su.base;
+      while (h) {
+        t = __dmul_rn(t, s_fac[__ffsll((long long)h) - 1]);
+        h &= h - 1;
+      }
+      if (su.reps > 0 && su.sigma > 0.0) {
+        double z = unit_normal(su.seed, x0, 0);
+        for (int r = 1; r < su.reps; ++r) z = fmin(z, unit_normal(su.seed, x0, r));
+        t = __dmul_rn(t, exp(__dmul_rn(su.sigma, z)));
+      }
+    }
+    times[i] = t;
+  }
+}
+
 __global__ void k_surr_best_final(const SurrPart* __restrict__ part, int n, SurrPart* __restrict__ out) {
   __shared__ SurrPart w[1024];
   SurrPart r{__longlong_as_double(0x7ff0000000000000ll), INT64_MAX, 0, 0};
