@@ -29,8 +29,9 @@
  *       MLT_EDATA -> InsufficientDataError, MLT_EDIVERGED -> DivergenceError,
  *       MLT_ECUDA / MLT_EINTERNAL -> RuntimeError.
  *   - Every call is synchronous on the context's stream (library-owned, or the
- *     caller's via mlt_ctx_set_stream). One context per device; a context is
- *     not re-entrant (the reference runner contract is sequential too).
+ *     caller's via mlt_ctx_set_stream). Calls on one context are serialised
+ *     by a per-context mutex (safe to share across threads; concurrent work on
+ *     one device runs in parallel only through several contexts).
  *   - There is no CPU fallback: without a usable sm_100 device every compute
  *     entry point fails with MLT_ECUDA (mlt_host_permutations is host-only:
  *     it reproduces the reference's RNG stream, it computes nothing of the path).

@@ -2,7 +2,9 @@
 
 Packs duck-typed space / ensemble objects — this package's own or the
 reference `mltune`'s — into the plain C descriptors, owns one library context
-per CUDA device, and maps native status codes to the tuner's exceptions.
+per CUDA device (the library serialises calls on a context, so one context
+can be shared across threads), and maps native status codes to the tuner's
+exceptions.
 Nothing here computes: every numeric entry point runs on the B200. If the
 library or the device is missing, calls raise NativeUnavailableError.
 """
@@ -125,8 +127,11 @@ _SIGNATURES = [
 ]
 EXPORTS = tuple(name for name, _, _ in _SIGNATURES)
 
+ABI_VERSION = 1      # MLT_ABI_VERSION of include/mltune_b200.h this binding's structs follow
+
 _lib = None
 _lib_lock = threading.Lock()
+_ctx_lock = threading.Lock()
 _ctxs: dict[int, C.c_void_p] = {}
 
 
@@ -143,6 +148,10 @@ def lib():
                 fn = getattr(h, name)
                 fn.restype = res
                 fn.argtypes = args
+            if h.mlt_abi_version() != ABI_VERSION:
+                raise errors.NativeUnavailableError(
+                    f"{_LIB_PATH} has ABI version {h.mlt_abi_version()}, this binding expects {ABI_VERSION}; "
+                    "rebuild it with __graft_entry__.build()")
             _lib = h
     return _lib
 
@@ -184,10 +193,14 @@ def default_device() -> int:
 def ctx(device: int | None = None) -> C.c_void_p:
     """The library context of `device` (created on first use)."""
     dev = default_device() if device is None else int(device)
-    if dev not in _ctxs:
-        h = C.c_void_p()
-        check(lib().mlt_ctx_create(dev, C.byref(h)), "mlt_ctx_create")
-        _ctxs[dev] = h
+    hit = _ctxs.get(dev)
+    if hit is not None:
+        return hit
+    with _ctx_lock:            # one context per device even under concurrent first use
+        if dev not in _ctxs:
+            h = C.c_void_p()
+            check(lib().mlt_ctx_create(dev, C.byref(h)), "mlt_ctx_create")
+            _ctxs[dev] = h
     return _ctxs[dev]
 
 
@@ -197,10 +210,11 @@ def extra_ctx(device: int, slot: int) -> C.c_void_p:
     if slot == 0:
         return ctx(device)
     key = (int(device), int(slot))
-    if key not in _ctxs:
-        h = C.c_void_p()
-        check(lib().mlt_ctx_create(int(device), C.byref(h)), "mlt_ctx_create")
-        _ctxs[key] = h
+    with _ctx_lock:
+        if key not in _ctxs:
+            h = C.c_void_p()
+            check(lib().mlt_ctx_create(int(device), C.byref(h)), "mlt_ctx_create")
+            _ctxs[key] = h
     return _ctxs[key]
 
 

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -41,6 +42,8 @@ int fail(int code, const char* fmt, ...) {
                   __FILE__, __LINE__);                                                  \
   } while (0)
 
+#define CTX_GUARD(c) std::lock_guard<std::recursive_mutex> ctx_guard_((c)->mu)
+
 #define TRY(expr)            \
   do {                       \
     int rc_ = (expr);        \
@@ -71,6 +74,10 @@ struct mlt_ctx {
   size_t stage_cap = 0;
   size_t stage_off = 0;         // next free byte of the ring
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // Serialises every entry point on this context (workspace slots, pinned
+  // staging and the stream are per-context state): concurrent callers of one
+  // context queue instead of racing. Recursive: mlt_top_m -> mlt_plan_create.
+  std::recursive_mutex mu;
 };
 
 namespace {
@@ -769,12 +776,14 @@ int mlt_ctx_destroy(mlt_ctx* c) {
 
 int mlt_ctx_set_stream(mlt_ctx* c, void* stream) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
   return MLT_OK;
 }
 
 int mlt_ctx_set_profiling(mlt_ctx* c, int on) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   c->prof = on != 0;
   return MLT_OK;
 }
@@ -783,6 +792,7 @@ int64_t mlt_ctx_launches(mlt_ctx* c) { return c ? c->launches : -1; }
 
 int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   switch (key) {
     case MLT_OPT_PATH: c->opt_path = (int)value; return MLT_OK;
     case MLT_OPT_GROUP: c->opt_group = (int)value; return MLT_OK;
@@ -795,6 +805,7 @@ int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
 
 int mlt_decode(mlt_ctx* c, const mlt_space* space, const int64_t* idx, int64_t n, int64_t* values_out) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   if (n == 0) return MLT_OK;
   CU(cudaSetDevice(c->dev));
@@ -819,6 +830,7 @@ int mlt_decode(mlt_ctx* c, const mlt_space* space, const int64_t* idx, int64_t n
 
 int mlt_valid_mask(mlt_ctx* c, const mlt_space* space, const int64_t* idx, int64_t n, uint8_t* mask_out) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   if (n == 0) return MLT_OK;
   CU(cudaSetDevice(c->dev));
@@ -844,6 +856,7 @@ int mlt_valid_mask(mlt_ctx* c, const mlt_space* space, const int64_t* idx, int64
 
 int mlt_encode(mlt_ctx* c, const int32_t* counts, int32_t d, const int64_t* idx, int64_t n, double* feat_out) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (d < 1 || d > kMaxP) return fail(MLT_EINVAL, "input dimension must be 1..%d", kMaxP);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   if (n == 0) return MLT_OK;
@@ -869,6 +882,7 @@ int mlt_encode(mlt_ctx* c, const int32_t* counts, int32_t d, const int64_t* idx,
 
 int mlt_predict_indices(mlt_ctx* c, const mlt_ensemble* ens, const int64_t* idx, int64_t n, double* pred_out) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   CU(cudaSetDevice(c->dev));
   HostEns he;
@@ -893,6 +907,7 @@ int mlt_predict_indices(mlt_ctx* c, const mlt_ensemble* ens, const int64_t* idx,
 
 int mlt_predict_features(mlt_ctx* c, const mlt_ensemble* ens, const double* x, int64_t n, double* pred_out) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   CU(cudaSetDevice(c->dev));
   HostEns he;
@@ -914,6 +929,7 @@ int mlt_predict_features(mlt_ctx* c, const mlt_ensemble* ens, const double* x, i
 
 int mlt_member_outputs(mlt_ctx* c, const mlt_ensemble* ens, const double* x, int64_t n, double* out) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   CU(cudaSetDevice(c->dev));
   HostEns he;
@@ -937,6 +953,7 @@ int mlt_member_outputs(mlt_ctx* c, const mlt_ensemble* ens, const double* x, int
 
 int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, mlt_plan** out) {
   if (!c || !out) return fail(MLT_EINVAL, "ctx/out is NULL");
+  CTX_GUARD(c);
   *out = nullptr;
   CU(cudaSetDevice(c->dev));
   mlt_plan* p = new mlt_plan();
@@ -962,6 +979,7 @@ int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens,
 
 int mlt_plan_destroy(mlt_plan* p) {
   if (!p) return MLT_OK;
+  CTX_GUARD(p->ctx);
   cudaSetDevice(p->ctx->dev);
   plan_free(p);   // stream-ordered frees: no host wait
   delete p;
@@ -1397,6 +1415,7 @@ static int plan_top_m_range(mlt_plan* p, int64_t m, int64_t begin, int64_t end, 
 int mlt_plan_top_m(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* out_idx, double* out_pred,
                    int64_t* out_n, mlt_sweep_stats* st) {
   if (!p) return fail(MLT_EINVAL, "plan is NULL");
+  CTX_GUARD(p->ctx);
   return plan_top_m_range(p, m, begin, end, out_idx, out_pred, out_n, st);
 }
 
@@ -1404,6 +1423,7 @@ int mlt_top_m(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, int64
               const int64_t* idx_list, int64_t n_list, int64_t* out_idx, double* out_pred, int64_t* out_n,
               mlt_sweep_stats* st) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
   mlt_plan* p = nullptr;
   TRY(mlt_plan_create(c, space, ens, &p));
@@ -1496,6 +1516,7 @@ int mlt_top_m_multi(mlt_ctx* const* ctxs, int32_t n_ctx, const mlt_space* space,
 int mlt_merge_top_m(mlt_ctx* c, const int64_t* dev_idx, const double* dev_pred, int64_t n, int64_t m,
                     int64_t* out_idx, double* out_pred, int64_t* out_n) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   CU(cudaSetDevice(c->dev));
@@ -1535,6 +1556,7 @@ int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* launches, cons
 int mlt_train_members(mlt_ctx* c, const mlt_train_desc* desc, double* w1, double* b1, double* w2, double* b2,
                       double* loss_first, double* loss_final, int32_t* diverged_epoch) {
   if (!c || !desc) return fail(MLT_EINVAL, "ctx/desc is NULL");
+  CTX_GUARD(c);
   const char* err = "";
   const int rc = mlt_train_members_impl(c->dev, c->stream, &c->launches, desc, w1, b1, w2, b2, loss_first,
                                         loss_final, diverged_epoch, &err);
@@ -1647,6 +1669,7 @@ extern "C" {
 int mlt_surrogate_times(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* spec, const int64_t* idx, int64_t n,
                         int32_t reps, double* times, uint8_t* ok) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
   if (n < 0) return fail(MLT_EINVAL, "negative count");
   if (reps < 0) return fail(MLT_EINVAL, "repetitions must be >= 0");
   CU(cudaSetDevice(c->dev));
@@ -1701,6 +1724,7 @@ int mlt_surrogate_best(mlt_ctx* c, const mlt_space* space, const mlt_surrogate* 
                        int32_t reps, double threshold, int64_t* best_idx, double* best_time, int64_t* n_valid,
                        int64_t* n_below) {
   if (!c || !best_idx || !best_time || !n_valid || !n_below) return fail(MLT_EINVAL, "NULL argument");
+  CTX_GUARD(c);
   if (reps < 0) return fail(MLT_EINVAL, "repetitions must be >= 0");
   CU(cudaSetDevice(c->dev));
   HostSpace hs, lr;

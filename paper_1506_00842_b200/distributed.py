@@ -85,11 +85,11 @@ def top_m_arrays_sharded(ensemble, space, m: int, group=None, local_fn=None, mer
 def top_m_predicted(ensemble, space, m: int, sweep_cap=None, seed: int = 0, group=None):
     """Drop-in for tuner.top_m_predicted across the ranks of `group`
     (sweep_cap subsets are small: they run on each rank's device unsharded)."""
-    from .tuner import top_m_predicted as single
+    from .tuner import configs_of, top_m_predicted as single
     if sweep_cap is not None and space.cardinality() > sweep_cap:
         return single(ensemble, space, m, sweep_cap, seed)
     idx, pred = top_m_arrays_sharded(ensemble, space, m, group)
-    return list(zip(space.configs_at(idx), np.asarray(pred, dtype=np.float64).tolist()))
+    return list(zip(configs_of(space, idx), np.asarray(pred, dtype=np.float64).tolist()))
 
 
 def top_m_arrays_multi_device(ensemble, space, m: int, devices, begin: int = 0, end: int | None = None,
@@ -170,7 +170,8 @@ def _measured_slice_best(runner, space, lo, hi, repetitions=None, chunk=1 << 17)
     for s in range(lo, hi, chunk):
         idx = np.arange(s, min(s + chunk, hi), dtype=np.int64)
         if getattr(space, "rules", ()):
-            idx = idx[space.valid_mask_indices(idx)]
+            idx = idx[space.valid_mask_indices(idx)] if hasattr(space, "valid_mask_indices") else \
+                idx[space.static_valid_mask(space.decode_indices(idx))]
         if idx.size == 0:
             continue
         times, ok = runner.measured_times(idx, reps)

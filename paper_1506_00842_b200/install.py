@@ -6,9 +6,13 @@
 Rebinds the module globals the reference resolves at call time:
 `mltune.tuner.top_m_predicted` and `mltune.tuner.train_ensemble`
 (autotune looks both up as module globals, tuner.py:25, :152, :155),
-`mltune.evaluation.train_ensemble` (evaluation.py:22, :134), and the
-package-level re-exports (__init__.py:44-61). Native errors then raise the
-reference's own exception classes.
+`mltune.evaluation.train_ensemble` (evaluation.py:22, :134),
+`mltune.cli.train_ensemble` (cli.py:44-49, :324: `mltune train`),
+`mltune.model.train_ensemble / train_network` and the package-level
+re-exports (__init__.py:44-61). Native errors then raise the reference's own
+exception classes. The replacements take the reference's own objects
+(ParamSpace, SampleSet, TrainConfig, Ensemble) structurally — see
+tests/test_dropin_reference.py, which drives the real `mltune` through here.
 """
 
 from __future__ import annotations
@@ -30,6 +34,14 @@ def install(mltune_module=None) -> None:
                (mt.evaluation, "train_ensemble", model.train_ensemble),
                (mt, "top_m_predicted", tuner.top_m_predicted),
                (mt, "train_ensemble", model.train_ensemble)]
+    for sub, names in (("model", ("train_ensemble", "train_network")), ("cli", ("train_ensemble",))):
+        try:
+            mod = importlib.import_module(f"{mt.__name__}.{sub}")
+        except ImportError:
+            continue
+        targets += [(mod, n, getattr(model, n)) for n in names if hasattr(mod, n)]
+    if hasattr(mt, "train_network"):
+        targets.append((mt, "train_network", model.train_network))
     for mod, attr, fn in targets:
         _saved.setdefault((mod.__name__, attr), (mod, getattr(mod, attr)))
         setattr(mod, attr, fn)

@@ -106,6 +106,17 @@ def top_m_arrays(ensemble, space, m: int, begin: int = 0, end: int | None = None
     return res + (st.as_dict(),) if with_stats else res
 
 
+def configs_of(space, indices) -> list:
+    """Configuration tuples of `indices`. Works on any space object the
+    reference's `top_m_predicted` accepts: this package's ParamSpace has a
+    batched `configs_at`; the reference's has only the scalar `config_at`
+    (paramspace.py:149-158), which is what its own sweep uses (tuner.py:131)."""
+    batched = getattr(space, "configs_at", None)
+    if batched is not None:
+        return batched(indices)
+    return [space.config_at(int(i)) for i in indices]
+
+
 def top_m_predicted(ensemble, space, m: int, sweep_cap: int | None = None, seed: int = 0) -> list:
     """The m statically-valid configurations with the lowest predicted times,
     ascending, ties broken by index; fewer when fewer are valid (tuner.py:95-131)."""
@@ -117,7 +128,7 @@ def top_m_predicted(ensemble, space, m: int, sweep_cap: int | None = None, seed:
         idx, pred = top_m_arrays(ensemble, space, m, indices=subset)
     else:
         idx, pred = top_m_arrays(ensemble, space, m)
-    return list(zip(space.configs_at(idx), pred.tolist()))
+    return list(zip(configs_of(space, idx), pred.tolist()))
 
 
 def measure_configs(space, runner, configs, repetitions: int | None = None) -> list:

@@ -69,3 +69,22 @@ def gpu_ok():
     from paper_1506_00842_b200 import _native as N
     N.ctx(0)   # raises NativeUnavailableError without a B200: the GPU tests must not pass silently
     return True
+
+
+def oracle_of_product_ensemble(ens):
+    """The oracle restatement of an in-memory product (or reference) Ensemble."""
+    from oracle.model import OEnsemble, ONet
+    nets = [ONet(np.asarray(m.weights_hidden, dtype=np.float64), np.asarray(m.biases_hidden, dtype=np.float64),
+                 np.asarray(m.weights_out, dtype=np.float64), float(m.bias_out), float(m.target_mean),
+                 float(m.target_std)) for m in ens.members]
+    return OEnsemble(nets, [len(v) for _, v in ens.encoder.params])
+
+
+def oracle_of_product_space(sp):
+    """The oracle restatement of an in-memory ParamSpace (product or reference)."""
+    from oracle.space import space_from_doc
+    return space_from_doc({"name": sp.name,
+                           "params": [{"name": p.name, "values": list(p.values)} for p in sp.params],
+                           "rules": [{"kind": r.kind, "operands": list(r.operands),
+                                      "coefficients": list(r.coefficients), "bound": int(r.bound)}
+                                     for r in getattr(sp, "rules", ())]})

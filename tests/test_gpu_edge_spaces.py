@@ -1,12 +1,17 @@
 """Unusual space shapes through the device sweep: one huge parameter, many
 binary parameters, single-value parameters, 32 parameters (a slice). For each,
-the fp32 guard-band sweep (with and without pruning) must return exactly the
-fp64 materialising path's top-m (ties by index included)."""
+the fp32 guard-band sweep (with and without pruning) and the fp64
+materialising path must all return the ORACLE's top-m (oracle/tuner.py, the
+reference's chunked predict + lexsort; ties by index included)."""
 
 from __future__ import annotations
 
+from functools import lru_cache
+
 import numpy as np
 import pytest
+
+from conftest import oracle_of_product_ensemble, oracle_of_product_space
 
 pytestmark = pytest.mark.gpu
 
@@ -49,6 +54,19 @@ CASES = [
 ]
 
 
+@lru_cache(maxsize=None)
+def _oracle_top(name, trial, m_max=100):
+    """Oracle top-m_max of CASES[name] / trial (prefixes give every smaller m:
+    the lexsort order is total)."""
+    from oracle.tuner import top_m
+    radices, rng_ = {c[0]: (c[1], c[2]) for c in CASES}[name]
+    sp = _space(name, radices)
+    lo, hi = rng_ if rng_ else (0, sp.cardinality())
+    k, scale = [(3, 0.7), (5, 3.0)][trial]
+    ens = _ensemble(sp, k, scale, 100 * len(radices) + trial)
+    return top_m(oracle_of_product_ensemble(ens), oracle_of_product_space(sp), m_max, begin=lo, end=hi)
+
+
 @pytest.mark.parametrize("name,radices,rng_", CASES)
 @pytest.mark.parametrize("m", [1, 10, 100])
 def test_band_and_pruned_equal_exact(name, radices, rng_, m):
@@ -58,8 +76,11 @@ def test_band_and_pruned_equal_exact(name, radices, rng_, m):
     lo, hi = rng_ if rng_ else (0, sp.cardinality())
     for trial, (k, scale) in enumerate([(3, 0.7), (5, 3.0)]):
         ens = _ensemble(sp, k, scale, 100 * len(radices) + trial)
+        oi, op = _oracle_top(name, trial)
         _opt(N.MLT_OPT_PATH, 1)
         ref = top_m_arrays(ens, sp, m, begin=lo, end=hi)
+        assert np.array_equal(ref[0], oi[:m]), (name, m, trial, "exact path vs oracle")
+        np.testing.assert_allclose(ref[1], op[:m], rtol=1e-12, atol=0)
         _opt(N.MLT_OPT_PATH, 0)
         for prune in (0, 1):
             _opt(N.MLT_OPT_PRUNE, prune)

@@ -15,8 +15,9 @@ import math
 import numpy as np
 import pytest
 
-from conftest import (CASE_SPACE, golden, oracle_ensemble, oracle_space, product_ensemble, product_space,
-                      surrogates_doc)
+from conftest import (CASE_SPACE, golden, oracle_ensemble, oracle_of_product_ensemble, oracle_space,
+                      product_ensemble, product_space, surrogates_doc)
+from oracle.tuner import top_m as oracle_top_m
 
 pytestmark = pytest.mark.gpu
 
@@ -202,6 +203,9 @@ def test_pruned_random_ensembles_and_rules():
             set_opt(N.MLT_OPT_PRUNE, pr)
             res.append(top_m_arrays(ens, sp, 100))
         assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1]), trial
+        oi, op = oracle_top_m(oracle_of_product_ensemble(ens), oracle_space("stereo"), 100)
+        assert np.array_equal(res[0][0], oi), (trial, "vs oracle")
+        np.testing.assert_allclose(res[0][1], op, rtol=1e-12, atol=0)
     set_opt(N.MLT_OPT_PRUNE, 1)
     g = golden("topm_conv-rules_k11.npz")
     ens = product_ensemble("conv_k11")
