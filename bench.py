@@ -14,9 +14,14 @@ per-rank top-200 and a device merge. `value` = configurations / step time
 the same metric through the public Python API from host objects (weights
 H2D and results D2H inside the timed region). Rank 0 prints one JSON line.
 
---impl reference times the reference algorithm on the host CPU (the numpy
-restatement in oracle/, pinned to the real reference by tests/golden) on a
-bounded contiguous sample of the same workload.
+--impl reference times the reference's own CPU implementation on the host:
+the unmodified `mltune` package installed in baseline/_ref (the pip install of
+/root/reference, which travels to the GPU box) -- `ParamSpace.decode_indices`,
+`static_valid_mask`, `Ensemble.predict_indices` and the `lexsort` selection of
+`top_m_predicted` (tuner.py:95-131) on a bounded contiguous slice of the same
+workload, float64 numpy/OpenBLAS on every host thread. Without baseline/_ref
+the oracle port (oracle/, bit-exact with the reference on every golden
+fixture) is timed instead and the line says `kind: "port"`.
 """
 
 from __future__ import annotations
@@ -117,7 +122,48 @@ def pipe_peaks():
         out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout.strip().splitlines()
         return json.loads(out[-1])
     except Exception:
-        return {"fp32_ffma_tflops": 70.8, "mufu_ex2_gops": 4635.0, "source": "profiles/pipe_peaks_r01.json"}
+        return {"fp32_ffma2_tflops": 73.57, "mufu_rcp_gops": 4623.0,
+                "source": "profiles/r01_pipe_peaks.json (tools/pipe_peaks did not run)"}
+
+
+def reference_module():
+    """The unmodified reference package from baseline/_ref (its pip install),
+    or None. Never /root/reference: that tree does not exist on the GPU box."""
+    d = ROOT / "baseline" / "_ref"
+    if not (d / "mltune" / "__init__.py").exists():
+        return None
+    if str(d) not in sys.path:
+        sys.path.insert(0, str(d))
+    try:
+        import mltune
+        import mltune.tuner  # noqa: F401
+        return mltune
+    except Exception:
+        return None
+
+
+def _reference_workload(mt, space_name):
+    spaces = json.loads((GOLDEN / "spaces.json").read_text())
+    case = {"synthetic-1e8": "synth_k16", "stereo": "stereo_k8"}[space_name]
+    return mt.paramspace.space_from_json(spaces[space_name]), mt.model.load_model(str(GOLDEN / f"model_{case}.json"))
+
+
+def reference_slice_top_m(mt, space, ens, m, lo, hi, chunk=1 << 17):
+    """The body of the reference's top_m_predicted (tuner.py:110-130) over the
+    contiguous slice [lo, hi): its own decode_indices, static_valid_mask,
+    Ensemble.predict_indices and lexsort, chunk by chunk (_SWEEP_CHUNK)."""
+    kept_i, kept_p = [], []
+    for s0 in range(lo, hi, chunk):
+        idx = np.arange(s0, min(s0 + chunk, hi), dtype=np.int64)
+        valid = space.static_valid_mask(space.decode_indices(idx))
+        if not valid.any():
+            continue
+        idx = idx[valid]
+        kept_i.append(idx)
+        kept_p.append(ens.predict_indices(idx))
+    ind, prd = np.concatenate(kept_i), np.concatenate(kept_p)
+    order = np.lexsort((ind, prd))[:m]
+    return ind[order], prd[order]
 
 
 def _oracle_workload(space_name):
@@ -137,18 +183,29 @@ def blas_threads() -> int:
 
 
 def cpu_baseline(space_name, m, n_cfg):
-    """The reference algorithm (oracle restatement, bit-exact with `mltune` on
-    every golden fixture) on a bounded contiguous sample, host cores, float64
+    """The reference's CPU path on a bounded contiguous sample of the workload
+    (kind "reference": the baseline/_ref package itself; kind "port": the
+    oracle restatement when baseline/_ref is absent), host cores, float64
     numpy/OpenBLAS."""
-    from oracle.tuner import top_m
-    osp, oens = _oracle_workload(space_name)
-    top_m(oens, osp, m, begin=0, end=1 << 17)          # warm-up (BLAS threads, allocation)
+    mt = reference_module()
+    if mt is not None:
+        rsp, rens = _reference_workload(mt, space_name)
+        run = lambda lo, hi: reference_slice_top_m(mt, rsp, rens, m, lo, hi)   # noqa: E731
+        k, kind = len(rens.members), "reference"
+    else:
+        from oracle.tuner import top_m
+        osp, oens = _oracle_workload(space_name)
+        run = lambda lo, hi: top_m(oens, osp, m, begin=lo, end=hi)   # noqa: E731
+        k, kind = len(oens.nets), "port"
+    run(0, 1 << 17)          # warm-up (BLAS threads, allocation)
     t0 = time.perf_counter()
-    top_m(oens, osp, m, begin=0, end=n_cfg)
+    run(0, n_cfg)
     dt = time.perf_counter() - t0
     cores = blas_threads()
-    return {"value": n_cfg / dt, "unit": "configs/s", "cores": cores, "kind": "port",
-            "sample": f"contiguous slice [0, {n_cfg}) of {space_name}, k={len(oens.nets)}, top-{m}, "
+    what = "the reference package (baseline/_ref mltune: decode_indices, static_valid_mask, predict_indices, " \
+           "lexsort of top_m_predicted)" if kind == "reference" else "the oracle port of top_m_predicted"
+    return {"value": n_cfg / dt, "unit": "configs/s", "cores": cores, "kind": kind,
+            "sample": f"contiguous slice [0, {n_cfg}) of {space_name}, k={k}, top-{m}, {what}, "
                       f"float64 numpy/OpenBLAS ({cores} threads for BLAS), {dt:.1f} s",
             "seconds": dt}
 
@@ -174,24 +231,56 @@ def train_bench(space_name, with_cpu=True):
     out = {"k": k, "epochs": 500, "samples_valid": int(st["ok"].sum()), "device_wall_s": dev_s,
            "final_losses_mean": float(np.mean([m.final_epoch_loss for m in ens.members]))}
     if with_cpu:
-        from oracle.model import OTrainCfg, fold_rows, fit
+        out.update(reference_train_times(space_name, k))
+        seq = out.get("cpu_reference_s_jobs1")
+        par = out.get("cpu_reference_s_jobs_cores")
+        if seq:
+            out["speedup_vs_cpu_jobs1"] = seq / dev_s
+        if par:
+            out["speedup_vs_cpu_jobs_cores"] = par / dev_s
+    return out
+
+
+def reference_train_times(space_name, k):
+    """The reference trainer's own wall time: mltune.train_ensemble
+    with jobs=1 (members in turn) and jobs=cores (its ProcessPoolExecutor,
+    model.py:334-337), same stage-1 sample, k, and TrainConfig(seed=0).
+    Both MEASURED; the oracle port stands in only without baseline/_ref."""
+    cores = len(os.sched_getaffinity(0))
+    st = np.load(GOLDEN / f"stage1_{space_name}.npz")
+    mt = reference_module()
+    if mt is not None:
+        rsp = mt.paramspace.space_from_json(json.loads((GOLDEN / "spaces.json").read_text())[space_name])
+        M = mt.measurement
+        samples = M.SampleSet(rsp, "golden", tuple(
+            M.Sample(rsp.config_at(int(i)), M.Outcome.valid(float(t)) if ok else M.Outcome.invalid("invalid-launch"))
+            for i, ok, t in zip(st["idx"], st["ok"], st["time"])))
+        cfg = mt.model.TrainConfig(seed=0)
+        train = lambda jobs: mt.model.train_ensemble(samples, rsp, k=k, cfg=cfg, jobs=jobs)   # noqa: E731
+        kind = "reference (baseline/_ref mltune.train_ensemble)"
+    else:
+        from concurrent.futures import ProcessPoolExecutor
+
+        from oracle.model import OTrainCfg, fit, fold_rows
         from oracle.space import space_from_doc
-        osp = space_from_doc(spaces[space_name])
-        X = osp.encode(st["idx"][st["ok"]])
-        y = np.log(st["time"][st["ok"]])
-        rows = fold_rows(X.shape[0], k, 0)[0]
-        t0 = time.perf_counter()
-        fit(X[rows], y[rows], OTrainCfg(seed=0), (0, 0))
-        cpu_member = time.perf_counter() - t0
-        out["cpu_reference_s_per_member"] = cpu_member
-        out["cpu_reference_s_all_members_sequential"] = cpu_member * k
-        out["speedup_vs_sequential_cpu"] = cpu_member * k / dev_s
-        # train_ensemble(jobs=cores) runs members in separate processes (model.py:334-339):
-        # with one BLAS thread each its wall time is about ceil(k / cores) member times
-        cores = len(os.sched_getaffinity(0))
-        par = cpu_member * -(-k // cores)
-        out["cpu_reference_s_all_members_parallel_estimate"] = par
-        out["speedup_vs_parallel_cpu_estimate"] = par / dev_s
+        osp = space_from_doc(json.loads((GOLDEN / "spaces.json").read_text())[space_name])
+        X, y = osp.encode(st["idx"][st["ok"]]), np.log(st["time"][st["ok"]])
+        rows = fold_rows(X.shape[0], k, 0)
+        tasks = [(X[r], y[r], OTrainCfg(seed=0), (0, i)) for i, r in enumerate(rows)]
+
+        def train(jobs):
+            if jobs == 1:
+                return [fit(*t) for t in tasks]
+            with ProcessPoolExecutor(max_workers=min(jobs, k)) as pool:
+                return list(pool.map(fit, *zip(*tasks)))
+        kind = "port (oracle fit; ProcessPoolExecutor like model.py:334-337)"
+    out = {"cpu_reference_kind": kind, "cpu_cores": cores}
+    t0 = time.perf_counter()
+    train(1)
+    out["cpu_reference_s_jobs1"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    train(cores)
+    out["cpu_reference_s_jobs_cores"] = time.perf_counter() - t0
     return out
 
 
@@ -268,31 +357,42 @@ def seed_variance(space_name, steps=5):
 
 
 def run_reference(args, rank):
-    """The reference's CPU path on this host: every step is the reference
-    top-m sweep (tuner.py:95-131, via the oracle port) over a fresh contiguous
-    slice of `--ref-sample` configurations of the same workload."""
+    """The reference's CPU path on this host: every step is the reference's
+    top-m sweep (tuner.py:95-131: baseline/_ref mltune's own decode, rule mask,
+    predict_indices and lexsort; the oracle port without baseline/_ref) over a
+    fresh contiguous slice of `--ref-sample` configurations of the workload."""
     if rank != 0:
         return
-    from oracle.tuner import top_m
-    osp, oens = _oracle_workload(args.workload)
+    mt = reference_module()
+    if mt is not None:
+        rsp, rens = _reference_workload(mt, args.workload)
+        card, k, kind = rsp.cardinality(), len(rens.members), "reference"
+        run = lambda lo, hi: reference_slice_top_m(mt, rsp, rens, M_TOP, lo, hi)   # noqa: E731
+        what = "baseline/_ref mltune (decode_indices, static_valid_mask, Ensemble.predict_indices, lexsort)"
+    else:
+        from oracle.tuner import top_m
+        osp, oens = _oracle_workload(args.workload)
+        card, k, kind = osp.card, len(oens.nets), "port"
+        run = lambda lo, hi: top_m(oens, osp, M_TOP, begin=lo, end=hi)   # noqa: E731
+        what = "oracle port of top_m_predicted"
     n_cfg = args.ref_sample
     secs = 0.0
     for s in range(args.warmup + args.steps):
-        lo = (s * n_cfg) % max(osp.card - n_cfg, 1)
+        lo = (s * n_cfg) % max(card - n_cfg, 1)
         t0 = time.perf_counter()
-        top_m(oens, osp, M_TOP, begin=lo, end=lo + n_cfg)
+        run(lo, lo + n_cfg)
         if s >= args.warmup:
             secs += time.perf_counter() - t0
     value = n_cfg * args.steps / secs
     cores = blas_threads()
-    cb = {"value": value, "unit": "configs/s", "cores": cores, "kind": "port",
-          "sample": f"{args.steps} contiguous slices of {n_cfg} configs of {args.workload}, k={len(oens.nets)}, "
-                    f"top-{M_TOP}, float64 numpy/OpenBLAS ({cores} threads for BLAS)"}
+    cb = {"value": value, "unit": "configs/s", "cores": cores, "kind": kind,
+          "sample": f"{args.steps} contiguous slices of {n_cfg} configs of {args.workload}, k={k}, "
+                    f"top-{M_TOP}, {what}, float64 numpy/OpenBLAS ({cores} threads for BLAS)"}
     line = {"metric": METRIC, "value": value, "unit": "configs/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: bounded CPU sample of {n_cfg} configs per step",
-                       "k": len(oens.nets), "m": M_TOP},
+                       "k": k, "m": M_TOP},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -349,6 +449,9 @@ def main():
     out_n = N.C.c_int64()
     st = N.MltSweepStats()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    # the headline step rebuilds the factored tables every call (what a freshly
+    # trained ensemble costs); the resident-table step is reported beside it
+    N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_TABLE_CACHE, 0))
 
     def step():
         N.check(N.lib().mlt_plan_top_m(plan, M_TOP, lo, hi, N.ptr(out_i, N.C.c_int64), N.ptr(out_p, N.C.c_double),
@@ -387,10 +490,29 @@ def main():
     ms_step = t[0].item() / args.steps
     value = card / (ms_step / 1e3)
 
+    # ---- the same step with the plan's tables kept between calls (a resident
+    # ensemble swept repeatedly, e.g. over several slices)
+    N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_TABLE_CACHE, 1))
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for s_ in range(args.steps):
+        flush.zero_()
+        cev[s_][0].record(stream)
+        step()
+        cev[s_][1].record(stream)
+    torch.cuda.synchronize()
+    tc = torch.tensor([sum(a.elapsed_time(b) for a, b in cev) / args.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+    resident = {"ms_per_step": tc.item(), "configs_per_s": card / (tc.item() / 1e3)}
+
     # ---- the same step with exact bound-based pruning (MLT_OPT_PRUNE): reported
     # beside the headline, which evaluates every configuration
     pruned = None
     if world == 1:
+        N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_TABLE_CACHE, 0))
         N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_PRUNE, 1))
         for _ in range(args.warmup):
             flush.zero_()
@@ -403,10 +525,12 @@ def main():
             pev[s_][1].record(stream)
         torch.cuda.synchronize()
         N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_PRUNE, 0))
+        N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_TABLE_CACHE, 1))
         pms = sum(a.elapsed_time(b) for a, b in pev) / args.steps
         pruned = {"ms_per_step": pms, "configs_per_s": card / (pms / 1e3), "evaluated_frac": st.evaluated_frac,
                   "same_top200": bool(np.array_equal(np.asarray(pres[0]), np.asarray(res[0])))}
 
+    N.check(N.lib().mlt_ctx_set_option(ctx, N.MLT_OPT_TABLE_CACHE, 1))
     # ---- e2e: public API from host objects (weights H2D + results D2H every step)
     N.check(N.lib().mlt_ctx_set_profiling(ctx, 0))
     e2e_api = (lambda: D.top_m_predicted(ens, space, M_TOP)) if world > 1 else \
@@ -437,14 +561,16 @@ def main():
         ok = bool(np.array_equal(idx_res, e2e_idx))
         if "m200_i" in gold.files:
             ok = ok and bool(np.array_equal(idx_res, gold["m200_i"]))
-        peaks = pipe_peaks() if not args.no_peaks else {"fp32_ffma_tflops": 70.8, "mufu_ex2_gops": 4635.0}
+        peaks = pipe_peaks() if not args.no_peaks else {"fp32_ffma2_tflops": 73.57, "mufu_rcp_gops": 4623.0,
+                                                         "source": "profiles/r01_pipe_peaks.json"}
         n_local = hi - lo
         sweep_s = t[1].item() / 1e3
-        ffma_tflops = float(peaks.get("fp32_ffma_tflops", 70.8))
+        # the hot loop issues FFMA2/FMUL2/FADD2: its peak is the measured FFMA2 rate
+        ffma_tflops = float(peaks.get("fp32_ffma2_tflops", 73.57))
         lane_ops = k * H * {3: 8.0 / 3.0, 2: 2.5, 1: 2.0}.get(st.group, 8.0 / 3.0)   # FMA-pipe lane-ops/config
         achieved = 2.0 * lane_ops * n_local / sweep_s / 1e12
         mufu_rate = k * H / max(st.group, 1) * n_local / sweep_s   # reciprocals per second
-        mufu_peak = float(peaks.get("mufu_ex2_gops", 4635.0)) * 1e9
+        mufu_peak = float(peaks.get("mufu_rcp_gops", 4623.0)) * 1e9
         traffic = None
         tf = ROOT / "profiles" / "sweep_dram_bytes.json"
         if tf.exists():
@@ -461,7 +587,8 @@ def main():
             "clocks": clocks.result(),
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": ffma_tflops, "unit": "TFLOP/s",
                          "frac": achieved / ffma_tflops, "traffic": traffic,
-                         "peak_source": "measured FFMA rate (tools/pipe_peaks, this GPU)",
+                         "peak_source": "measured FFMA2 rate (tools/pipe_peaks on this GPU; MEASURED_PEAKS.json "
+                                        "has no FP32 figure)" if "source" not in peaks else peaks["source"],
                          "mufu_frac": mufu_rate / mufu_peak,
                          "sweep_ms_per_launch": t[1].item(),
                          "naive_sec8d_tflops": flops_per_config(k, d) * n_local / sweep_s / 1e12},
@@ -469,6 +596,7 @@ def main():
             "guard_band": {"delta": st.delta, "group": st.group, "split_inner_params": st.split},
             "parity_top200_vs_reference": ok,
             "pruned_sweep": pruned,
+            "resident_tables_step": resident,
             "e2e": {"value": e2e_value, "unit": "configs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "h2d_from": "pinned staging buffer (library)",
                     "ms_per_step_median": 1e3 * statistics.median(e2e_times),

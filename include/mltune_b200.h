@@ -141,6 +141,10 @@ MLT_API int64_t mlt_ctx_launches(mlt_ctx* ctx);
 /*   MLT_OPT_CHUNK     configurations per sweep chunk (default 2^27): longer slices are swept
  *                     chunk by chunk and the per-chunk top-m merged (bounded memory).   */
 #define MLT_OPT_CHUNK 5
+/*   MLT_OPT_TABLE_CACHE 1 (default) = a plan keeps its factored sweep tables between calls
+ *                     with the same slice shape; 0 = rebuild them on every call (what a
+ *                     fresh ensemble costs; bench.py times the headline step this way).  */
+#define MLT_OPT_TABLE_CACHE 6
 MLT_API int mlt_ctx_set_option(mlt_ctx* ctx, int key, int64_t value);
 
 /* A1: values[n][P] = decode(idx[n]).                 paramspace.py:184-193 */

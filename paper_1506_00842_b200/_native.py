@@ -11,6 +11,7 @@ library or the device is missing, calls raise NativeUnavailableError.
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import threading
@@ -23,7 +24,7 @@ from . import errors
 _LIB_PATH = Path(os.environ.get("MLTUNE_B200_LIB", Path(__file__).resolve().parent / "libmltune_b200.so"))
 
 MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
-MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE, MLT_OPT_CHUNK = 1, 2, 3, 4, 5
+MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE, MLT_OPT_CHUNK, MLT_OPT_TABLE_CACHE = 1, 2, 3, 4, 5, 6
 RULE_KIND = {"max-product": 0, "max-weighted-sum": 1, "forbidden-combination": 2}
 
 _i32p = C.POINTER(C.c_int32)
@@ -216,6 +217,23 @@ def extra_ctx(device: int, slot: int) -> C.c_void_p:
             check(lib().mlt_ctx_create(int(device), C.byref(h)), "mlt_ctx_create")
             _ctxs[key] = h
     return _ctxs[key]
+
+
+def shutdown() -> None:
+    """Destroy every context (workspaces, pinned staging, streams). Registered
+    with atexit so a process ends with the library's device memory released
+    (compute-sanitizer's leak check sees no leftovers); ctx() after this
+    creates fresh contexts."""
+    with _ctx_lock:
+        items = list(_ctxs.items())
+        _ctxs.clear()
+    if _lib is None:
+        return
+    for _, h in items:
+        _lib.mlt_ctx_destroy(h)
+
+
+atexit.register(shutdown)
 
 
 def ptr(a: np.ndarray, ctype):

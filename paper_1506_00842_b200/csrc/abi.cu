@@ -63,6 +63,7 @@ struct mlt_ctx {
   bool prof = false;
   int64_t launches = 0;
   int opt_path = -1, opt_group = -1, opt_prune = 0;
+  int opt_table_cache = 1;            // MLT_OPT_TABLE_CACHE
   int64_t chunk = int64_t(1) << 27;   // configurations per sweep chunk (MLT_OPT_CHUNK)
   int64_t cand_cap = 1 << 20;
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
@@ -513,14 +514,17 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
       log2dmin = std::min(log2dmin, -lw / std::log(2.0));
     }
   }
+  // Units per shared reciprocal: the largest G <= the requested maximum
+  // (MLT_OPT_GROUP, default kDefaultGroup) whose G-fold products of d' stay
+  // inside the normal fp32 range and that divides the unit count.
+  const int gmax = (p->ctx->opt_group >= 1 && p->ctx->opt_group <= 4) ? p->ctx->opt_group : kDefaultGroup;
   int G = 0;
-  for (int g = 3; g >= 1; --g) {
-    if (g * std::max(log2dmax, 0.0) < 124.0 && g * std::min(log2dmin, 0.0) > -124.0) {
+  for (int g = gmax; g >= 1; --g) {
+    if (KH % g == 0 && g * std::max(log2dmax, 0.0) < 124.0 && g * std::min(log2dmin, 0.0) > -124.0) {
       G = g;
       break;
     }
   }
-  if (p->ctx->opt_group >= 1 && p->ctx->opt_group <= 3) G = std::min(G, p->ctx->opt_group);
   if (G == 0) {
     b.why = "reciprocal products would overflow fp32";
     return MLT_OK;
@@ -541,7 +545,7 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   //  * the running accumulator is rounded once per group, each time by at most
   //    u * |partial sum| <= u * (prefix sum of |w'| up to that group);
   //  * + cst (rounded) and the final add.
-  const double cg = G == 3 ? 30.0 : (G == 2 ? 16.0 : 8.0);
+  const double cg = G == 4 ? 40.0 : (G == 3 ? 30.0 : (G == 2 ? 16.0 : 8.0));
   double prefix = 0.0, acc_bound = 0.0;
   for (int q = 0; q < KH; q += G) {
     for (int x = 0; x < G; ++x) prefix += wpv[q + x] != 0.0 ? std::fabs(wpv[q + x]) : 1.0;
@@ -770,6 +774,10 @@ int mlt_ctx_destroy(mlt_ctx* c) {
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->own) cudaStreamDestroy(c->own);
+  // stream-ordered frees (plans, tables, trainer buffers) return memory to the
+  // device's default pool; hand the pool's idle memory back to the driver
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, c->dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   delete c;
   return MLT_OK;
 }
@@ -799,6 +807,7 @@ int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
     case MLT_OPT_CAND_CAP: c->cand_cap = value < 0 ? (1 << 20) : std::max<int64_t>(value, 1); return MLT_OK;
     case MLT_OPT_PRUNE: c->opt_prune = value == 1 ? 1 : 0; return MLT_OK;
     case MLT_OPT_CHUNK: c->chunk = value < 0 ? (int64_t(1) << 27) : std::max<int64_t>(value, 4096); return MLT_OK;
+    case MLT_OPT_TABLE_CACHE: c->opt_table_cache = value == 0 ? 0 : 1; return MLT_OK;
     default: return fail(MLT_EINVAL, "unknown option %d", key);
   }
 }
@@ -1035,7 +1044,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     float *ea, *ebp, *cval;
     int64_t* cidx;
     uint32_t* gs;
-    const int ebw = B.G == 3 ? ebw_of(3) : (B.G == 2 ? ebw_of(2) : ebw_of(1));
+    const int ebw = ebw_of(B.G);
     const size_t n_ea = (size_t)n_ob * KH * kOB, n_ebp = (size_t)n_ib * (KH / B.G) * kThreads * ebw * 4;
     const bool prune = c->opt_prune == 1;
     const int ngroups = KH / B.G;
@@ -1059,7 +1068,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     }
     const size_t n_remlo = prune ? (size_t)n_ob * kOB * n_ib * ck.n : 0;
     const int64_t key[5] = {B.split, B.G, o_lo, n_ob, prune ? 1 : 0};
-    const bool tables_cached = std::equal(key, key + 5, p->t_key);
+    const bool tables_cached = c->opt_table_cache && std::equal(key, key + 5, p->t_key);
     if (!tables_cached) {
       if (p->t_remlo_cap < n_remlo) {
         pool_free(c, p->t_remlo);
@@ -1111,12 +1120,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.ea = ea;
     ta.ebp = ebp;
     uint32_t* hs = static_cast<uint32_t*>(c->pinned);
+    // gs[0] theta key, [1] candidate count, [2..3] band-stage counters, [4..5]
+    // pruning work (64-bit), [6] pruning: next work item, [7] unused: all 8 set
+    // so the end-of-step 32-byte read-back never copies uninitialised memory
+    std::fill(hs, hs + 8, 0u);
     hs[0] = 0xFF800000u;   // fkey(+inf)
-    hs[1] = 0u;
-    hs[4] = hs[5] = 0u;    // pruning work counter (64-bit at gs + 4)
-    hs[6] = 0u;            // pruning: next work item
-    CU(cudaMemcpyAsync(gs, hs, 8, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(gs + 4, hs + 4, 12, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(gs, hs, 32, cudaMemcpyHostToDevice, c->stream));
     if (!tables_cached) {
       // two-level split of each side: lo = trailing parameters with <= 64 combinations
       auto lo_split = [&](int p_lo, int p_hi, int* sa, int64_t* nlo) {
@@ -1157,7 +1166,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       ta.i_nhi = nhi_i;
       k_table_outer<<<grid_for(c, (int64_t)n_ob * KH * kOB, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
-      void (*tin)(TableArgs) = B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
+      void (*tin)(TableArgs) = B.G == 4 ? k_table_inner<4>
+                               : B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
       tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads * 4 * ebw, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
       if (prune) {
@@ -1236,8 +1246,11 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     sa.sp = p->ds;
     const size_t smem = sweep_smem(p->he.k);
     if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);
-    void (*kern)(SweepArgs) = prune ? (B.G == 3 ? k_sweep<3, true> : (B.G == 2 ? k_sweep<2, true> : k_sweep<1, true>))
-                                    : (B.G == 3 ? k_sweep<3, false> : (B.G == 2 ? k_sweep<2, false> : k_sweep<1, false>));
+    void (*kern)(SweepArgs) =
+        prune ? (B.G == 4 ? k_sweep<4, true>
+                 : B.G == 3 ? k_sweep<3, true> : (B.G == 2 ? k_sweep<2, true> : k_sweep<1, true>))
+              : (B.G == 4 ? k_sweep<4, false>
+                 : B.G == 3 ? k_sweep<3, false> : (B.G == 2 ? k_sweep<2, false> : k_sweep<1, false>));
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));

@@ -73,6 +73,10 @@ constexpr int kOB = MLT_OB;         // outer configurations per work item (per t
 
 // float4s per thread per group in the thread-contiguous exp(-B')/w' layout
 __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
+#ifndef MLT_DEFAULT_GROUP
+#define MLT_DEFAULT_GROUP 3
+#endif
+constexpr int kDefaultGroup = MLT_DEFAULT_GROUP;   // units per shared reciprocal unless MLT_OPT_GROUP says otherwise
 constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
 constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
 constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path

@@ -301,6 +301,17 @@ __device__ __forceinline__ void combine<3>(const f2 (&d)[3], f2& num, f2& den) {
   den = fmul2(p, d[2]);
 }
 
+template <>
+__device__ __forceinline__ void combine<4>(const f2 (&d)[4], f2& num, f2& den) {
+  // 1/d0 + 1/d1 + 1/d2 + 1/d3 = (s01*p23 + s23*p01) / (p01*p23)
+  const f2 s01 = fadd2(d[0], d[1]);
+  const f2 p01 = fmul2(d[0], d[1]);
+  const f2 s23 = fadd2(d[2], d[3]);
+  const f2 p23 = fmul2(d[2], d[3]);
+  num = ffma2(s23, p01, fmul2(s01, p23));
+  den = fmul2(p01, p23);
+}
+
 // Per-thread factors of one group of G units: exp(-B')/w' for the thread's
 // kInner inners, stored thread-contiguously (k_table_inner layout) so they
 // arrive in ebw_of(G) 16-byte loads; 1/w' is a shared-memory broadcast.
@@ -369,14 +380,19 @@ __device__ __forceinline__ void gappend(const SweepArgs& a, int64_t idx, float v
 __device__ __forceinline__ void lower_threshold(const SweepArgs& a, uint32_t* s_th, uint32_t nth_key) {
   // new threshold = (m-th best) + band, rounded up so it stays an upper bound
   const uint32_t nk = fkey(__fadd_ru(fkey_inv(nth_key), a.band));
-  if (threadIdx.x == 0 && nk < *s_th) {
-    *s_th = nk;
-    atomicMin(a.g_theta, nk);
+  if (threadIdx.x == 0) {
+    // only thread 0 touches s_th here (volatile: the compiler may not widen
+    // or hoist this load into the other threads, where it would race with
+    // the store below -- compute-sanitizer racecheck)
+    if (nk < *reinterpret_cast<volatile uint32_t*>(s_th)) {
+      *s_th = nk;
+      atomicMin(a.g_theta, nk);
+    }
   }
 }
 
 // the per-thread factor ring: [stage][w][thread] float4 (conflict-free LDS.128)
-__host__ __device__ constexpr size_t eb_ring_bytes() { return (size_t)kEbStages * ebw_of(3) * kThreads * 16; }
+__host__ __device__ constexpr size_t eb_ring_bytes() { return (size_t)kEbStages * ebw_of(4) * kThreads * 16; }
 
 // byte offset of the second exp(-A') tile buffer (the next item's tile lands
 // there by cp.async while the current item computes)
@@ -783,11 +799,14 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
 template __global__ void k_table_inner<1>(TableArgs t);
 template __global__ void k_table_inner<2>(TableArgs t);
 template __global__ void k_table_inner<3>(TableArgs t);
+template __global__ void k_table_inner<4>(TableArgs t);
 template __global__ void k_sweep<1, false>(SweepArgs a);
 template __global__ void k_sweep<2, false>(SweepArgs a);
 template __global__ void k_sweep<3, false>(SweepArgs a);
+template __global__ void k_sweep<4, false>(SweepArgs a);
 template __global__ void k_sweep<1, true>(SweepArgs a);
 template __global__ void k_sweep<2, true>(SweepArgs a);
 template __global__ void k_sweep<3, true>(SweepArgs a);
+template __global__ void k_sweep<4, true>(SweepArgs a);
 
 }  // namespace mlt

@@ -250,7 +250,7 @@ def test_top_m_with_every_rule_kind(m):
         np.testing.assert_allclose(pred, g[f"m{m}_p"], rtol=PRED_RTOL)
 
 
-@pytest.mark.parametrize("group", [1, 2, 3])
+@pytest.mark.parametrize("group", [1, 2, 3, 4])
 def test_every_reciprocal_grouping_is_exact(group):
     from paper_1506_00842_b200.tuner import top_m_arrays
     set_opt(_lib().MLT_OPT_GROUP, group)

@@ -76,12 +76,17 @@ def band_overflow_exact():
 
 
 def sweep_groups():
-    """Reciprocal groupings G = 1, 2 of the sweep kernel."""
+    """Reciprocal groupings G = 1, 2, 4 of the sweep kernel (k = 11 gives 330
+    units, not a multiple of 4: the G = 4 request falls back to 3; the k = 8
+    stereo ensemble has 240 units and runs G = 4)."""
     out = {}
-    for g in (1, 2):
+    for g in (1, 2, 4):
         _reset()
         _opt(N.MLT_OPT_GROUP, g)
         out[f"g{g}"] = _check_top("raycast_k11", "raycasting", 20, 0, 1 << 17)["group"]
+    _reset()
+    _opt(N.MLT_OPT_GROUP, 4)
+    out["g4_stereo"] = _check_top("stereo_k8", "stereo", 50, 0, 1 << 18)["group"]
     _reset()
     return out
 
@@ -156,8 +161,11 @@ def stereo():
     left, right = r.input()
     gold = stereo_sad(left, right, 16, 4)
     n = 0
-    for cfg in [(16, 8, 1, 1, 0, 0, 0, 0, 1, 1, 1), (16, 8, 1, 1, 0, 0, 1, 1, 4, 4, 1), (8, 8, 2, 2, 1, 1, 0, 0, 2, 1, 3),
-                (32, 4, 1, 1, 0, 0, 1, 1, 1, 4, 9)]:
+    # (wg_x, wg_y, ppt_x, ppt_y, img_left, img_right, local_left, local_right,
+    #  unroll_disparity, unroll_diff_x, unroll_diff_y): global, textures, smem
+    # tiles, the packed-row path (both tiles local, diff_x = 4)
+    for cfg in [(16, 8, 1, 1, 0, 0, 0, 0, 1, 1, 1), (16, 8, 1, 1, 0, 0, 1, 1, 4, 4, 1), (8, 8, 2, 2, 1, 1, 0, 0, 2, 1, 2),
+                (32, 4, 1, 1, 0, 0, 1, 1, 1, 4, 4), (16, 8, 2, 1, 0, 1, 1, 0, 8, 2, 4)]:
         _, ok = r.run(cfg, 1)
         if ok:
             assert np.array_equal(r.output(), gold), cfg

@@ -17,6 +17,8 @@ sp = space_from_json(json.loads((G / "spaces.json").read_text())[name])
 ens = model_from_json(json.loads((G / f"model_{case}.json").read_text()))
 c = N.ctx(0)
 N.check(N.lib().mlt_ctx_set_profiling(c, 1))
+if os.environ.get("MLT_GROUP"):
+    N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_GROUP, int(os.environ["MLT_GROUP"])))
 if os.environ.get("MLT_PRUNE") == "1":
     N.check(N.lib().mlt_ctx_set_option(c, 4, 1))
 ps, pe = N.packed(sp, "space"), N.packed(ens, "ensemble")
