@@ -145,6 +145,10 @@ MLT_API int64_t mlt_ctx_launches(mlt_ctx* ctx);
  *                     with the same slice shape; 0 = rebuild them on every call (what a
  *                     fresh ensemble costs; bench.py times the headline step this way).  */
 #define MLT_OPT_TABLE_CACHE 6
+/*   MLT_OPT_HALF_ITEMS  1 = sweep with two CTAs per SM, each owning half a work item;
+ *                     0 = one CTA per SM owning whole items; -1 (default) = half items
+ *                     when the slice is shallower than a few waves of whole items.    */
+#define MLT_OPT_HALF_ITEMS 7
 MLT_API int mlt_ctx_set_option(mlt_ctx* ctx, int key, int64_t value);
 
 /* A1: values[n][P] = decode(idx[n]).                 paramspace.py:184-193 */
@@ -195,6 +199,25 @@ MLT_API int mlt_plan_create(mlt_ctx* ctx, const mlt_space* space, const mlt_ense
 MLT_API int mlt_plan_top_m(mlt_plan* plan, int64_t m, int64_t begin, int64_t end,
                    int64_t* out_idx, double* out_pred, int64_t* out_n, mlt_sweep_stats* stats);
 MLT_API int mlt_plan_destroy(mlt_plan* plan);
+
+/* Device-resident step for the multi-GPU path: the whole
+ * top-m of [begin, end) is enqueued on the context's stream and written to
+ * the DEVICE record rec[2m+1] (int64): rec[0..m) indices (-1 = padding),
+ * rec[m..2m) the fp64 bit patterns of the predictions (+inf = padding),
+ * rec[2m] a status word (0 = exact result; 1 = the guard band overflowed,
+ * 2 = too many survivors for the one-CTA sort: redo this shard with
+ * mlt_plan_top_m). No host wait on the fast path, so an NCCL all-gather of
+ * the records can be enqueued right behind it; where only the exact fp64
+ * path applies (m > 1024, tiny slices) the call runs it synchronously and
+ * uploads the record. tuner.py:95-131 over one shard. */
+MLT_API int mlt_plan_top_m_record(mlt_plan* plan, int64_t m, int64_t begin, int64_t end, int64_t* dev_rec);
+
+/* Merge n_rec gathered records (n_rec x (2m+1) int64, DEVICE memory, layout
+ * of mlt_plan_top_m_record) into the global top-m by (prediction, index):
+ * the final lexsort of tuner.py:128-131. *out_status = OR of the records'
+ * status words (nonzero: some shard must be redone). One host wait. */
+MLT_API int mlt_merge_records(mlt_ctx* ctx, const int64_t* dev_recs, int64_t n_rec, int64_t m,
+                      int64_t* out_idx, double* out_pred, int64_t* out_n, int64_t* out_status);
 
 /* Merge per-shard top-m lists (e.g. after an all-gather across GPUs) into the
  * global top-m by (prediction, index). Entries with idx < 0 are padding.

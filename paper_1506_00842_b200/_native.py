@@ -24,7 +24,8 @@ from . import errors
 _LIB_PATH = Path(os.environ.get("MLTUNE_B200_LIB", Path(__file__).resolve().parent / "libmltune_b200.so"))
 
 MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
-MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE, MLT_OPT_CHUNK, MLT_OPT_TABLE_CACHE = 1, 2, 3, 4, 5, 6
+(MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE, MLT_OPT_CHUNK, MLT_OPT_TABLE_CACHE,
+ MLT_OPT_HALF_ITEMS) = 1, 2, 3, 4, 5, 6, 7
 RULE_KIND = {"max-product": 0, "max-weighted-sum": 1, "forbidden-combination": 2}
 
 _i32p = C.POINTER(C.c_int32)
@@ -94,6 +95,8 @@ _SIGNATURES = [
                                  C.POINTER(MltSweepStats)]),
     ("mlt_plan_destroy", C.c_int, [C.c_void_p]),
     ("mlt_merge_top_m", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _i64p, _f64p, _i64p]),
+    ("mlt_plan_top_m_record", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
+    ("mlt_merge_records", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _i64p, _f64p, _i64p, _i64p]),
     ("mlt_train_members", C.c_int, [C.c_void_p, C.POINTER(MltTrainDesc), _f64p, _f64p, _f64p, _f64p, _f64p,
                                      _f64p, _i32p]),
     ("mlt_format_predictions", C.c_int, [_i64p, _f64p, C.c_int64, C.c_char_p, C.c_int64, _i64p, C.c_int32]),
@@ -219,11 +222,85 @@ def extra_ctx(device: int, slot: int) -> C.c_void_p:
     return _ctxs[key]
 
 
+class Plan:
+    """A resident mlt_plan of one (space, ensemble) on one device: the
+    descriptors are uploaded and the factored tables built once, and kept
+    while the plan lives (the reference's spaces and ensembles are immutable,
+    model.py:262-301, so identity is a sound cache key)."""
+
+    def __init__(self, space, ensemble, device):
+        self.device = int(device)
+        self.ctx = ctx(self.device)
+        self.ps, self.pe = packed(space, "space"), packed(ensemble, "ensemble")
+        self.h = C.c_void_p()
+        check(lib().mlt_plan_create(self.ctx, C.byref(self.ps.c), C.byref(self.pe.c), C.byref(self.h)),
+              "mlt_plan_create")
+
+    def destroy(self):
+        if self.h:
+            if _lib is not None and _ctxs.get(self.device) is not None:
+                _lib.mlt_plan_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+_plan_cache: dict[tuple, tuple] = {}
+_PLAN_CACHE_MAX = 8
+
+
+def plan(space, ensemble, device=None) -> Plan:
+    """The cached resident plan of (space, ensemble) on `device` (LRU of
+    _PLAN_CACHE_MAX plans; the cache pins both objects so ids stay unique)."""
+    dev = default_device() if device is None else int(device)
+    key = (dev, id(space), id(ensemble))
+    with _ctx_lock:
+        hit = _plan_cache.pop(key, None)
+        if hit is not None and hit[0] is space and hit[1] is ensemble:
+            _plan_cache[key] = hit                      # most recently used last
+            return hit[2]
+    p = Plan(space, ensemble, dev)
+    with _ctx_lock:
+        _plan_cache[key] = (space, ensemble, p)
+        while len(_plan_cache) > _PLAN_CACHE_MAX:
+            old = _plan_cache.pop(next(iter(_plan_cache)))
+            old[2].destroy()
+    return p
+
+
+def clear_plans() -> None:
+    with _ctx_lock:
+        items = list(_plan_cache.values())
+        _plan_cache.clear()
+    for _, _, p in items:
+        p.destroy()
+
+
+class on_stream:
+    """Run a context's work on a CUDA stream (a torch stream's handle) for the
+    duration of a `with` block, so device results order against collectives
+    and kernels the caller enqueues on that stream; the previous stream is
+    restored afterwards."""
+    _current: dict[int, int] = {}
+
+    def __init__(self, device: int, stream_handle: int):
+        self.device, self.handle = int(device), int(stream_handle)
+
+    def __enter__(self):
+        self.prev = on_stream._current.get(self.device, 0)
+        check(lib().mlt_ctx_set_stream(ctx(self.device), C.c_void_p(self.handle or None)), "mlt_ctx_set_stream")
+        on_stream._current[self.device] = self.handle
+        return self
+
+    def __exit__(self, *exc):
+        lib().mlt_ctx_set_stream(ctx(self.device), C.c_void_p(self.prev or None))
+        on_stream._current[self.device] = self.prev
+
+
 def shutdown() -> None:
     """Destroy every context (workspaces, pinned staging, streams). Registered
     with atexit so a process ends with the library's device memory released
     (compute-sanitizer's leak check sees no leftovers); ctx() after this
     creates fresh contexts."""
+    clear_plans()
     with _ctx_lock:
         items = list(_ctxs.items())
         _ctxs.clear()

@@ -64,6 +64,7 @@ struct mlt_ctx {
   int64_t launches = 0;
   int opt_path = -1, opt_group = -1, opt_prune = 0;
   int opt_table_cache = 1;            // MLT_OPT_TABLE_CACHE
+  int opt_half_items = -1;            // MLT_OPT_HALF_ITEMS (-1 = by slice depth)
   int64_t chunk = int64_t(1) << 27;   // configurations per sweep chunk (MLT_OPT_CHUNK)
   int64_t cand_cap = 1 << 20;
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
@@ -373,6 +374,37 @@ __global__ void k_merge_prep(const int64_t* idx, const double* pred, int64_t n, 
   }
 }
 
+// One shard's top-m as an all-gather record (mlt_plan_top_m_record): gs = the
+// step's counters (gs[1] candidates, gs[3] / gs[4] k_sort_small's status / take).
+__global__ void k_pack_record(const double* tp, const int64_t* ti, const uint32_t* gs, uint32_t cap, int m,
+                              int64_t* rec) {
+  const uint32_t count = gs[1], big = gs[3], take = gs[4];
+  const int64_t status = count > cap ? 1 : (big ? 2 : 0);
+  const int tk = status ? 0 : (int)min(take, (uint32_t)m);
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    const bool ok = t < tk && ti[t] != INT64_MAX && ti[t] >= 0;
+    rec[t] = ok ? ti[t] : -1;
+    rec[m + t] = ok ? __double_as_longlong(tp[t]) : 0x7ff0000000000000ll;
+  }
+  if (threadIdx.x == 0) rec[2 * m] = status;
+}
+
+// Gathered records -> (index, prediction) pairs for the merge sort; padding
+// becomes (INT64_MAX, +inf); the status words are OR-ed into *status.
+__global__ void k_merge_rec_prep(const int64_t* recs, int64_t n_rec, int m, int64_t* io, double* po,
+                                 unsigned long long* status) {
+  const int64_t n = n_rec * m, stride = 2 * (int64_t)m + 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / m, j = t - r * m;
+    const int64_t* rec = recs + r * stride;
+    const int64_t i = rec[j];
+    const bool ok = i >= 0 && i != INT64_MAX;
+    io[t] = ok ? i : INT64_MAX;
+    po[t] = ok ? __longlong_as_double(rec[m + j]) : __longlong_as_double(0x7ff0000000000000ll);
+    if (j == 0 && rec[2 * m] != 0) atomicOr(status, (unsigned long long)rec[2 * m]);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -563,7 +595,10 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
 }
 
 int get_setup(mlt_plan* p, int split, BandSetup** out) {
-  auto it = p->setups.find(split);
+  // keyed by the split and the requested reciprocal grouping (MLT_OPT_GROUP
+  // may change between calls on a resident plan)
+  const int key = split | (std::max(p->ctx->opt_group, 0) << 8);
+  auto it = p->setups.find(key);
   if (it == p->setups.end()) {
     BandSetup b;
     const int rc = band_setup(p, split, b);
@@ -572,7 +607,7 @@ int get_setup(mlt_plan* p, int split, BandSetup** out) {
       pool_free(p->ctx, b.d_u);
       return rc;
     }
-    it = p->setups.emplace(split, b).first;
+    it = p->setups.emplace(key, b).first;
   }
   *out = &it->second;
   return MLT_OK;
@@ -808,6 +843,7 @@ int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
     case MLT_OPT_PRUNE: c->opt_prune = value == 1 ? 1 : 0; return MLT_OK;
     case MLT_OPT_CHUNK: c->chunk = value < 0 ? (int64_t(1) << 27) : std::max<int64_t>(value, 4096); return MLT_OK;
     case MLT_OPT_TABLE_CACHE: c->opt_table_cache = value == 0 ? 0 : 1; return MLT_OK;
+    case MLT_OPT_HALF_ITEMS: c->opt_half_items = value < 0 ? -1 : (value ? 1 : 0); return MLT_OK;
     default: return fail(MLT_EINVAL, "unknown option %d", key);
   }
 }
@@ -995,9 +1031,13 @@ int mlt_plan_destroy(mlt_plan* p) {
   return MLT_OK;
 }
 
+// d_rec != nullptr: the device-record variant (mlt_plan_top_m_record): the
+// band path is only enqueued (its result packed into d_rec, no host wait) and
+// the function returns with *out_n = -1; callers fall back to the host-output
+// path when the band path does not apply.
 static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, const int64_t* idx_list,
                            int64_t n_list, int64_t* out_idx, double* out_pred, int64_t* out_n,
-                           mlt_sweep_stats* st) {
+                           mlt_sweep_stats* st, int64_t* d_rec = nullptr) {
   mlt_ctx* c = p->ctx;
   if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
   if (!out_idx || !out_pred || !out_n) return fail(MLT_EINVAL, "output pointers are NULL");
@@ -1045,7 +1085,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     int64_t* cidx;
     uint32_t* gs;
     const int ebw = ebw_of(B.G);
-    const size_t n_ea = (size_t)n_ob * KH * kOB, n_ebp = (size_t)n_ib * (KH / B.G) * kThreads * ebw * 4;
+    const size_t n_ea = (size_t)n_ob * KH * kOB, n_ebp = ((size_t)n_ib * (KH / B.G) + 2) * kThreads * ebw * 4;   // + 2 groups
+                                                                             // of padding (the sweep's prefetch)
     const bool prune = c->opt_prune == 1;
     const int ngroups = KH / B.G;
     CkList ck;
@@ -1123,9 +1164,10 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     // gs[0] theta key, [1] candidate count, [2..3] band-stage counters, [4..5]
     // pruning work (64-bit), [6] pruning: next work item, [7] unused: all 8 set
     // so the end-of-step 32-byte read-back never copies uninitialised memory
-    std::fill(hs, hs + 8, 0u);
-    hs[0] = 0xFF800000u;   // fkey(+inf)
-    CU(cudaMemcpyAsync(gs, hs, 32, cudaMemcpyHostToDevice, c->stream));
+    {
+      uint32_t init[8] = {0xFF800000u, 0, 0, 0, 0, 0, 0, 0};   // [0] = fkey(+inf)
+      TRY(upload_pinned(c, gs, init, sizeof init));   // the ring: safe with no host wait behind it
+    }
     if (!tables_cached) {
       // two-level split of each side: lo = trailing parameters with <= 64 combinations
       auto lo_split = [&](int p_lo, int p_hi, int* sa, int64_t* nlo) {
@@ -1244,29 +1286,45 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     sa.g_work = reinterpret_cast<unsigned long long*>(gs + 4);
     sa.g_next = reinterpret_cast<int*>(gs + 6);
     sa.sp = p->ds;
-    const size_t smem = sweep_smem(p->he.k);
+    const bool big = m > kMaxTopMSmall;   // the instance with kSBBig candidate slots per CTA
+    const size_t smem = sweep_smem(p->he.k, big ? kSBBig : kSB);
     if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);
-    void (*kern)(SweepArgs) =
-        prune ? (B.G == 4 ? k_sweep<4, true>
-                 : B.G == 3 ? k_sweep<3, true> : (B.G == 2 ? k_sweep<2, true> : k_sweep<1, true>))
-              : (B.G == 4 ? k_sweep<4, false>
-                 : B.G == 3 ? k_sweep<3, false> : (B.G == 2 ? k_sweep<2, false> : k_sweep<1, false>));
+    using KF = void (*)(SweepArgs);
+#define MLT_KROW(SBV, PR, NTV) \
+  { k_sweep<1, PR, SBV, NTV>, k_sweep<2, PR, SBV, NTV>, k_sweep<3, PR, SBV, NTV>, k_sweep<4, PR, SBV, NTV> }
+    static const KF kerns[2][2][2][4] = {
+        {{MLT_KROW(kSB, false, kThreads), MLT_KROW(kSB, true, kThreads)},
+         {MLT_KROW(kSBBig, false, kThreads), MLT_KROW(kSBBig, true, kThreads)}},
+        {{MLT_KROW(kSB, false, kThreads / 2), MLT_KROW(kSB, true, kThreads / 2)},
+         {MLT_KROW(kSBBig, false, kThreads / 2), MLT_KROW(kSBBig, true, kThreads / 2)}}};
+#undef MLT_KROW
+    // Half-item CTAs (two per SM) when the slice is only a few waves of whole
+    // items deep: the last wave's stragglers then share their SM with nobody
+    // (1/8 of the 10^8 space, 5.2 waves: 0.73 -> 0.67 ms; whole-item CTAs stay
+    // ~2 % faster on deep slices). MLT_OPT_HALF_ITEMS forces either.
+    const int64_t whole_items = (int64_t)n_ob * n_ib;
+    const bool halves = c->opt_half_items >= 0 ? c->opt_half_items == 1
+                                               : whole_items < (int64_t)kHalfItemWaves * c->sms;
+    const int nt = halves ? kThreads / 2 : kThreads;
+    KF kern = kerns[halves ? 1 : 0][big ? 1 : 0][prune ? 1 : 0][B.G - 1];
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem));
     nb = std::max(nb, 1);
-    const int64_t items = (int64_t)n_ob * n_ib;
+    const int64_t items = whole_items * (kThreads / nt);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nb * c->sms));
     if (c->prof) CU(cudaEventRecord(c->ev[1], c->stream));
-    kern<<<grid, kThreads, smem, c->stream>>>(sa);
+    kern<<<grid, nt, smem, c->stream>>>(sa);
     TRY(check_launch(c));
     if (c->prof) CU(cudaEventRecord(c->ev[2], c->stream));
     // Snapshot the sweep's counters (the band stage reuses gs[2..4]) and launch
     // the band stage right behind the sweep, without a host round trip: its
     // buffers are sized for the candidate capacity and its kernels read the
     // candidate count on the device. One host wait at the end of the step.
-    CU(cudaMemcpyAsync(hs + 8, gs, 8, cudaMemcpyDeviceToHost, c->stream));            // theta, count
-    if (prune) CU(cudaMemcpyAsync(hs + 10, gs + 4, 8, cudaMemcpyDeviceToHost, c->stream));   // work
+    if (!d_rec) {
+      CU(cudaMemcpyAsync(hs + 8, gs, 8, cudaMemcpyDeviceToHost, c->stream));            // theta, count
+      if (prune) CU(cudaMemcpyAsync(hs + 10, gs + 4, 8, cudaMemcpyDeviceToHost, c->stream));   // work
+    }
     const uint32_t cap = (uint32_t)std::min<int64_t>(c->cand_cap, UINT32_MAX);
     const size_t cap1 = std::max<size_t>(cap, 1);
     double *pa, *pb, *tp;
@@ -1295,6 +1353,16 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
     k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3);
     TRY(check_launch(c));
+    if (d_rec) {   // device record: pack and return without waiting
+      k_pack_record<<<1, 256, 0, c->stream>>>(tp, ti, gs, cap, (int)m, d_rec);
+      TRY(check_launch(c));
+      local.group = B.G;
+      local.delta = B.delta;
+      local.launches = (int32_t)(c->launches - l0);
+      if (st) *st = local;
+      *out_n = -1;
+      return MLT_OK;
+    }
     if (c->res_cap < (size_t)m * 16) {
       if (c->res_pin) CU(cudaFreeHost(c->res_pin));
       c->res_pin = nullptr;
@@ -1430,6 +1498,83 @@ int mlt_plan_top_m(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* 
   if (!p) return fail(MLT_EINVAL, "plan is NULL");
   CTX_GUARD(p->ctx);
   return plan_top_m_range(p, m, begin, end, out_idx, out_pred, out_n, st);
+}
+
+int mlt_plan_top_m_record(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* d_rec) {
+  if (!p) return fail(MLT_EINVAL, "plan is NULL");
+  if (!d_rec) return fail(MLT_EINVAL, "record pointer is NULL");
+  CTX_GUARD(p->ctx);
+  if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
+  std::vector<int64_t> hi(m);
+  std::vector<double> hp(m);
+  int64_t n = 0;
+  if (end - begin <= p->ctx->chunk) {
+    TRY(plan_top_m_impl(p, m, begin, end, nullptr, 0, hi.data(), hp.data(), &n, nullptr, d_rec));
+    if (n < 0) return MLT_OK;   // enqueued on the device
+  } else {
+    TRY(plan_top_m_range(p, m, begin, end, hi.data(), hp.data(), &n, nullptr));
+  }
+  // host-side result (exact path, or a chunked slice): upload it as the record
+  std::vector<int64_t> rec(2 * m + 1);
+  for (int64_t t = 0; t < m; ++t) {
+    const bool ok = t < n;
+    rec[t] = ok ? hi[t] : -1;
+    double v = ok ? hp[t] : INFINITY;
+    std::memcpy(&rec[m + t], &v, 8);
+  }
+  rec[2 * m] = 0;
+  return upload_pinned(p->ctx, d_rec, rec.data(), rec.size() * 8);
+}
+
+int mlt_merge_records(mlt_ctx* c, const int64_t* d_recs, int64_t n_rec, int64_t m, int64_t* out_idx,
+                      double* out_pred, int64_t* out_n, int64_t* out_status) {
+  if (!c) return fail(MLT_EINVAL, "ctx is NULL");
+  CTX_GUARD(c);
+  if (m < 1) return fail(MLT_EINVAL, "m must be >= 1");
+  if (n_rec < 0 || !d_recs || !out_idx || !out_pred || !out_n || !out_status)
+    return fail(MLT_EINVAL, "bad record merge arguments");
+  CU(cudaSetDevice(c->dev));
+  *out_n = 0;
+  *out_status = 0;
+  const int64_t n = n_rec * m;
+  if (n == 0) return MLT_OK;
+  double *pa, *pb;
+  int64_t *ia, *ib;
+  uint32_t* gs;
+  TRY(ws_t(c, S_OUT_A, n, &pa));
+  TRY(ws_t(c, S_OUT_B, n, &pb));
+  TRY(ws_t(c, S_OUT_C, n, &ia));
+  TRY(ws_t(c, S_OUT_D, n, &ib));
+  TRY(ws_t(c, S_GSCAL, 8, &gs));
+  {
+    uint32_t init[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    TRY(upload_pinned(c, gs, init, sizeof init));
+  }
+  unsigned long long* dstat = reinterpret_cast<unsigned long long*>(gs + 6);
+  k_merge_rec_prep<<<grid_for(c, n, 256), 256, 0, c->stream>>>(d_recs, n_rec, (int)m, ia, pa, dstat);
+  TRY(check_launch(c));
+  int64_t* hst = reinterpret_cast<int64_t*>(static_cast<uint32_t*>(c->pinned) + 12);
+  CU(cudaMemcpyAsync(hst, dstat, 8, cudaMemcpyDeviceToHost, c->stream));
+  if (n <= kSmallSort) {
+    double* tp;
+    int64_t* ti;
+    TRY(ws_t(c, S_TOPI, (size_t)std::min(m, n), &ti));
+    TRY(ws_t(c, S_TOPP, (size_t)std::min(m, n), &tp));
+    {
+      const uint32_t cnt = (uint32_t)n;
+      TRY(upload_pinned(c, gs + 2, &cnt, 4));
+    }
+    const int ssmem = 16 * kSmallSort;
+    CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)std::min<int64_t>(m, n), tp, ti, gs + 3);
+    TRY(check_launch(c));
+    TRY(emit_top(c, tp, ti, std::min(m, n), m, out_idx, out_pred, out_n));
+  } else {
+    TRY(sort_pairs(c, &pa, &ia, pb, ib, n, true));
+    TRY(emit_top(c, pa, ia, n, m, out_idx, out_pred, out_n));
+  }
+  *out_status = *hst;   // landed before emit_top's host wait returned
+  return MLT_OK;
 }
 
 int mlt_top_m(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens, int64_t m, int64_t begin, int64_t end,

@@ -43,7 +43,7 @@ __global__ void k_surr_times_masks(DSpace lr, DSurr su, const uint64_t* gmask, i
 __global__ void k_surr_best_final(const SurrPart* part, int n, SurrPart* out);
 
 // ---- final guard-band stage (select.cu) ------------------------------------
-constexpr int kSmallSort = 4096;  // survivors sorted in one CTA's shared memory
+constexpr int kSmallSort = 8192;  // survivors sorted in one CTA's shared memory (128 KB)
 __global__ void k_band_filter(const int64_t* cidx, const float* cval, const uint32_t* count_ptr, uint32_t cap, int m,
                               float band, int64_t* out_idx, float* out_val, uint32_t* out_n);
 __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint32_t* n_ptr, int m, double* out_pred,
@@ -62,6 +62,9 @@ __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint3
 #ifndef MLT_MINB
 #define MLT_MINB 1
 #endif
+#ifndef MLT_NOSEL
+#define MLT_NOSEL 1   // sweep loop without per-pair bounds selects (padded tables)
+#endif
 #ifndef MLT_EBS
 #define MLT_EBS 0
 #endif
@@ -77,9 +80,11 @@ __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 #define MLT_DEFAULT_GROUP 3
 #endif
 constexpr int kDefaultGroup = MLT_DEFAULT_GROUP;   // units per shared reciprocal unless MLT_OPT_GROUP says otherwise
-constexpr int kSB = 2048;       // per-CTA guard-band candidate slots
-constexpr int kSBLimit = 1536;  // refine/compact when the buffer would pass this
-constexpr int kMaxTopM = 1024;  // largest m served by the guard-band path
+constexpr int kSB = kThreads >= 512 ? 2 * kThreads : 1024;   // per-CTA guard-band candidate slots
+constexpr int kHalfItemWaves = 12;   // slices shallower than this many waves of whole items use half-item CTAs
+constexpr int kSBBig = 8192;   // ... in the instance for large m (kMaxTopMSmall < m <= kMaxTopM)
+constexpr int kMaxTopMSmall = 1024;  // largest m of the default sweep instance
+constexpr int kMaxTopM = 4096;       // largest m served by the guard-band path (kSBBig instance)
 constexpr int kMaxCk = 32;      // pruning checkpoints per work item
 
 struct SweepArgs {
@@ -154,8 +159,8 @@ __global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* 
 template <int G>
 __global__ void k_table_inner(TableArgs t);
 
-template <int G, bool PRUNE>
+template <int G, bool PRUNE, int SB, int NT>
 __global__ void k_sweep(SweepArgs a);
-size_t sweep_smem(int k);
+size_t sweep_smem(int k, int sb);
 
 }  // namespace mlt

@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
   const int tid = threadIdx.x;
   if (n > (uint32_t)kSmallSort) {
     if (tid == 0) status[0] = 1;                 // caller sorts with CUB
+    for (int e = tid; e < m; e += blockDim.x) {  // defined padding (the host copies the
+      out_pred[e] = __longlong_as_double(0x7ff0000000000000ll);   // lists unconditionally)
+      out_idx[e] = INT64_MAX;
+    }
     return;
   }
   uint32_t N = 1;
@@ -88,9 +92,9 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
     }
   }
   const uint32_t take = min((uint32_t)m, n);
-  for (uint32_t e = tid; e < take; e += blockDim.x) {
-    out_pred[e] = __longlong_as_double((long long)key[e]);
-    out_idx[e] = ix[e];
+  for (uint32_t e = tid; e < (uint32_t)m; e += blockDim.x) {   // padded past `take`
+    out_pred[e] = e < take ? __longlong_as_double((long long)key[e]) : __longlong_as_double(0x7ff0000000000000ll);
+    out_idx[e] = e < take ? ix[e] : INT64_MAX;
   }
   if (tid == 0) {
     status[0] = 0;

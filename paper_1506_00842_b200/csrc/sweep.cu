@@ -396,15 +396,15 @@ __host__ __device__ constexpr size_t eb_ring_bytes() { return (size_t)kEbStages 
 
 // byte offset of the second exp(-A') tile buffer (the next item's tile lands
 // there by cp.async while the current item computes)
-__host__ __device__ inline size_t ea2_offset(int k) {
+__host__ __device__ inline size_t ea2_offset(int k, int sb) {
   const size_t KH = (size_t)k * kH;
-  const size_t b = KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)kSB * (8 + 4) + 256 * 4 + eb_ring_bytes();
+  const size_t b = KH * kOB * 4 + ((KH + 3) & ~(size_t)3) * 4 + (size_t)sb * (8 + 4) + 256 * 4 + eb_ring_bytes();
   return (b + 15) & ~(size_t)15;
 }
 
-size_t sweep_smem(int k) {
+size_t sweep_smem(int k, int sb) {
   const size_t KH = (size_t)k * kH;
-  return ea2_offset(k) + KH * kOB * 4;   // ... + the second exp(-A') buffer
+  return ea2_offset(k, sb) + KH * kOB * 4;   // ... + the second exp(-A') buffer
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -425,8 +425,18 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // f32x2 pair of outers (2q, 2q+1) for inner s. (Tile constants: kernels.cuh,
 // overridable for A/B builds with tools/build_variants.sh.)
 // ---------------------------------------------------------------------------
-template <int G, bool PRUNE>
-__global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
+// NT: threads per CTA. NT = kThreads: one CTA per SM, a CTA owns whole work
+// items. NT = kThreads / 2: two CTAs per SM, each owning one HALF of an item
+// (layout threads [h*NT, h*NT + NT) of the inner block; same per-thread work
+// and table layout): used for short slices, where the last wave of whole
+// items would leave SMs idle -- a straggler CTA then has its SM to itself.
+template <int G, bool PRUNE, int SB, int NT>
+__global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepArgs a) {
+  // SB: per-CTA candidate slots (kSB; kSBBig for m > kMaxTopMSmall)
+  constexpr int kSB = SB;
+  constexpr int kSBLimit = SB * 3 / 4;
+  constexpr int HALVES = kThreads / NT;   // CTA work units per item
+  static_assert(kEbStages == 0 || NT == kThreads, "the cp.async factor ring assumes whole-item CTAs");
   extern __shared__ __align__(16) unsigned char smraw[];
   const int KH = a.k * kH;
   float* s_ea = reinterpret_cast<float*>(smraw);                 // [KH][kOB]
@@ -435,19 +445,19 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
   float* s_bval = reinterpret_cast<float*>(s_bidx + kSB);
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_bval + kSB);
   float4* s_eb = reinterpret_cast<float4*>(s_hist + 256);        // [kEbStages][W][kThreads]
-  float* s_ea2 = reinterpret_cast<float*>(smraw + ea2_offset(a.k));   // [KH][kOB], the other tile buffer
+  float* s_ea2 = reinterpret_cast<float*>(smraw + ea2_offset(a.k, SB));   // [KH][kOB], the other tile buffer
   __shared__ int s_n, s_tot;
   __shared__ unsigned int s_work;   // pruning: groups evaluated by the warps of this item
-  __shared__ uint32_t s_th, s_sel[2], s_wsum[kThreads / 32];
+  __shared__ uint32_t s_th, s_sel[2], s_wsum[NT / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int q = tid; q < KH; q += kThreads) s_u[q] = a.u[q];
+  for (int q = tid; q < KH; q += NT) s_u[q] = a.u[q];
   if (tid == 0) {
     s_n = 0;
     s_th = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
   }
   const int ngroups = KH / G;
-  const int n_items = a.n_ob * a.n_ib;
+  const int n_items = a.n_ob * a.n_ib * HALVES;   // CTA work units
   constexpr int kV = kInner * kOB;   // configurations per thread per work item (32)
 
   __shared__ __align__(16) float s_cr[kOB * kMaxCk];   // pruning: cst + remaining-unit lower bound per outer, checkpoint
@@ -465,11 +475,13 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     if (w >= n_items) break;
     // pruning visits work items best-first (ascending lower bound of their
     // mean log time), so the threshold reaches its final value within the first wave
-    const int wi = PRUNE ? __ldg(a.item_order + w) : w;
+    const int half = HALVES == 1 ? 0 : w % HALVES;
+    const int wi = PRUNE ? __ldg(a.item_order + w / HALVES) : w / HALVES;
     const int ob = wi / a.n_ib, ib = wi - ob * a.n_ib;
+    const int tl = half * NT + tid;   // this thread's column of the item's (layout) thread block
     __syncthreads();
     if (PRUNE) {
-      for (int q = tid; q < kOB * a.n_ck; q += kThreads) {   // s_cr[checkpoint][outer]
+      for (int q = tid; q < kOB * a.n_ck; q += NT) {   // s_cr[checkpoint][outer]
         const int c = q / kOB, r = q - c * kOB;
         s_cr[q] = a.cst + __ldg(a.remlo + (((size_t)ob * kOB + r) * a.n_ib + ib) * a.n_ck + c);
       }
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       cur = 0;
       const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)ob * KH * kOB);
       float4* dst = reinterpret_cast<float4*>(s_ea);
-      for (int q = tid; q < KH * kOB / 4; q += kThreads) dst[q] = __ldg(src + q);
+      for (int q = tid; q < KH * kOB / 4; q += NT) dst[q] = __ldg(src + q);
     }
     if (tid == 0) {
       s_tot = 0;
@@ -514,14 +526,14 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       const int wn = w + (int)gridDim.x;
       pf_ob = -1;
       if (wn < n_items) {
-        const int obn = wn / a.n_ib;
+        const int obn = wn / HALVES / a.n_ib;
         if (obn == ob) {
           pf_ob = ob;
           pf_buf = cur;
         } else {
           const float4* src = reinterpret_cast<const float4*>(a.ea + (size_t)obn * KH * kOB);
           float* dst = cur ? s_ea : s_ea2;
-          for (int q = tid; q < KH * kOB / 4; q += kThreads) cp_async16(dst + 4 * q, src + q);
+          for (int q = tid; q < KH * kOB / 4; q += NT) cp_async16(dst + 4 * q, src + q);
           cp_async_commit();
           pf_ob = obn;
           pf_buf = cur ^ 1;
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       }
     }
 
-    const int64_t ibase = (int64_t)ib * kInnerBlock + tid;     // inner s is ibase + s*kThreads
+    const int64_t ibase = (int64_t)ib * kInnerBlock + tl;      // inner s is ibase + s*kThreads
     bool pruned = false;   // this WARP's configurations are all provably above the threshold
     int done = ngroups;    // groups this warp evaluated
     f2 acc[kInner][kOB / 2];
@@ -540,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
 
     constexpr int W = ebw_of(G);
     const size_t gstride = (size_t)kThreads * W;   // float4s per group
-    const float4* pe = reinterpret_cast<const float4*>(a.ebp) + ((size_t)ib * ngroups * kThreads + tid) * W;
+    const float4* pe = reinterpret_cast<const float4*>(a.ebp) + ((size_t)ib * ngroups * kThreads + tl) * W;
     const float* pu = s_u;                   // 1/w' of the current group
     const float* E = s_cur;                  // exp(-A') rows of the current group
     if (kEbStages > 0) {
@@ -625,6 +637,20 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
             break;
           }
         }
+#if MLT_NOSEL
+        // No bounds selects: the tables carry one group of padding past the
+        // end (ebp allocation; s_u / s_ea are followed by other shared
+        // memory), so the prefetch of group gi + 2 on the last pair reads
+        // valid memory it never uses, and odd group counts end below.
+        if (gi + 1 >= ngroups) {
+          group_step<G>(acc, E, ebA, uA);
+          break;
+        }
+        load_group<G>(pe + gstride, pu + G, ebB, uB);
+        group_step<G>(acc, E, ebA, uA);
+        load_group<G>(pe + 2 * gstride, pu + 2 * G, ebA, uA);
+        group_step<G>(acc, E + G * kOB, ebB, uB);
+#else
         const bool has_b = gi + 1 < ngroups;
         load_group<G>(has_b ? pe + gstride : pe, has_b ? pu + G : pu, ebB, uB);
         group_step<G>(acc, E, ebA, uA);
@@ -632,6 +658,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
         const bool has_c = gi + 2 < ngroups;
         load_group<G>(has_c ? pe + 2 * gstride : pe, has_c ? pu + 2 * G : pu, ebA, uA);
         group_step<G>(acc, E + G * kOB, ebB, uB);
+#endif
         pe += 2 * gstride;
         pu += 2 * G;
         E += 2 * G * kOB;
@@ -735,14 +762,14 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       if (n >= a.m) {
         const uint32_t key = block_select(
             [&](auto&& f) {
-              for (int e = tid; e < n; e += kThreads) f(fkey(s_bval[e]));
+              for (int e = tid; e < n; e += NT) f(fkey(s_bval[e]));
             },
             a.m, s_hist, s_sel);
         lower_threshold(a, &s_th, key);
         __syncthreads();
       }
       const float thf = fkey_inv(s_th);
-      constexpr int kPer = (kSB + kThreads - 1) / kThreads;   // any block size (768: 3 slots per thread)
+      constexpr int kPer = (kSB + NT - 1) / NT;   // any block size (768: 3 slots per thread)
       int64_t ki[kPer];
       float kv[kPer];
       uint32_t keep = 0;
@@ -765,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       if (lane == 31) s_wsum[warp] = incl;
       __syncthreads();
       int off = incl - c, total = 0;
-      for (int q = 0; q < kThreads / 32; ++q) {
+      for (int q = 0; q < NT / 32; ++q) {
         if (q < warp) off += s_wsum[q];
         total += s_wsum[q];
       }
@@ -779,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
       }
       __syncthreads();
       if (total > kSBLimit) {  // a crowded band: spill everything to the global buffer
-        for (int e = tid; e < total; e += kThreads) gappend(a, s_bidx[e], s_bval[e]);
+        for (int e = tid; e < total; e += NT) gappend(a, s_bidx[e], s_bval[e]);
         total = 0;
       }
       if (tid == 0) s_n = total;
@@ -791,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, MLT_MINB) k_sweep(SweepArgs a) {
     const uint32_t g = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
     const float thf = fkey_inv(min(s_th, g));
     const int n = min(s_n, kSB);
-    for (int e = tid; e < n; e += kThreads)
+    for (int e = tid; e < n; e += NT)
       if (!(s_bval[e] > thf)) gappend(a, s_bidx[e], s_bval[e]);
   }
 }
@@ -800,13 +827,37 @@ template __global__ void k_table_inner<1>(TableArgs t);
 template __global__ void k_table_inner<2>(TableArgs t);
 template __global__ void k_table_inner<3>(TableArgs t);
 template __global__ void k_table_inner<4>(TableArgs t);
-template __global__ void k_sweep<1, false>(SweepArgs a);
-template __global__ void k_sweep<2, false>(SweepArgs a);
-template __global__ void k_sweep<3, false>(SweepArgs a);
-template __global__ void k_sweep<4, false>(SweepArgs a);
-template __global__ void k_sweep<1, true>(SweepArgs a);
-template __global__ void k_sweep<2, true>(SweepArgs a);
-template __global__ void k_sweep<3, true>(SweepArgs a);
-template __global__ void k_sweep<4, true>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSB, kThreads>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSBBig, kThreads>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSB, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSBBig, kThreads / 2>(SweepArgs a);
 
 }  // namespace mlt

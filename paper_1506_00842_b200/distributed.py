@@ -65,11 +65,102 @@ def gather_top_lists(idx, pred, m: int, group=None):
     return out[:, 0, :].reshape(-1).contiguous(), out[:, 1, :].reshape(-1).contiguous().view(torch.float64)
 
 
+def _record_from_host(idx, pred, m, dev):
+    """A host (index, prediction) list as an mlt_plan_top_m_record record."""
+    import torch
+    rec = torch.empty(2 * m + 1, dtype=torch.int64)
+    rec[:m] = PAD_IDX
+    rec[m:2 * m] = torch.tensor([float("inf")], dtype=torch.float64).view(torch.int64)
+    n = len(idx)
+    rec[:n] = torch.from_numpy(np.asarray(idx, dtype=np.int64))
+    rec[m:m + n] = torch.from_numpy(np.asarray(pred, dtype=np.float64).view(np.int64))
+    rec[2 * m] = 0
+    return rec.to(dev)
+
+
+def records_protocol(rank: int, world: int, m: int, first_record, gather, merge, redo_record):
+    """The exchange of the sharded step, backend- and device-agnostic (CPU
+    tests drive it over gloo with numpy records):
+      rec = first_record()            this rank's (2m+1)-int64 record
+      out = gather(rec)               all ranks' records, (world*(2m+1),)
+      idx, pred, status = merge(out)  global top-m, OR of the status words
+    A nonzero status means some shard's fast path could not finish (guard
+    band overflow): every rank sees the same gathered statuses, the ranks
+    whose own status is set rebuild their record with `redo_record()` (the
+    exact path), and all ranks gather and merge once more."""
+    rec = first_record()
+    for attempt in range(2):
+        out = gather(rec)
+        idx, pred, status = merge(out)
+        if status == 0:
+            return idx, pred
+        if attempt == 1:
+            raise RuntimeError("sharded top-m: a shard stayed unresolved after the exact redo")
+        mine = int(np.asarray(out.reshape(world, 2 * m + 1)[rank, 2 * m].tolist()))
+        if mine != 0:
+            rec = redo_record()
+    raise AssertionError("unreachable")
+
+
+def top_m_arrays_records(ensemble, space, m: int, group=None, plan=None):
+    """The device-resident sharded step: every rank enqueues its
+    shard's top-m straight into a device record (`mlt_plan_top_m_record`, no
+    host round trip), ONE all-gather moves the (2m+1)-int64 records (NCCL:
+    device to device, ordered on the caller's stream), and `mlt_merge_records`
+    sorts the P*m entries on the device with one host wait for the result
+    (`records_protocol` handles a shard whose guard band overflowed)."""
+    import torch
+    import torch.distributed as dist
+    from . import _native as N
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.cuda.current_device()
+    cdev = torch.device("cuda", dev)
+    lo, hi = shard_bounds(space.cardinality(), rank, world)
+    plan = plan or N.plan(space, ensemble, dev)
+
+    def first_record():
+        rec = torch.empty(2 * m + 1, dtype=torch.int64, device=cdev)
+        N.check(N.lib().mlt_plan_top_m_record(plan.h, int(m), lo, hi, N.C.c_void_p(rec.data_ptr())),
+                "mlt_plan_top_m_record")
+        return rec
+
+    def gather(rec):
+        send = rec if nccl else rec.cpu()          # gloo: functional runs only
+        out = torch.empty(world * (2 * m + 1), dtype=torch.int64, device=send.device)
+        dist.all_gather_into_tensor(out, send, group=group)
+        return out if nccl else out.to(cdev)
+
+    def merge(out):
+        oi, op = np.empty(m, np.int64), np.empty(m, np.float64)
+        on, ost = N.C.c_int64(0), N.C.c_int64(0)
+        N.check(N.lib().mlt_merge_records(N.ctx(dev), N.C.c_void_p(out.data_ptr()), world, int(m),
+                                          N.ptr(oi, N.C.c_int64), N.ptr(op, N.C.c_double), N.C.byref(on),
+                                          N.C.byref(ost)), "mlt_merge_records")
+        return oi[:on.value], op[:on.value], ost.value
+
+    def redo_record():
+        li, lp = np.empty(m, np.int64), np.empty(m, np.float64)
+        ln, st = N.C.c_int64(0), N.MltSweepStats()
+        N.check(N.lib().mlt_plan_top_m(plan.h, int(m), lo, hi, N.ptr(li, N.C.c_int64), N.ptr(lp, N.C.c_double),
+                                       N.C.byref(ln), N.C.byref(st)), "mlt_plan_top_m")
+        return _record_from_host(li[:ln.value], lp[:ln.value], m, cdev)
+
+    with N.on_stream(dev, torch.cuda.current_stream().cuda_stream):
+        return records_protocol(rank, world, m, first_record, gather, merge, redo_record)
+
+
 def top_m_arrays_sharded(ensemble, space, m: int, group=None, local_fn=None, merge_fn=None):
-    """Sharded top-m over the whole space; identical result on every rank."""
+    """Sharded top-m over the whole space; identical result on every rank.
+    Without injected local/merge functions (CPU tests inject the oracle) this
+    is the device-resident record path, `top_m_arrays_records`."""
     import torch.distributed as dist
     if m < 1:
         raise ValueError("m must be >= 1")
+    if local_fn is None and merge_fn is None:
+        return top_m_arrays_records(ensemble, space, m, group)
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     lo, hi = shard_bounds(space.cardinality(), rank, world)

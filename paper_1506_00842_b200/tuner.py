@@ -94,13 +94,17 @@ def top_m_arrays(ensemble, space, m: int, begin: int = 0, end: int | None = None
     st = N.MltSweepStats()
     if indices is not None:
         lst = np.ascontiguousarray(indices, dtype=np.int64)
-        lp, ln = N.ptr(lst, N.C.c_int64), lst.shape[0]
+        rc = N.lib().mlt_top_m(N.ctx(device), N.C.byref(ps.c), N.C.byref(pe.c), int(m), int(begin), end,
+                               N.ptr(lst, N.C.c_int64), lst.shape[0], N.ptr(out_idx, N.C.c_int64),
+                               N.ptr(out_pred, N.C.c_double), N.C.byref(out_n), N.C.byref(st))
+        N.check(rc, "mlt_top_m")
     else:
-        lp, ln = None, 0
-    rc = N.lib().mlt_top_m(N.ctx(device), N.C.byref(ps.c), N.C.byref(pe.c), int(m), int(begin), end, lp, ln,
-                           N.ptr(out_idx, N.C.c_int64), N.ptr(out_pred, N.C.c_double), N.C.byref(out_n),
-                           N.C.byref(st))
-    N.check(rc, "mlt_top_m")
+        # slices run on the resident plan of (space, ensemble): descriptors and
+        # factored tables persist across calls with the same objects
+        plan = N.plan(space, ensemble, device)
+        rc = N.lib().mlt_plan_top_m(plan.h, int(m), int(begin), end, N.ptr(out_idx, N.C.c_int64),
+                                    N.ptr(out_pred, N.C.c_double), N.C.byref(out_n), N.C.byref(st))
+        N.check(rc, "mlt_plan_top_m")
     n = out_n.value
     res = (out_idx[:n].copy(), out_pred[:n].copy())
     return res + (st.as_dict(),) if with_stats else res

@@ -149,3 +149,85 @@ def test_sharded_exhaustive_equals_single(world):
         assert p.exitcode == 0
     for rank, i, t, nv in res:
         assert i == 88599 and abs(t - 0.014444711) < 1e-8 and nv > 0
+
+
+def _records_worker(rank, world, port, case, m, bad_rank, q):
+    """records_protocol over gloo with numpy records: rank `bad_rank` reports a
+    guard-band overflow on its first record (status 1) and must redo its shard;
+    every rank must still end with the single-sweep top-m."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch
+    import torch.distributed as dist
+    from conftest import CASE_SPACE, oracle_ensemble, oracle_space
+    from oracle.tuner import top_m
+    from paper_1506_00842_b200.distributed import records_protocol, shard_bounds
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        osp = oracle_space(CASE_SPACE[case])
+        oens = oracle_ensemble(case)
+        lo, hi = shard_bounds(osp.card, rank, world)
+        calls = {"redo": 0, "gather": 0}
+
+        def record(status):
+            i, p = top_m(oens, osp, m, begin=lo, end=hi)
+            rec = np.full(2 * m + 1, -1, dtype=np.int64)
+            rec[m:2 * m] = np.array([np.inf]).view(np.int64)[0]
+            if status == 0:
+                rec[:len(i)] = i
+                rec[m:m + len(i)] = np.asarray(p, dtype=np.float64).view(np.int64)
+            rec[2 * m] = status
+            return torch.from_numpy(rec)
+
+        def gather(rec):
+            calls["gather"] += 1
+            out = torch.empty(world * (2 * m + 1), dtype=torch.int64)
+            dist.all_gather_into_tensor(out, rec)
+            return out
+
+        def merge(out):
+            recs = out.numpy().reshape(world, 2 * m + 1)
+            gi = recs[:, :m].reshape(-1)
+            gp = recs[:, m:2 * m].reshape(-1).copy().view(np.float64)
+            status = int(np.bitwise_or.reduce(recs[:, 2 * m]))
+            keep = gi >= 0
+            gi, gp = gi[keep], gp[keep]
+            o = np.lexsort((gi, gp))[:m]
+            return gi[o], gp[o], status
+
+        def redo():
+            calls["redo"] += 1
+            return record(0)
+
+        i, p = records_protocol(rank, world, m, lambda: record(1 if rank == bad_rank else 0), gather, merge, redo)
+        q.put((rank, i.tolist(), p.tolist(), calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bad_rank", [-1, 1])
+def test_records_protocol_redoes_overflowed_shards(bad_rank):
+    from conftest import golden
+    world, m = 2, 200
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_records_worker, args=(r, world, port, "conv_k1", m, bad_rank, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = golden("topm_conv_k1.npz")
+    for rank, i, p, calls in res:
+        assert i == g["m200_i"].tolist(), rank
+        assert p == g["m200_p"].tolist()
+        assert calls["gather"] == (1 if bad_rank < 0 else 2)
+        assert calls["redo"] == (1 if rank == bad_rank else 0)

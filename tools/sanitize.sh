@@ -7,7 +7,7 @@ set -u
 cd "$(dirname "$0")/.."
 OUT=gpurun_out/sanitize
 mkdir -p $OUT
-CASES=${*:-sweep_band sweep_pruned_chunked band_overflow_exact sweep_groups train surrogate conv stereo raycast predict_merge}
+CASES=${*:-sweep_band sweep_pruned_chunked band_overflow_exact sweep_groups train surrogate conv stereo raycast predict_merge records}
 : > $OUT/summary.txt
 for tool in memcheck racecheck synccheck initcheck; do
   for c in $CASES; do

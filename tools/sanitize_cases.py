@@ -6,7 +6,7 @@ but computes garbage fails too.
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py sweep_band
 
 Cases: sweep_band, sweep_pruned_chunked, band_overflow_exact, sweep_groups,
-train, surrogate, conv, stereo, raycast, predict_merge. `all` runs them in turn.
+train, surrogate, conv, stereo, raycast, predict_merge, records. `all` runs them in turn.
 """
 
 from __future__ import annotations
@@ -210,11 +210,44 @@ def predict_merge():
     mi, _ = _device_merge(gi, gp, 30)
     whole = top_m_arrays(ens, product_space("convolution"), 30, begin=0, end=32768)
     assert np.array_equal(mi, whole[0])
+    del gi, gp
+    torch.cuda.empty_cache()   # torch's caching allocator would otherwise show as a leak
     return {}
 
 
+def records():
+    """mlt_plan_top_m_record (k_pack_record behind the band stage) for 4 shards
+    + mlt_merge_records (k_merge_rec_prep + k_sort_small), and a forced
+    overflow record."""
+    import torch
+    from paper_1506_00842_b200.distributed import shard_bounds
+    sp, ens = product_space("stereo"), product_ensemble("stereo_k8")
+    lo_all, hi_all = 0, 1 << 19
+    m, world = 40, 4
+    plan = N.plan(sp, ens, 0)
+    out = torch.empty((world, 2 * m + 1), dtype=torch.int64, device="cuda:0")
+    for r in range(world):
+        lo, hi = shard_bounds(hi_all - lo_all, r, world)
+        N.check(N.lib().mlt_plan_top_m_record(plan.h, m, lo, hi, N.C.c_void_p(out[r].data_ptr())))
+    oi, op = np.empty(m, np.int64), np.empty(m, np.float64)
+    on, ost = N.C.c_int64(0), N.C.c_int64(0)
+    N.check(N.lib().mlt_merge_records(N.ctx(0), N.C.c_void_p(out.data_ptr()), world, m, N.ptr(oi, N.C.c_int64),
+                                      N.ptr(op, N.C.c_double), N.C.byref(on), N.C.byref(ost)))
+    from oracle.tuner import top_m
+    ri, rp = top_m(oracle_ensemble("stereo_k8"), oracle_space("stereo"), m, begin=lo_all, end=hi_all)
+    assert ost.value == 0 and np.array_equal(oi[:on.value], ri)
+    _opt(N.MLT_OPT_CAND_CAP, 8)
+    N.check(N.lib().mlt_plan_top_m_record(plan.h, m, 0, 1 << 18, N.C.c_void_p(out[0].data_ptr())))
+    _reset()
+    assert int(out[0, 2 * m].item()) == 1
+    del out
+    N.clear_plans()
+    torch.cuda.empty_cache()
+    return {"merged": int(on.value)}
+
+
 CASES = {f.__name__: f for f in (sweep_band, sweep_pruned_chunked, band_overflow_exact, sweep_groups, train,
-                                 surrogate, conv, stereo, raycast, predict_merge)}
+                                 surrogate, conv, stereo, raycast, predict_merge, records)}
 
 if __name__ == "__main__":
     names = list(CASES) if sys.argv[1:] in ([], ["all"]) else sys.argv[1:]

@@ -19,21 +19,25 @@ c = N.ctx(0)
 N.check(N.lib().mlt_ctx_set_profiling(c, 1))
 if os.environ.get("MLT_GROUP"):
     N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_GROUP, int(os.environ["MLT_GROUP"])))
+if os.environ.get("MLT_HALF"):
+    N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_HALF_ITEMS, int(os.environ["MLT_HALF"])))
 if os.environ.get("MLT_PRUNE") == "1":
     N.check(N.lib().mlt_ctx_set_option(c, 4, 1))
 ps, pe = N.packed(sp, "space"), N.packed(ens, "ensemble")
 plan = N.C.c_void_p()
 N.check(N.lib().mlt_plan_create(c, N.C.byref(ps.c), N.C.byref(pe.c), N.C.byref(plan)))
 oi, op, on, st = np.empty(200, np.int64), np.empty(200), N.C.c_int64(), N.MltSweepStats()
+P = int(os.environ.get("MLT_SLICE", "1"))      # sweep [0, card/P): one rank's shard at P ranks
+hi = sp.cardinality() // P
 sw, tot = [], []
 for r in range(reps + 2):
-    N.check(N.lib().mlt_plan_top_m(plan, 200, 0, sp.cardinality(), N.ptr(oi, N.C.c_int64), N.ptr(op, N.C.c_double),
+    N.check(N.lib().mlt_plan_top_m(plan, 200, 0, hi, N.ptr(oi, N.C.c_int64), N.ptr(op, N.C.c_double),
                                    N.C.byref(on), N.C.byref(st)))
     if r >= 2:
         sw.append(st.sweep_ms)
         tot.append(st.total_ms)
 g = np.load(G / f"topm_{case}.npz")
-ok = bool(np.array_equal(oi[:on.value], g["m200_i"])) if "m200_i" in g.files else None
-print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "prune": os.environ.get("MLT_PRUNE") == "1", "sweep_ms_min": min(sw),
+ok = bool(np.array_equal(oi[:on.value], g["m200_i"])) if "m200_i" in g.files and P == 1 else None
+print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "prune": os.environ.get("MLT_PRUNE") == "1", "slice": P, "half": os.environ.get("MLT_HALF", "auto"), "sweep_ms_min": min(sw),
                   "sweep_ms_med": float(np.median(sw)), "total_ms_med": float(np.median(tot)),
                   "parity": ok, "group": st.group, "cands": st.candidates, "evaluated_frac": st.evaluated_frac, "raw": st.raw_candidates, "delta": st.delta}))
