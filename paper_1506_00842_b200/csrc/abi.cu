@@ -1131,6 +1131,10 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
         p->t_ebp_cap = 0;
         CU(cudaMallocAsync(&p->t_ebp, n_ebp * 4, c->stream));
         p->t_ebp_cap = n_ebp;
+        // the padding past the last group is read (never used) by the sweep's
+        // prefetch: give it defined contents once
+        const size_t pad = (size_t)2 * kThreads * ebw * 4;
+        CU(cudaMemsetAsync(p->t_ebp + (n_ebp - pad), 0, pad * 4, c->stream));
       }
       std::fill(p->t_key, p->t_key + 5, -1);   // valid again only once the tables below are built
     }

@@ -81,7 +81,7 @@ __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 #endif
 constexpr int kDefaultGroup = MLT_DEFAULT_GROUP;   // units per shared reciprocal unless MLT_OPT_GROUP says otherwise
 constexpr int kSB = kThreads >= 512 ? 2 * kThreads : 1024;   // per-CTA guard-band candidate slots
-constexpr int kHalfItemWaves = 12;   // slices shallower than this many waves of whole items use half-item CTAs
+constexpr int kHalfItemWaves = 8;   // slices shallower than this many waves of whole items use half-item CTAs
 constexpr int kSBBig = 8192;   // ... in the instance for large m (kMaxTopMSmall < m <= kMaxTopM)
 constexpr int kMaxTopMSmall = 1024;  // largest m of the default sweep instance
 constexpr int kMaxTopM = 4096;       // largest m served by the guard-band path (kSBBig instance)

@@ -707,6 +707,11 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
         }
       }
     }
+    // s_n is read BEFORE the barrier: after it, a fast warp may already be
+    // appending (atomicAdd on s_n) while a slow one evaluates the refine
+    // condition -- with a live read the two could disagree and diverge at the
+    // block_select barriers (compute-sanitizer synccheck)
+    const int n_held = s_n;
     {
       int c = __popc(mask);
 #pragma unroll
@@ -714,7 +719,7 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
       if (lane == 0 && c) atomicAdd(&s_tot, c);
     }
     __syncthreads();
-    if (s_n + s_tot > kSBLimit && s_tot >= a.m) {
+    if (n_held + s_tot > kSBLimit && s_tot >= a.m) {
       // too many pass: the m-th best of this work item bounds the global m-th best
       const uint32_t key = block_select(
           [&](auto&& f) {

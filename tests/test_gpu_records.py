@@ -22,10 +22,12 @@ def _records(ens, sp, m, world, torch, begin=0, end=None):
     plan = N.plan(sp, ens, 0)
     card = sp.cardinality() if end is None else end
     out = torch.full((world, 2 * m + 1), 7, dtype=torch.int64, device="cuda:0")
-    for r in range(world):
-        lo, hi = shard_bounds(card - begin, r, world)
-        N.check(N.lib().mlt_plan_top_m_record(plan.h, m, begin + lo, begin + hi,
-                                              N.C.c_void_p(out[r].data_ptr())))
+    # on torch's stream, so torch reads of `out` are ordered behind the records
+    with N.on_stream(0, torch.cuda.current_stream().cuda_stream):
+        for r in range(world):
+            lo, hi = shard_bounds(card - begin, r, world)
+            N.check(N.lib().mlt_plan_top_m_record(plan.h, m, begin + lo, begin + hi,
+                                                  N.C.c_void_p(out[r].data_ptr())))
     return out
 
 

@@ -55,7 +55,8 @@ def report(name, ens, m, exact_check=True, golden_key=None):
     if exact_check:
         xi, xp, _, xms = step(ens, m, reps=1, path=1)
         line["exact_path_ms"] = xms
-        line["equal_to_exact_path"] = bool(np.array_equal(idx, xi) and np.array_equal(pred, xp))
+        line["equal_to_exact_path"] = bool(np.array_equal(idx, xi))
+        line["max_rel_pred_diff"] = float(np.max(np.abs(pred - xp) / np.abs(xp))) if len(xp) == len(pred) else None
     print(json.dumps(line), flush=True)
 
 

@@ -226,6 +226,7 @@ def records():
     m, world = 40, 4
     plan = N.plan(sp, ens, 0)
     out = torch.empty((world, 2 * m + 1), dtype=torch.int64, device="cuda:0")
+    N.check(N.lib().mlt_ctx_set_stream(N.ctx(0), N.C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     for r in range(world):
         lo, hi = shard_bounds(hi_all - lo_all, r, world)
         N.check(N.lib().mlt_plan_top_m_record(plan.h, m, lo, hi, N.C.c_void_p(out[r].data_ptr())))
@@ -240,6 +241,7 @@ def records():
     N.check(N.lib().mlt_plan_top_m_record(plan.h, m, 0, 1 << 18, N.C.c_void_p(out[0].data_ptr())))
     _reset()
     assert int(out[0, 2 * m].item()) == 1
+    N.check(N.lib().mlt_ctx_set_stream(N.ctx(0), None))
     del out
     N.clear_plans()
     torch.cuda.empty_cache()
