@@ -439,7 +439,7 @@ def main():
     k, d = ens.k, ens.encoder.input_dim
     ctx = N.ctx(local)
     stream = torch.cuda.current_stream()
-    N.check(N.lib().mlt_ctx_set_stream(ctx, N.C.c_void_p(stream.cuda_stream)))
+    N.check(N.lib().mlt_ctx_set_stream(ctx, N.C.c_void_p(N.stream_handle(stream))))
     N.check(N.lib().mlt_ctx_set_profiling(ctx, 1))
     ps, pe = N.packed(space, "space"), N.packed(ens, "ensemble")
     rplan = N.plan(space, ens, local)          # the resident plan of the workload

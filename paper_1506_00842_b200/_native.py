@@ -274,6 +274,17 @@ def clear_plans() -> None:
         p.destroy()
 
 
+CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: the legacy default stream as an explicit handle
+
+
+def stream_handle(torch_stream) -> int:
+    """A torch stream as a handle for mlt_ctx_set_stream. torch's default
+    stream reports handle 0, which mlt_ctx_set_stream reads as "the library's
+    own (non-blocking) stream"; pass cudaStreamLegacy instead so the library's
+    work really orders against torch's kernels and events."""
+    return int(torch_stream.cuda_stream) or CUDA_STREAM_LEGACY
+
+
 class on_stream:
     """Run a context's work on a CUDA stream (a torch stream's handle) for the
     duration of a `with` block, so device results order against collectives
@@ -282,7 +293,8 @@ class on_stream:
     _current: dict[int, int] = {}
 
     def __init__(self, device: int, stream_handle: int):
-        self.device, self.handle = int(device), int(stream_handle)
+        # handle 0 from torch is its legacy default stream, not "no stream"
+        self.device, self.handle = int(device), int(stream_handle) or CUDA_STREAM_LEGACY
 
     def __enter__(self):
         self.prev = on_stream._current.get(self.device, 0)

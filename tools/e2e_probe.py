@@ -42,7 +42,7 @@ print(json.dumps(out))
 if "--torch" in sys.argv:
     import torch
     stream = torch.cuda.current_stream()
-    N.check(N.lib().mlt_ctx_set_stream(c, N.C.c_void_p(stream.cuda_stream)))
+    N.check(N.lib().mlt_ctx_set_stream(c, N.C.c_void_p(N.stream_handle(stream))))
     N.check(N.lib().mlt_ctx_set_profiling(c, 0))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     res = {}

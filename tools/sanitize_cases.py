@@ -226,7 +226,7 @@ def records():
     m, world = 40, 4
     plan = N.plan(sp, ens, 0)
     out = torch.empty((world, 2 * m + 1), dtype=torch.int64, device="cuda:0")
-    N.check(N.lib().mlt_ctx_set_stream(N.ctx(0), N.C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    N.check(N.lib().mlt_ctx_set_stream(N.ctx(0), N.C.c_void_p(N.stream_handle(torch.cuda.current_stream()))))
     for r in range(world):
         lo, hi = shard_bounds(hi_all - lo_all, r, world)
         N.check(N.lib().mlt_plan_top_m_record(plan.h, m, lo, hi, N.C.c_void_p(out[r].data_ptr())))
