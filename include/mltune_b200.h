@@ -120,7 +120,9 @@ MLT_API const char* mlt_last_error(void);
 
 MLT_API int mlt_ctx_create(int device, mlt_ctx** out);
 MLT_API int mlt_ctx_destroy(mlt_ctx* ctx);
-/* Use `stream` (a cudaStream_t) for all work; NULL restores the library stream. */
+/* Use `stream` (a cudaStream_t; cudaStreamLegacy = (void*)1 for the legacy
+ * default stream) for all work; NULL restores the library's own stream. Work
+ * already queued on the previous stream is ordered before the new stream's. */
 MLT_API int mlt_ctx_set_stream(mlt_ctx* ctx, void* stream);
 /* When on, mlt_top_m records CUDA events around its kernels (mlt_sweep_stats). */
 MLT_API int mlt_ctx_set_profiling(mlt_ctx* ctx, int on);

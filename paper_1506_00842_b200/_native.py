@@ -242,6 +242,13 @@ class Plan:
                 _lib.mlt_plan_destroy(self.h)
             self.h = C.c_void_p()
 
+    def __del__(self):
+        # plans live while anyone holds them: the cache only drops its reference
+        try:
+            self.destroy()
+        except Exception:   # interpreter shutdown: the library may be gone
+            pass
+
 
 _plan_cache: dict[tuple, tuple] = {}
 _PLAN_CACHE_MAX = 8
@@ -261,17 +268,14 @@ def plan(space, ensemble, device=None) -> Plan:
     with _ctx_lock:
         _plan_cache[key] = (space, ensemble, p)
         while len(_plan_cache) > _PLAN_CACHE_MAX:
-            old = _plan_cache.pop(next(iter(_plan_cache)))
-            old[2].destroy()
+            _plan_cache.pop(next(iter(_plan_cache)))   # destroyed once no caller holds it
     return p
 
 
 def clear_plans() -> None:
+    """Drop every cached plan (each is destroyed once no caller holds it)."""
     with _ctx_lock:
-        items = list(_plan_cache.values())
         _plan_cache.clear()
-    for _, _, p in items:
-        p.destroy()
 
 
 CUDA_STREAM_LEGACY = 1   # cudaStreamLegacy: the legacy default stream as an explicit handle
@@ -312,7 +316,11 @@ def shutdown() -> None:
     with atexit so a process ends with the library's device memory released
     (compute-sanitizer's leak check sees no leftovers); ctx() after this
     creates fresh contexts."""
-    clear_plans()
+    with _ctx_lock:
+        plans = [v[2] for v in _plan_cache.values()]
+        _plan_cache.clear()
+    for p in plans:          # before their contexts go away
+        p.destroy()
     with _ctx_lock:
         items = list(_ctxs.items())
         _ctxs.clear()

@@ -76,6 +76,7 @@ struct mlt_ctx {
   size_t stage_cap = 0;
   size_t stage_off = 0;         // next free byte of the ring
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_switch = nullptr;   // orders work across mlt_ctx_set_stream
   // Serialises every entry point on this context (workspace slots, pinned
   // staging and the stream are per-context state): concurrent callers of one
   // context queue instead of racing. Recursive: mlt_top_m -> mlt_plan_create.
@@ -793,6 +794,7 @@ int mlt_ctx_create(int device, mlt_ctx** out) {
   }
   CU(cudaMallocHost(&c->pinned, 4096));
   for (auto& ev : c->ev) CU(cudaEventCreate(&ev));
+  CU(cudaEventCreateWithFlags(&c->ev_switch, cudaEventDisableTiming));
   *out = c;
   return MLT_OK;
 }
@@ -808,6 +810,7 @@ int mlt_ctx_destroy(mlt_ctx* c) {
   if (c->res_pin) cudaFreeHost(c->res_pin);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
+  if (c->ev_switch) cudaEventDestroy(c->ev_switch);
   if (c->own) cudaStreamDestroy(c->own);
   // stream-ordered frees (plans, tables, trainer buffers) return memory to the
   // device's default pool; hand the pool's idle memory back to the driver
@@ -820,7 +823,14 @@ int mlt_ctx_destroy(mlt_ctx* c) {
 int mlt_ctx_set_stream(mlt_ctx* c, void* stream) {
   if (!c) return fail(MLT_EINVAL, "ctx is NULL");
   CTX_GUARD(c);
-  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  if (next != c->stream) {
+    // work already queued on the old stream (workspace slots, pinned staging,
+    // device results) must precede everything queued on the new one
+    CU(cudaEventRecord(c->ev_switch, c->stream));
+    CU(cudaStreamWaitEvent(next, c->ev_switch, 0));
+    c->stream = next;
+  }
   return MLT_OK;
 }
 
@@ -1347,10 +1357,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     TRY(check_launch(c));
     // 2) fp64 rescoring of the survivors, one warp each (grid-stride over the
     //    device count; survivors are few, ~m, so 32 CTAs of 8 warps)
-    const size_t smem64 = predict64_smem(p->de);
-    if (smem64 > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem64);
-    CU(cudaFuncSetAttribute(k_rescore_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64));
-    k_rescore_warp<<<32, 256, smem64, c->stream>>>(p->de, ia, gs + 2, pa);
+    k_rescore_warp<<<64, 256, 0, c->stream>>>(p->de, ia, gs + 2, pa);
     TRY(check_launch(c));
     // 3) sort by (prediction, index) in one CTA when small
     const int ssmem = 16 * kSmallSort;

@@ -44,6 +44,7 @@ __global__ void k_surr_best_final(const SurrPart* part, int n, SurrPart* out);
 
 // ---- final guard-band stage (select.cu) ------------------------------------
 constexpr int kSmallSort = 8192;  // survivors sorted in one CTA's shared memory (128 KB)
+constexpr int kRankSort = 2048;   // ... by rank counting up to this many, bitonic above
 __global__ void k_band_filter(const int64_t* cidx, const float* cval, const uint32_t* count_ptr, uint32_t cap, int m,
                               float band, int64_t* out_idx, float* out_val, uint32_t* out_n);
 __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint32_t* n_ptr, int m, double* out_pred,

@@ -161,23 +161,17 @@ size_t predict64_smem(const DEns& e) {
 namespace mlt {
 
 // Guard-band rescoring: one warp per candidate; lane j evaluates hidden unit j
-// of every member, the member output is a warp reduction. Same per-member
-// rounding sequence as k_predict64 (out*std + mean, member order, /k, exp).
+// of every member, each member output is a warp reduction. The per-unit and
+// per-member rounding sequence is k_predict64's (out*std + mean, member
+// order, /k, exp). The members' chains are independent: they run kRU at a
+// time (the exp / divide latencies overlap), weights straight from L2 (a
+// survivor reads its 53 KB once; no per-CTA staging of the whole ensemble).
 __global__ void __launch_bounds__(256) k_rescore_warp(DEns e, const int64_t* __restrict__ idx,
                                                       const uint32_t* __restrict__ n_ptr, double* __restrict__ pred) {
-  extern __shared__ double sm[];
-  stage_weights(e, sm);
-  __syncthreads();
+  constexpr int kRU = 4;
   const uint32_t n = *n_ptr;
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  const int nw = e.k * e.h * e.d, nh = e.k * e.h;
-  const double* W1 = sm;
-  const double* B1 = sm + nw;
-  const double* W2 = sm + nw + nh;
-  const double* B2 = sm + nw + 2 * nh;
-  const double* MU = B2 + e.k;
-  const double* SD = MU + e.k;
   for (uint32_t t = blockIdx.x * wpb + (threadIdx.x >> 5); t < n; t += gridDim.x * wpb) {
     uint64_t r = (uint64_t)idx[t];
     double x[kMaxP];
@@ -193,22 +187,37 @@ __global__ void __launch_bounds__(256) k_rescore_warp(DEns e, const int64_t* __r
       }
     }
     double acc = 0.0;
-    for (int m = 0; m < e.k; ++m) {
-      double part = 0.0;
-      for (int j = lane; j < e.h; j += 32) {
-        const double* w = W1 + (m * e.h + j) * e.d;
-        double z = 0.0;
+    for (int m0 = 0; m0 < e.k; m0 += kRU) {
+      double part[kRU];
 #pragma unroll
-        for (int p = 0; p < kMaxP; ++p)
-          if (p < e.d) z = fma(x[p], w[p], z);
-        z = __dadd_rn(z, B1[m * e.h + j]);
-        part = fma(1.0 / (1.0 + exp(-z)), W2[m * e.h + j], part);
+      for (int u = 0; u < kRU; ++u) {
+        part[u] = 0.0;
+        const int m = m0 + u;
+        if (m < e.k) {
+          for (int j = lane; j < e.h; j += 32) {
+            const double* w = e.w1 + ((size_t)m * e.h + j) * e.d;
+            double z = 0.0;
+#pragma unroll
+            for (int p = 0; p < kMaxP; ++p)
+              if (p < e.d) z = fma(x[p], __ldg(w + p), z);
+            z = __dadd_rn(z, __ldg(e.b1 + m * e.h + j));
+            part[u] = fma(1.0 / (1.0 + exp(-z)), __ldg(e.w2 + m * e.h + j), part[u]);
+          }
+        }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      const double out = __dadd_rn(part, B2[m]);
-      const double lg = __dadd_rn(__dmul_rn(out, SD[m]), MU[m]);
-      acc = (m == 0) ? lg : __dadd_rn(acc, lg);
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < kRU; ++u) part[u] += __shfl_xor_sync(0xffffffffu, part[u], o);
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const int m = m0 + u;
+        if (m < e.k) {
+          const double out = __dadd_rn(part[u], __ldg(e.b2 + m));
+          const double lg = __dadd_rn(__dmul_rn(out, __ldg(e.std_ + m)), __ldg(e.mean + m));
+          acc = (m == 0) ? lg : __dadd_rn(acc, lg);
+        }
+      }
     }
     if (lane == 0) pred[t] = exp(__ddiv_rn(acc, (double)e.k));
   }

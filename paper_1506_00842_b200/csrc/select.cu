@@ -61,10 +61,45 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
     }
     return;
   }
-  uint32_t N = 1;
-  while (N < n) N <<= 1;
   unsigned long long* key = sk;
   long long* ix = reinterpret_cast<long long*>(sk + kSmallSort);
+  if (n <= (uint32_t)kRankSort) {
+    // Rank sort: (prediction, index) pairs are distinct (indices are), so the
+    // rank of an entry -- how many entries precede it -- is its position. One
+    // pass of broadcast shared-memory reads, two barriers (a bitonic network
+    // over n = 256 takes 36 barrier-separated passes).
+    for (uint32_t e = tid; e < n; e += blockDim.x) {
+      key[e] = (unsigned long long)__double_as_longlong(pred[e]);
+      ix[e] = idx[e];
+    }
+    __syncthreads();
+    const uint32_t take = min((uint32_t)m, n);
+    for (uint32_t e0 = 0; e0 < n; e0 += blockDim.x) {
+      const uint32_t e = e0 + tid;
+      const unsigned long long ke = e < n ? key[e] : 0ull;
+      const long long ie = e < n ? ix[e] : 0ll;
+      uint32_t rank = 0;
+      for (uint32_t u = 0; u < n; ++u) {
+        const unsigned long long ku = key[u];
+        rank += (ku < ke || (ku == ke && ix[u] < ie)) ? 1u : 0u;
+      }
+      if (e < n && rank < take) {
+        out_pred[rank] = __longlong_as_double((long long)ke);
+        out_idx[rank] = ie;
+      }
+    }
+    for (uint32_t e = take + tid; e < (uint32_t)m; e += blockDim.x) {   // padded past `take`
+      out_pred[e] = __longlong_as_double(0x7ff0000000000000ll);
+      out_idx[e] = INT64_MAX;
+    }
+    if (tid == 0) {
+      status[0] = 0;
+      status[1] = take;
+    }
+    return;
+  }
+  uint32_t N = 1;
+  while (N < n) N <<= 1;
   for (uint32_t e = tid; e < N; e += blockDim.x) {
     key[e] = e < n ? (unsigned long long)__double_as_longlong(pred[e]) : 0x7ff0000000000000ull;
     ix[e] = e < n ? idx[e] : INT64_MAX;
