@@ -147,10 +147,12 @@ MLT_API int64_t mlt_ctx_launches(mlt_ctx* ctx);
  *                     with the same slice shape; 0 = rebuild them on every call (what a
  *                     fresh ensemble costs; bench.py times the headline step this way).  */
 #define MLT_OPT_TABLE_CACHE 6
-/*   MLT_OPT_HALF_ITEMS  1 = sweep with two CTAs per SM, each owning half a work item;
- *                     0 = one CTA per SM owning whole items; -1 (default) = half items
- *                     when the slice is shallower than a few waves of whole items.    */
+/*   MLT_OPT_HALF_ITEMS  1 = sweep with two CTAs per SM, each owning half a work item
+ *                     (no tail launch); 0 (default) = one CTA per SM on whole items.
+ *   MLT_OPT_TAIL_SPLIT  1 (default) = the items of the last, partial wave of the sweep
+ *                     run in a second launch split into quarter items; 0 = off.        */
 #define MLT_OPT_HALF_ITEMS 7
+#define MLT_OPT_TAIL_SPLIT 8
 MLT_API int mlt_ctx_set_option(mlt_ctx* ctx, int key, int64_t value);
 
 /* A1: values[n][P] = decode(idx[n]).                 paramspace.py:184-193 */

@@ -15,6 +15,7 @@ import atexit
 import ctypes as C
 import os
 import threading
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -25,7 +26,7 @@ _LIB_PATH = Path(os.environ.get("MLTUNE_B200_LIB", Path(__file__).resolve().pare
 
 MLT_OK, MLT_EINVAL, MLT_EMISMATCH, MLT_EDATA, MLT_EDIVERGED, MLT_ECUDA, MLT_EINTERNAL = 0, -1, -2, -3, -4, -5, -6
 (MLT_OPT_PATH, MLT_OPT_GROUP, MLT_OPT_CAND_CAP, MLT_OPT_PRUNE, MLT_OPT_CHUNK, MLT_OPT_TABLE_CACHE,
- MLT_OPT_HALF_ITEMS) = 1, 2, 3, 4, 5, 6, 7
+ MLT_OPT_HALF_ITEMS, MLT_OPT_TAIL_SPLIT) = 1, 2, 3, 4, 5, 6, 7, 8
 RULE_KIND = {"max-product": 0, "max-weighted-sum": 1, "forbidden-combination": 2}
 
 _i32p = C.POINTER(C.c_int32)
@@ -235,6 +236,7 @@ class Plan:
         self.h = C.c_void_p()
         check(lib().mlt_plan_create(self.ctx, C.byref(self.ps.c), C.byref(self.pe.c), C.byref(self.h)),
               "mlt_plan_create")
+        _live_plans.add(self)
 
     def destroy(self):
         if self.h:
@@ -251,6 +253,7 @@ class Plan:
 
 
 _plan_cache: dict[tuple, tuple] = {}
+_live_plans: "weakref.WeakSet[Plan]" = weakref.WeakSet()   # shutdown() frees these before the contexts
 _PLAN_CACHE_MAX = 8
 
 
@@ -317,9 +320,8 @@ def shutdown() -> None:
     (compute-sanitizer's leak check sees no leftovers); ctx() after this
     creates fresh contexts."""
     with _ctx_lock:
-        plans = [v[2] for v in _plan_cache.values()]
         _plan_cache.clear()
-    for p in plans:          # before their contexts go away
+    for p in list(_live_plans):   # cached or still held: before their contexts go away
         p.destroy()
     with _ctx_lock:
         items = list(_ctxs.items())

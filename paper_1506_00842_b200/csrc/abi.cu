@@ -64,7 +64,8 @@ struct mlt_ctx {
   int64_t launches = 0;
   int opt_path = -1, opt_group = -1, opt_prune = 0;
   int opt_table_cache = 1;            // MLT_OPT_TABLE_CACHE
-  int opt_half_items = -1;            // MLT_OPT_HALF_ITEMS (-1 = by slice depth)
+  int opt_half_items = 0;             // MLT_OPT_HALF_ITEMS
+  int opt_tail_split = 1;             // MLT_OPT_TAIL_SPLIT
   int64_t chunk = int64_t(1) << 27;   // configurations per sweep chunk (MLT_OPT_CHUNK)
   int64_t cand_cap = 1 << 20;
   std::vector<void*> slots = std::vector<void*>(32, nullptr);
@@ -853,7 +854,8 @@ int mlt_ctx_set_option(mlt_ctx* c, int key, int64_t value) {
     case MLT_OPT_PRUNE: c->opt_prune = value == 1 ? 1 : 0; return MLT_OK;
     case MLT_OPT_CHUNK: c->chunk = value < 0 ? (int64_t(1) << 27) : std::max<int64_t>(value, 4096); return MLT_OK;
     case MLT_OPT_TABLE_CACHE: c->opt_table_cache = value == 0 ? 0 : 1; return MLT_OK;
-    case MLT_OPT_HALF_ITEMS: c->opt_half_items = value < 0 ? -1 : (value ? 1 : 0); return MLT_OK;
+    case MLT_OPT_HALF_ITEMS: c->opt_half_items = value == 1 ? 1 : 0; return MLT_OK;
+    case MLT_OPT_TAIL_SPLIT: c->opt_tail_split = value == 0 ? 0 : 1; return MLT_OK;
     default: return fail(MLT_EINVAL, "unknown option %d", key);
   }
 }
@@ -1304,32 +1306,52 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     const size_t smem = sweep_smem(p->he.k, big ? kSBBig : kSB);
     if (smem > 227 * 1024) return fail(MLT_EINTERNAL, "sweep needs %zu B of shared memory", smem);
     using KF = void (*)(SweepArgs);
-#define MLT_KROW(SBV, PR, NTV) \
-  { k_sweep<1, PR, SBV, NTV>, k_sweep<2, PR, SBV, NTV>, k_sweep<3, PR, SBV, NTV>, k_sweep<4, PR, SBV, NTV> }
+#define MLT_KROW(SBV, PR, NTV, OB) \
+  { k_sweep<1, PR, SBV, NTV, OB>, k_sweep<2, PR, SBV, NTV, OB>, k_sweep<3, PR, SBV, NTV, OB>, \
+    k_sweep<4, PR, SBV, NTV, OB> }
     static const KF kerns[2][2][2][4] = {
-        {{MLT_KROW(kSB, false, kThreads), MLT_KROW(kSB, true, kThreads)},
-         {MLT_KROW(kSBBig, false, kThreads), MLT_KROW(kSBBig, true, kThreads)}},
-        {{MLT_KROW(kSB, false, kThreads / 2), MLT_KROW(kSB, true, kThreads / 2)},
-         {MLT_KROW(kSBBig, false, kThreads / 2), MLT_KROW(kSBBig, true, kThreads / 2)}}};
+        {{MLT_KROW(kSB, false, kThreads, kOB), MLT_KROW(kSB, true, kThreads, kOB)},
+         {MLT_KROW(kSBBig, false, kThreads, kOB), MLT_KROW(kSBBig, true, kThreads, kOB)}},
+        {{MLT_KROW(kSB, false, kThreads / 2, kOB), MLT_KROW(kSB, true, kThreads / 2, kOB)},
+         {MLT_KROW(kSBBig, false, kThreads / 2, kOB), MLT_KROW(kSBBig, true, kThreads / 2, kOB)}}};
+    static const KF tails[2][4] = {MLT_KROW(kSB, false, kThreads, kTailOBU), MLT_KROW(kSBBig, false, kThreads, kTailOBU)};
 #undef MLT_KROW
-    // Half-item CTAs (two per SM) when the slice is only a few waves of whole
-    // items deep: the last wave's stragglers then share their SM with nobody
-    // (1/8 of the 10^8 space, 5.2 waves: 0.73 -> 0.67 ms; whole-item CTAs stay
-    // ~2 % faster on deep slices). MLT_OPT_HALF_ITEMS forces either.
-    const int64_t whole_items = (int64_t)n_ob * n_ib;
-    const bool halves = c->opt_half_items >= 0 ? c->opt_half_items == 1
-                                               : whole_items < (int64_t)kHalfItemWaves * c->sms;
+    // Wave quantisation: whole items (8 outers x 2048 inners, one 1024-thread
+    // CTA per SM) run in full waves; the items of the last, partial wave go to
+    // a second TAIL launch that splits each into kOB / kTailOBU parts, so the
+    // step ends with a short round on many SMs instead of one item-time on a
+    // few (1/8 of the 10^8 space: 768 items = 5.2 waves). MLT_OPT_TAIL_SPLIT
+    // turns it off; MLT_OPT_HALF_ITEMS = 1 instead runs two 512-thread CTAs
+    // per SM on half items (the round-2 alternative, kept for A/B).
+    const int whole_items = n_ob * n_ib;
+    const bool halves = c->opt_half_items == 1;
     const int nt = halves ? kThreads / 2 : kThreads;
     KF kern = kerns[halves ? 1 : 0][big ? 1 : 0][prune ? 1 : 0][B.G - 1];
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem));
     nb = std::max(nb, 1);
-    const int64_t items = whole_items * (kThreads / nt);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)nb * c->sms));
+    const int slots = nb * c->sms;   // CTAs resident at once
+    int main_hi = whole_items;
+    if (!prune && !halves && c->opt_tail_split != 0 && whole_items > slots && whole_items % slots != 0)
+      main_hi = whole_items / slots * slots;
+    sa.item_lo = 0;
+    sa.item_hi = main_hi;
+    const int64_t units = (int64_t)main_hi * (kThreads / nt);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, slots));
     if (c->prof) CU(cudaEventRecord(c->ev[1], c->stream));
     kern<<<grid, nt, smem, c->stream>>>(sa);
     TRY(check_launch(c));
+    if (main_hi < whole_items) {
+      KF tk = tails[big ? 1 : 0][B.G - 1];
+      CU(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      SweepArgs ta2 = sa;
+      ta2.item_lo = main_hi;
+      ta2.item_hi = whole_items;
+      const int64_t tunits = (int64_t)(whole_items - main_hi) * (kOB / kTailOBU);
+      tk<<<(int)std::min<int64_t>(tunits, slots), kThreads, smem, c->stream>>>(ta2);
+      TRY(check_launch(c));
+    }
     if (c->prof) CU(cudaEventRecord(c->ev[2], c->stream));
     // Snapshot the sweep's counters (the band stage reuses gs[2..4]) and launch
     // the band stage right behind the sweep, without a host round trip: its

@@ -44,7 +44,7 @@ __global__ void k_surr_best_final(const SurrPart* part, int n, SurrPart* out);
 
 // ---- final guard-band stage (select.cu) ------------------------------------
 constexpr int kSmallSort = 8192;  // survivors sorted in one CTA's shared memory (128 KB)
-constexpr int kRankSort = 2048;   // ... by rank counting up to this many, bitonic above
+constexpr int kRankSort = 256;    // ... by rank counting up to this many, bitonic above
 __global__ void k_band_filter(const int64_t* cidx, const float* cval, const uint32_t* count_ptr, uint32_t cap, int m,
                               float band, int64_t* out_idx, float* out_val, uint32_t* out_n);
 __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint32_t* n_ptr, int m, double* out_pred,
@@ -82,7 +82,7 @@ __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 #endif
 constexpr int kDefaultGroup = MLT_DEFAULT_GROUP;   // units per shared reciprocal unless MLT_OPT_GROUP says otherwise
 constexpr int kSB = kThreads >= 512 ? 2 * kThreads : 1024;   // per-CTA guard-band candidate slots
-constexpr int kHalfItemWaves = 8;   // slices shallower than this many waves of whole items use half-item CTAs
+constexpr int kTailOBU = 2;   // outers per work unit in the tail launch (kOB / kTailOBU parts per item)
 constexpr int kSBBig = 8192;   // ... in the instance for large m (kMaxTopMSmall < m <= kMaxTopM)
 constexpr int kMaxTopMSmall = 1024;  // largest m of the default sweep instance
 constexpr int kMaxTopM = 4096;       // largest m served by the guard-band path (kSBBig instance)
@@ -96,6 +96,7 @@ struct SweepArgs {
   int64_t c_in, c_in_pad;       // inner cardinality (and padded to kThreads)
   int64_t o_lo;                 // outer index of ea block 0, row 0
   int n_ob, n_ib;               // outer blocks x inner blocks = work items
+  int item_lo, item_hi;         // the work items [item_lo, item_hi) of this launch (row-major over (ob, ib))
   int64_t begin, end;           // configuration range of this call
   float cst;                    // sum_m (b2*std + mean)/k - (#dummy units)
   float band;                   // 2*delta (rounded up)
@@ -160,7 +161,7 @@ __global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* 
 template <int G>
 __global__ void k_table_inner(TableArgs t);
 
-template <int G, bool PRUNE, int SB, int NT>
+template <int G, bool PRUNE, int SB, int NT, int OBU>
 __global__ void k_sweep(SweepArgs a);
 size_t sweep_smem(int k, int sb);
 

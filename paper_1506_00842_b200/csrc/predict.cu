@@ -178,9 +178,14 @@ __global__ void __launch_bounds__(256) k_rescore_warp(DEns e, const int64_t* __r
 #pragma unroll
     for (int p = kMaxP - 1; p >= 0; --p) {
       if (p < e.d) {
-        const uint64_t c = (uint64_t)e.counts[p];
-        const uint64_t q = r / c;
-        x[p] = (double)(r - q * c) / (double)(e.counts[p] > 1 ? e.counts[p] - 1 : 1);
+        const uint32_t c = (uint32_t)e.counts[p];
+        uint64_t q;
+        if (r <= 0xffffffffull) {   // 32-bit division (the 64-bit one is a ~60-instruction call)
+          q = (uint32_t)r / c;
+        } else {
+          q = r / c;
+        }
+        x[p] = (double)(r - q * c) / (double)(c > 1 ? c - 1 : 1);
         r = q;
       } else {
         x[p] = 0.0;

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
     const uint32_t take = min((uint32_t)m, n);
     for (uint32_t e0 = 0; e0 < n; e0 += blockDim.x) {
       const uint32_t e = e0 + tid;
+      if (e0 + (tid & ~31u) >= n) break;   // whole warp past the end: skip the O(n) scan
       const unsigned long long ke = e < n ? key[e] : 0ull;
       const long long ie = e < n ? ix[e] : 0ll;
       uint32_t rank = 0;

@@ -339,16 +339,26 @@ __device__ __forceinline__ void load_group(const float4* pe, const float* pu, fl
 // One group of G units for all kInner x kOB configurations of the thread:
 // d' = exp(-A')*(exp(-B')/w') + 1/w' (FFMA2 over an outer pair), the G-term
 // rational combination, two reciprocals, one accumulate.
-template <int G>
-__device__ __forceinline__ void group_step(f2 (&acc)[kInner][kOB / 2], const float* E,
+// OBU: the outers of the item this thread evaluates (kOB, or a part of the
+// item in the tail launch); E points at the first of them in each unit row.
+template <int G, int OBU>
+__device__ __forceinline__ void group_step(f2 (&acc)[kInner][OBU / 2], const float* E,
                                            const float (&eb)[kInner][G], const float (&uu)[G]) {
+  static_assert(OBU == 2 || OBU % 4 == 0, "outers per part: 2 or a multiple of 4");
 #pragma unroll
-  for (int q = 0; q < kOB / 4; ++q) {
+  for (int q = 0; q < (OBU + 3) / 4; ++q) {
     float4 ea[G];
 #pragma unroll
-    for (int x = 0; x < G; ++x) ea[x] = *reinterpret_cast<const float4*>(E + x * kOB + 4 * q);
+    for (int x = 0; x < G; ++x) {
+      if (OBU >= 4) {
+        ea[x] = *reinterpret_cast<const float4*>(E + x * kOB + 4 * q);
+      } else {
+        const float2 t = *reinterpret_cast<const float2*>(E + x * kOB);
+        ea[x] = make_float4(t.x, t.y, 0.f, 0.f);
+      }
+    }
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
+    for (int half = 0; half < (OBU >= 4 ? 2 : 1); ++half) {
 #pragma unroll
       for (int s = 0; s < kInner; ++s) {
         f2 d[G];
@@ -430,12 +440,19 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (layout threads [h*NT, h*NT + NT) of the inner block; same per-thread work
 // and table layout): used for short slices, where the last wave of whole
 // items would leave SMs idle -- a straggler CTA then has its SM to itself.
-template <int G, bool PRUNE, int SB, int NT>
+//
+// OBU: outers per work unit. kOB = whole items; smaller in the TAIL launch,
+// which splits the last, partial wave's items into kOB / OBU parts so that
+// wave ends with a short round instead of a full item-time on a few SMs.
+template <int G, bool PRUNE, int SB, int NT, int OBU>
 __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepArgs a) {
   // SB: per-CTA candidate slots (kSB; kSBBig for m > kMaxTopMSmall)
   constexpr int kSB = SB;
   constexpr int kSBLimit = SB * 3 / 4;
-  constexpr int HALVES = kThreads / NT;   // CTA work units per item
+  constexpr int HALVES = kThreads / NT;   // CTA work units per item (inner halves)
+  constexpr int PARTS = kOB / OBU;        // ... (outer parts)
+  constexpr int SUB = HALVES * PARTS;
+  static_assert(!PRUNE || OBU == kOB, "the pruned sweep works on whole items");
   static_assert(kEbStages == 0 || NT == kThreads, "the cp.async factor ring assumes whole-item CTAs");
   extern __shared__ __align__(16) unsigned char smraw[];
   const int KH = a.k * kH;
@@ -457,8 +474,8 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
     s_th = *reinterpret_cast<volatile uint32_t*>(a.g_theta);
   }
   const int ngroups = KH / G;
-  const int n_items = a.n_ob * a.n_ib * HALVES;   // CTA work units
-  constexpr int kV = kInner * kOB;   // configurations per thread per work item (32)
+  const int n_items = (a.item_hi - a.item_lo) * SUB;   // CTA work units of this launch
+  constexpr int kV = kInner * OBU;   // configurations per thread per work unit (16)
 
   __shared__ __align__(16) float s_cr[kOB * kMaxCk];   // pruning: cst + remaining-unit lower bound per outer, checkpoint
   // pruning makes work items uneven: they are handed out dynamically then
@@ -476,7 +493,8 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
     // pruning visits work items best-first (ascending lower bound of their
     // mean log time), so the threshold reaches its final value within the first wave
     const int half = HALVES == 1 ? 0 : w % HALVES;
-    const int wi = PRUNE ? __ldg(a.item_order + w / HALVES) : w / HALVES;
+    const int part = PARTS == 1 ? 0 : (w / HALVES) % PARTS;
+    const int wi = PRUNE ? __ldg(a.item_order + w / SUB) : a.item_lo + w / SUB;
     const int ob = wi / a.n_ib, ib = wi - ob * a.n_ib;
     const int tl = half * NT + tid;   // this thread's column of the item's (layout) thread block
     __syncthreads();
@@ -526,7 +544,7 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
       const int wn = w + (int)gridDim.x;
       pf_ob = -1;
       if (wn < n_items) {
-        const int obn = wn / HALVES / a.n_ib;
+        const int obn = (a.item_lo + wn / SUB) / a.n_ib;
         if (obn == ob) {
           pf_ob = ob;
           pf_buf = cur;
@@ -544,17 +562,17 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
     const int64_t ibase = (int64_t)ib * kInnerBlock + tl;      // inner s is ibase + s*kThreads
     bool pruned = false;   // this WARP's configurations are all provably above the threshold
     int done = ngroups;    // groups this warp evaluated
-    f2 acc[kInner][kOB / 2];
+    f2 acc[kInner][OBU / 2];
 #pragma unroll
     for (int s = 0; s < kInner; ++s)
 #pragma unroll
-      for (int q = 0; q < kOB / 2; ++q) acc[s][q] = 0ull;
+      for (int q = 0; q < OBU / 2; ++q) acc[s][q] = 0ull;
 
     constexpr int W = ebw_of(G);
     const size_t gstride = (size_t)kThreads * W;   // float4s per group
     const float4* pe = reinterpret_cast<const float4*>(a.ebp) + ((size_t)ib * ngroups * kThreads + tl) * W;
     const float* pu = s_u;                   // 1/w' of the current group
-    const float* E = s_cur;                  // exp(-A') rows of the current group
+    const float* E = s_cur + part * OBU;     // exp(-A') rows of the current group (this part's outers)
     if (kEbStages > 0) {
       // Each thread streams ITS OWN factors through a private cp.async ring
       // kEbStages groups ahead: the L2 latency hides behind kEbStages-1 groups
@@ -593,7 +611,7 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
           for (int s2 = 0; s2 < kInner; ++s2) eb[s2][x] = f[x * kInner + s2];
           uu[x] = pu[x];
         }
-        group_step<G>(acc, E, eb, uu);
+        group_step<G, OBU>(acc, E, eb, uu);
         pu += G;
         E += G * kOB;
       }
@@ -625,7 +643,7 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
 #pragma unroll
           for (int s2 = 0; s2 < kInner; ++s2)
 #pragma unroll
-            for (int q = 0; q < kOB / 2; ++q) {
+            for (int q = 0; q < OBU / 2; ++q) {
               float lo, hi;
               upk(acc[s2][q], lo, hi);
               above = above && (lo + cr[2 * q] > thf) && (hi + cr[2 * q + 1] > thf);
@@ -643,21 +661,21 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
         // memory), so the prefetch of group gi + 2 on the last pair reads
         // valid memory it never uses, and odd group counts end below.
         if (gi + 1 >= ngroups) {
-          group_step<G>(acc, E, ebA, uA);
+          group_step<G, OBU>(acc, E, ebA, uA);
           break;
         }
         load_group<G>(pe + gstride, pu + G, ebB, uB);
-        group_step<G>(acc, E, ebA, uA);
+        group_step<G, OBU>(acc, E, ebA, uA);
         load_group<G>(pe + 2 * gstride, pu + 2 * G, ebA, uA);
-        group_step<G>(acc, E + G * kOB, ebB, uB);
+        group_step<G, OBU>(acc, E + G * kOB, ebB, uB);
 #else
         const bool has_b = gi + 1 < ngroups;
         load_group<G>(has_b ? pe + gstride : pe, has_b ? pu + G : pu, ebB, uB);
-        group_step<G>(acc, E, ebA, uA);
+        group_step<G, OBU>(acc, E, ebA, uA);
         if (!has_b) break;
         const bool has_c = gi + 2 < ngroups;
         load_group<G>(has_c ? pe + 2 * gstride : pe, has_c ? pu + 2 * G : pu, ebA, uA);
-        group_step<G>(acc, E + G * kOB, ebB, uB);
+        group_step<G, OBU>(acc, E + G * kOB, ebB, uB);
 #endif
         pe += 2 * gstride;
         pu += 2 * G;
@@ -677,21 +695,21 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
 #pragma unroll
     for (int s = 0; s < kInner; ++s)
 #pragma unroll
-      for (int q = 0; q < kOB / 2; ++q) {
-        upk(acc[s][q], v[s * kOB + 2 * q], v[s * kOB + 2 * q + 1]);
-        v[s * kOB + 2 * q] += a.cst;
-        v[s * kOB + 2 * q + 1] += a.cst;
+      for (int q = 0; q < OBU / 2; ++q) {
+        upk(acc[s][q], v[s * OBU + 2 * q], v[s * OBU + 2 * q + 1]);
+        v[s * OBU + 2 * q] += a.cst;
+        v[s * OBU + 2 * q + 1] += a.cst;
       }
-    const int64_t obase = a.o_lo + (int64_t)ob * kOB;
+    const int64_t obase = a.o_lo + (int64_t)ob * kOB + part * OBU;
     auto cfg_index = [&](int b) -> int64_t {
-      return (obase + (b % kOB)) * a.c_in + ibase + (b / kOB) * kThreads;
+      return (obase + (b % OBU)) * a.c_in + ibase + (b / OBU) * kThreads;
     };
     uint32_t mask = 0;
     {
       const float thf = fkey_inv(s_th);
 #pragma unroll
       for (int b = 0; b < kV; ++b) {
-        const int64_t i = ibase + (b / kOB) * kThreads;
+        const int64_t i = ibase + (b / OBU) * kThreads;
         const int64_t idx = cfg_index(b);
         const bool in = i < a.c_in && idx >= a.begin && idx < a.end;
         if (in && !(PRUNE && pruned) && !(v[b] > thf)) mask |= 1u << b;   // NaN passes (never silently dropped)
@@ -832,37 +850,45 @@ template __global__ void k_table_inner<1>(TableArgs t);
 template __global__ void k_table_inner<2>(TableArgs t);
 template __global__ void k_table_inner<3>(TableArgs t);
 template __global__ void k_table_inner<4>(TableArgs t);
-template __global__ void k_sweep<1, false, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<2, false, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<3, false, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<4, false, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<1, true, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<2, true, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<3, true, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<4, true, kSB, kThreads>(SweepArgs a);
-template __global__ void k_sweep<1, false, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<2, false, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<3, false, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<4, false, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<1, true, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<2, true, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<3, true, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<4, true, kSBBig, kThreads>(SweepArgs a);
-template __global__ void k_sweep<1, false, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<2, false, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<3, false, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<4, false, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<1, true, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<2, true, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<3, true, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<4, true, kSB, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<1, false, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<2, false, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<3, false, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<4, false, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<1, true, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<2, true, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<3, true, kSBBig, kThreads / 2>(SweepArgs a);
-template __global__ void k_sweep<4, true, kSBBig, kThreads / 2>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSB, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSBBig, kThreads, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSB, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<2, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<3, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<4, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
 
 }  // namespace mlt

@@ -21,6 +21,8 @@ if os.environ.get("MLT_GROUP"):
     N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_GROUP, int(os.environ["MLT_GROUP"])))
 if os.environ.get("MLT_HALF"):
     N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_HALF_ITEMS, int(os.environ["MLT_HALF"])))
+if os.environ.get("MLT_TAIL"):
+    N.check(N.lib().mlt_ctx_set_option(c, N.MLT_OPT_TAIL_SPLIT, int(os.environ["MLT_TAIL"])))
 if os.environ.get("MLT_PRUNE") == "1":
     N.check(N.lib().mlt_ctx_set_option(c, 4, 1))
 ps, pe = N.packed(sp, "space"), N.packed(ens, "ensemble")
@@ -38,6 +40,6 @@ for r in range(reps + 2):
         tot.append(st.total_ms)
 g = np.load(G / f"topm_{case}.npz")
 ok = bool(np.array_equal(oi[:on.value], g["m200_i"])) if "m200_i" in g.files and P == 1 else None
-print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "prune": os.environ.get("MLT_PRUNE") == "1", "slice": P, "half": os.environ.get("MLT_HALF", "auto"), "sweep_ms_min": min(sw),
+print(json.dumps({"lib": os.environ.get("MLTUNE_B200_LIB", "default"), "prune": os.environ.get("MLT_PRUNE") == "1", "slice": P, "half": os.environ.get("MLT_HALF", "0"), "tail": os.environ.get("MLT_TAIL", "1"), "sweep_ms_min": min(sw),
                   "sweep_ms_med": float(np.median(sw)), "total_ms_med": float(np.median(tot)),
                   "parity": ok, "group": st.group, "cands": st.candidates, "evaluated_frac": st.evaluated_frac, "raw": st.raw_candidates, "delta": st.delta}))
