@@ -1314,15 +1314,19 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
          {MLT_KROW(kSBBig, false, kThreads, kOB), MLT_KROW(kSBBig, true, kThreads, kOB)}},
         {{MLT_KROW(kSB, false, kThreads / 2, kOB), MLT_KROW(kSB, true, kThreads / 2, kOB)},
          {MLT_KROW(kSBBig, false, kThreads / 2, kOB), MLT_KROW(kSBBig, true, kThreads / 2, kOB)}}};
-    static const KF tails[2][4] = {MLT_KROW(kSB, false, kThreads, kTailOBU), MLT_KROW(kSBBig, false, kThreads, kTailOBU)};
+    static const KF tails[2][2][4] = {{MLT_KROW(kSB, false, kThreads, 2), MLT_KROW(kSBBig, false, kThreads, 2)},
+                                      {MLT_KROW(kSB, false, kThreads, 4), MLT_KROW(kSBBig, false, kThreads, 4)}};
 #undef MLT_KROW
     // Wave quantisation: whole items (8 outers x 2048 inners, one 1024-thread
-    // CTA per SM) run in full waves; the items of the last, partial wave go to
-    // a second TAIL launch that splits each into kOB / kTailOBU parts, so the
-    // step ends with a short round on many SMs instead of one item-time on a
-    // few (1/8 of the 10^8 space: 768 items = 5.2 waves). MLT_OPT_TAIL_SPLIT
-    // turns it off; MLT_OPT_HALF_ITEMS = 1 instead runs two 512-thread CTAs
-    // per SM on half items (the round-2 alternative, kept for A/B).
+    // CTA per SM) run in full waves; when the items of the last, partial wave
+    // fit ONE round of quarter (else half) items, they go to a second TAIL
+    // launch split that way, so the step ends with a short round on many SMs
+    // instead of a whole item-time on a few (1/8 of the 10^8 space: 768 items
+    // = 5.2 waves, 28 left over: 0.734 -> 0.692 ms). A split needing several
+    // rounds of parts loses to the plain last wave (parts are less efficient
+    // than whole items), so it is not taken then. MLT_OPT_TAIL_SPLIT = 0 turns
+    // it off; MLT_OPT_HALF_ITEMS = 1 instead runs two 512-thread CTAs per SM
+    // on half items (the earlier alternative, kept for A/B).
     const int whole_items = n_ob * n_ib;
     const bool halves = c->opt_half_items == 1;
     const int nt = halves ? kThreads / 2 : kThreads;
@@ -1332,9 +1336,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem));
     nb = std::max(nb, 1);
     const int slots = nb * c->sms;   // CTAs resident at once
-    int main_hi = whole_items;
-    if (!prune && !halves && c->opt_tail_split != 0 && whole_items > slots && whole_items % slots != 0)
-      main_hi = whole_items / slots * slots;
+    int main_hi = whole_items, tail_obu = 0;
+    if (!prune && !halves && c->opt_tail_split != 0 && whole_items > slots && whole_items % slots != 0) {
+      const int rem = whole_items % slots;
+      tail_obu = rem * (kOB / 2) <= slots ? 2 : (rem * (kOB / 4) <= slots ? 4 : 0);
+      if (tail_obu) main_hi = whole_items - rem;
+    }
     sa.item_lo = 0;
     sa.item_hi = main_hi;
     const int64_t units = (int64_t)main_hi * (kThreads / nt);
@@ -1343,12 +1350,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     kern<<<grid, nt, smem, c->stream>>>(sa);
     TRY(check_launch(c));
     if (main_hi < whole_items) {
-      KF tk = tails[big ? 1 : 0][B.G - 1];
+      KF tk = tails[tail_obu == 2 ? 0 : 1][big ? 1 : 0][B.G - 1];
       CU(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       SweepArgs ta2 = sa;
       ta2.item_lo = main_hi;
       ta2.item_hi = whole_items;
-      const int64_t tunits = (int64_t)(whole_items - main_hi) * (kOB / kTailOBU);
+      const int64_t tunits = (int64_t)(whole_items - main_hi) * (kOB / tail_obu);
       tk<<<(int)std::min<int64_t>(tunits, slots), kThreads, smem, c->stream>>>(ta2);
       TRY(check_launch(c));
     }
@@ -1379,7 +1386,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     TRY(check_launch(c));
     // 2) fp64 rescoring of the survivors, one warp each (grid-stride over the
     //    device count; survivors are few, ~m, so 32 CTAs of 8 warps)
-    k_rescore_warp<<<64, 256, 0, c->stream>>>(p->de, ia, gs + 2, pa);
+    {
+      const size_t rsm = ((size_t)p->he.k * p->he.h + p->he.k) * 8;
+      if (rsm > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the rescoring kernel (%zu B)", rsm);
+      CU(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      k_rescore<<<2 * c->sms, 256, rsm, c->stream>>>(p->de, ia, gs + 2, pa);
+    }
     TRY(check_launch(c));
     // 3) sort by (prediction, index) in one CTA when small
     const int ssmem = 16 * kSmallSort;

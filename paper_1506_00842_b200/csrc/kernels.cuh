@@ -16,7 +16,7 @@ __global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, co
                             const float* band_v, float band_theta);
 __global__ void k_member_out64(DEns e, const double* feat, int64_t n, double* out);
 size_t predict64_smem(const DEns& e);
-__global__ void k_rescore_warp(DEns e, const int64_t* idx, const uint32_t* n_ptr, double* pred);
+__global__ void k_rescore(DEns e, const int64_t* idx, const uint32_t* n_ptr, double* pred);
 
 // ---- analytic surrogate device (surrogate.cu) -------------------------------
 struct DSurr {
@@ -82,7 +82,6 @@ __host__ __device__ constexpr int ebw_of(int G) { return (kInner * G + 3) / 4; }
 #endif
 constexpr int kDefaultGroup = MLT_DEFAULT_GROUP;   // units per shared reciprocal unless MLT_OPT_GROUP says otherwise
 constexpr int kSB = kThreads >= 512 ? 2 * kThreads : 1024;   // per-CTA guard-band candidate slots
-constexpr int kTailOBU = 2;   // outers per work unit in the tail launch (kOB / kTailOBU parts per item)
 constexpr int kSBBig = 8192;   // ... in the instance for large m (kMaxTopMSmall < m <= kMaxTopM)
 constexpr int kMaxTopMSmall = 1024;  // largest m of the default sweep instance
 constexpr int kMaxTopM = 4096;       // largest m served by the guard-band path (kSBBig instance)

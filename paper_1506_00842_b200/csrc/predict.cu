@@ -160,71 +160,57 @@ size_t predict64_smem(const DEns& e) {
 
 namespace mlt {
 
-// Guard-band rescoring: one warp per candidate; lane j evaluates hidden unit j
-// of every member, each member output is a warp reduction. The per-unit and
-// per-member rounding sequence is k_predict64's (out*std + mean, member
-// order, /k, exp). The members' chains are independent: they run kRU at a
-// time (the exp / divide latencies overlap), weights straight from L2 (a
-// survivor reads its 53 KB once; no per-CTA staging of the whole ensemble).
-__global__ void __launch_bounds__(256) k_rescore_warp(DEns e, const int64_t* __restrict__ idx,
-                                                      const uint32_t* __restrict__ n_ptr, double* __restrict__ pred) {
-  constexpr int kRU = 4;
+// Guard-band rescoring (fp64, the reference's per-member arithmetic): one CTA
+// per survivor. The CTA decodes the configuration once (a thread per
+// parameter), evaluates all k*h hidden units in parallel (a unit per thread:
+// z = x.W1 + b1, w2 * sigmoid(z)), sums each member's units, de-standardises
+// (out*std + mean) and adds the members in member order, /k, exp -- the
+// k_predict64 sequence; only the order of the h-term sums differs (as it
+// does between any two BLAS dgemv builds). Survivors are few (~m), so the
+// latency of one survivor is what counts: its dependent chain here is one
+// unit plus two short reductions, not k units in a row.
+__global__ void __launch_bounds__(256) k_rescore(DEns e, const int64_t* __restrict__ idx,
+                                                 const uint32_t* __restrict__ n_ptr, double* __restrict__ pred) {
+  extern __shared__ double s_dyn[];   // [k*h] unit terms, [k] member logs
+  __shared__ double s_x[kMaxP];
+  double* s_term = s_dyn;
+  double* s_lg = s_dyn + (size_t)e.k * e.h;
   const uint32_t n = *n_ptr;
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (uint32_t t = blockIdx.x * wpb + (threadIdx.x >> 5); t < n; t += gridDim.x * wpb) {
-    uint64_t r = (uint64_t)idx[t];
-    double x[kMaxP];
-#pragma unroll
-    for (int p = kMaxP - 1; p >= 0; --p) {
-      if (p < e.d) {
-        const uint32_t c = (uint32_t)e.counts[p];
-        uint64_t q;
-        if (r <= 0xffffffffull) {   // 32-bit division (the 64-bit one is a ~60-instruction call)
-          q = (uint32_t)r / c;
-        } else {
-          q = r / c;
-        }
-        x[p] = (double)(r - q * c) / (double)(c > 1 ? c - 1 : 1);
-        r = q;
-      } else {
-        x[p] = 0.0;
-      }
+  const int tid = threadIdx.x;
+  const int nh = e.k * e.h;
+  for (uint32_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (tid < e.d) {   // digit of parameter tid: (idx / stride) % count, last parameter fastest
+      uint64_t stride = 1;
+      for (int q = e.d - 1; q > tid; --q) stride *= (uint64_t)e.counts[q];
+      const uint64_t id = (uint64_t)idx[t];
+      const uint64_t c = (uint64_t)e.counts[tid];
+      const uint64_t dig = ((id | stride) <= 0xffffffffull ? (uint64_t)((uint32_t)id / (uint32_t)stride) : id / stride) % c;
+      s_x[tid] = (double)dig / (double)(c > 1 ? c - 1 : 1);
     }
-    double acc = 0.0;
-    for (int m0 = 0; m0 < e.k; m0 += kRU) {
-      double part[kRU];
+    __syncthreads();
+    for (int u = tid; u < nh; u += blockDim.x) {
+      const double* w = e.w1 + (size_t)u * e.d;
+      double z = 0.0;
 #pragma unroll
-      for (int u = 0; u < kRU; ++u) {
-        part[u] = 0.0;
-        const int m = m0 + u;
-        if (m < e.k) {
-          for (int j = lane; j < e.h; j += 32) {
-            const double* w = e.w1 + ((size_t)m * e.h + j) * e.d;
-            double z = 0.0;
-#pragma unroll
-            for (int p = 0; p < kMaxP; ++p)
-              if (p < e.d) z = fma(x[p], __ldg(w + p), z);
-            z = __dadd_rn(z, __ldg(e.b1 + m * e.h + j));
-            part[u] = fma(1.0 / (1.0 + exp(-z)), __ldg(e.w2 + m * e.h + j), part[u]);
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int u = 0; u < kRU; ++u) part[u] += __shfl_xor_sync(0xffffffffu, part[u], o);
-#pragma unroll
-      for (int u = 0; u < kRU; ++u) {
-        const int m = m0 + u;
-        if (m < e.k) {
-          const double out = __dadd_rn(part[u], __ldg(e.b2 + m));
-          const double lg = __dadd_rn(__dmul_rn(out, __ldg(e.std_ + m)), __ldg(e.mean + m));
-          acc = (m == 0) ? lg : __dadd_rn(acc, lg);
-        }
-      }
+      for (int p = 0; p < kMaxP; ++p)
+        if (p < e.d) z = fma(s_x[p], __ldg(w + p), z);
+      z = __dadd_rn(z, __ldg(e.b1 + u));
+      s_term[u] = fma(1.0 / (1.0 + exp(-z)), __ldg(e.w2 + u), 0.0);
     }
-    if (lane == 0) pred[t] = exp(__ddiv_rn(acc, (double)e.k));
+    __syncthreads();
+    for (int mm = tid; mm < e.k; mm += blockDim.x) {
+      double out = 0.0;
+      for (int j = 0; j < e.h; ++j) out = __dadd_rn(out, s_term[mm * e.h + j]);
+      out = __dadd_rn(out, __ldg(e.b2 + mm));
+      s_lg[mm] = __dadd_rn(__dmul_rn(out, __ldg(e.std_ + mm)), __ldg(e.mean + mm));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double acc = s_lg[0];
+      for (int m = 1; m < e.k; ++m) acc = __dadd_rn(acc, s_lg[m]);
+      pred[t] = exp(__ddiv_rn(acc, (double)e.k));
+    }
+    __syncthreads();   // s_x / s_term are rewritten for the next survivor
   }
 }
 

@@ -4,7 +4,7 @@
 //   k_band_filter  one CTA: the exact m-th smallest fp32 mean log tau_m over all
 //                  candidates (radix select), then keep f32 <= tau_m + 2*delta.
 //                  Every configuration of the true top-m passes.
-//   k_rescore_warp (predict.cu) fp64 prediction of the survivors, one warp each.
+//   k_rescore      (predict.cu) fp64 prediction of the survivors, one CTA each.
 //   k_sort_small   one CTA: bitonic sort of <= kSmallSort (prediction, index)
 //                  pairs in shared memory and the first m written out; larger
 //                  survivor sets are sorted by the caller with CUB.
@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
       const unsigned long long ke = e < n ? key[e] : 0ull;
       const long long ie = e < n ? ix[e] : 0ll;
       uint32_t rank = 0;
+#pragma unroll 8
       for (uint32_t u = 0; u < n; ++u) {
         const unsigned long long ku = key[u];
         rank += (ku < ke || (ku == ke && ix[u] < ie)) ? 1u : 0u;

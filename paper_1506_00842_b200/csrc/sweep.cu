@@ -882,13 +882,21 @@ template __global__ void k_sweep<1, true, kSBBig, kThreads / 2, kOB>(SweepArgs a
 template __global__ void k_sweep<2, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
 template __global__ void k_sweep<3, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
 template __global__ void k_sweep<4, true, kSBBig, kThreads / 2, kOB>(SweepArgs a);
-template __global__ void k_sweep<1, false, kSB, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<2, false, kSB, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<3, false, kSB, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<4, false, kSB, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<1, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<2, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<3, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
-template __global__ void k_sweep<4, false, kSBBig, kThreads, kTailOBU>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads, 2>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSB, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSB, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSB, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSB, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<1, false, kSBBig, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<2, false, kSBBig, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<3, false, kSBBig, kThreads, 4>(SweepArgs a);
+template __global__ void k_sweep<4, false, kSBBig, kThreads, 4>(SweepArgs a);
 
 }  // namespace mlt

@@ -49,7 +49,7 @@ def _check_top(ens_case, space_name, m, lo, hi, **stats_want):
 
 
 def sweep_band():
-    """k_table_outer/inner + k_sweep<3,false> + k_band_filter + k_rescore_warp + k_sort_small."""
+    """k_table_outer/inner + k_sweep<3,false> + k_band_filter + k_rescore + k_sort_small."""
     _reset()
     st = _check_top("stereo_k8", "stereo", 50, 0, 1 << 18, path=0)
     return {"group": st["group"], "candidates": st["candidates"]}
