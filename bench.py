@@ -593,9 +593,13 @@ def main():
         sweep_s = t[1].item() / 1e3
         # the hot loop issues FFMA2/FMUL2/FADD2: its peak is the measured FFMA2 rate
         ffma_tflops = float(peaks.get("fp32_ffma2_tflops", 73.57))
-        lane_ops = k * H * {3: 8.0 / 3.0, 2: 2.5, 1: 2.0}.get(st.group, 8.0 / 3.0)   # FMA-pipe lane-ops/config
+        # FMA-pipe lane-ops and reciprocals per configuration of the sweep's
+        # algorithm: G units per reciprocal, 3 - 1/G lane-ops per unit
+        G = max(st.group, 1)
+        lane_ops = k * H * (3.0 - 1.0 / G)
+        rcp_per_config = k * H / G
         achieved = 2.0 * lane_ops * n_local / sweep_s / 1e12
-        mufu_rate = k * H / max(st.group, 1) * n_local / sweep_s   # reciprocals per second
+        mufu_rate = rcp_per_config * n_local / sweep_s   # reciprocals per second
         mufu_peak = float(peaks.get("mufu_rcp_gops", 4623.0)) * 1e9
         traffic = None
         tf = ROOT / "profiles" / "sweep_dram_bytes.json"
@@ -616,6 +620,8 @@ def main():
                          "peak_source": "measured FFMA2 rate (tools/pipe_peaks on this GPU; MEASURED_PEAKS.json "
                                         "has no FP32 figure)" if "source" not in peaks else peaks["source"],
                          "mufu_frac": mufu_rate / mufu_peak,
+                         "work_per_config": {"fma_pipe_lane_ops": lane_ops, "reciprocals": rcp_per_config,
+                                             "group": G},
                          "sweep_ms_per_launch": t[1].item(),
                          "naive_sec8d_tflops": flops_per_config(k, d) * n_local / sweep_s / 1e12},
             "candidates_rescored": int(np.mean(cands)),

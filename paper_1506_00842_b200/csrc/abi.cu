@@ -423,7 +423,7 @@ struct BandSetup {
   double delta = 0, cst = 0;
   double mag = 0;               // sum |w'| + dummies + |cst|: scale of every partial sum
   double* d_tab = nullptr;      // [ca | cb | wprime] (k*kH each)
-  float* d_u = nullptr;         // [k*kH] 1/w'
+  std::vector<float> u;         // [k*kH] 1/w' (the sweep's parameter block, SweepArgs::uc)
 };
 }  // namespace
 
@@ -496,6 +496,10 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   b.c_in_pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
 
   const int KH = e.k * kH;
+  if (KH > kMaxUnitsParam) {
+    b.why = "more hidden units than the sweep's parameter block holds";
+    return MLT_OK;
+  }
   std::vector<double> tab(3 * (size_t)KH, 0.0);
   double* ca = tab.data();
   double* cb = ca + KH;
@@ -589,9 +593,8 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
 
   mlt_ctx* c = p->ctx;
   CU(cudaMallocAsync(&b.d_tab, tab.size() * 8, c->stream));
-  CU(cudaMallocAsync(&b.d_u, (size_t)KH * 4, c->stream));
   TRY(upload_pinned(c, b.d_tab, tab.data(), tab.size() * 8));
-  TRY(upload_pinned(c, b.d_u, u.data(), (size_t)KH * 4));
+  b.u = std::move(u);
   b.ok = true;
   return MLT_OK;
 }
@@ -606,7 +609,6 @@ int get_setup(mlt_plan* p, int split, BandSetup** out) {
     const int rc = band_setup(p, split, b);
     if (rc != MLT_OK) {
       pool_free(p->ctx, b.d_tab);
-      pool_free(p->ctx, b.d_u);
       return rc;
     }
     it = p->setups.emplace(key, b).first;
@@ -730,7 +732,6 @@ void plan_free(mlt_plan* p) {
   pool_free(c, p->d_unit_of);
   for (auto& kv : p->setups) {
     pool_free(c, kv.second.d_tab);
-    pool_free(c, kv.second.d_u);
   }
   p->setups.clear();
   pool_free(c, p->t_ea);
@@ -1275,7 +1276,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     sa.k = p->he.k;
     sa.ea = ea;
     sa.ebp = ebp;
-    sa.u = B.d_u;
+    std::copy(B.u.begin(), B.u.end(), sa.uc);
     sa.c_in = B.c_in;
     sa.c_in_pad = B.c_in_pad;
     sa.o_lo = o_lo;

@@ -63,13 +63,6 @@ __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint3
 #ifndef MLT_MINB
 #define MLT_MINB 1
 #endif
-#ifndef MLT_NOSEL
-#define MLT_NOSEL 1   // sweep loop without per-pair bounds selects (padded tables)
-#endif
-#ifndef MLT_EBS
-#define MLT_EBS 0
-#endif
-constexpr int kEbStages = MLT_EBS;  // cp.async ring depth for the per-thread exp(-B')/w' factors (0 = LDG ping-pong)
 constexpr int kThreads = MLT_THREADS;   // threads per sweep CTA
 constexpr int kInner = MLT_INNER;   // inner configurations per thread (share every exp(-A') load)
 constexpr int kInnerBlock = kThreads * kInner;   // inner configurations per work item
@@ -86,12 +79,12 @@ constexpr int kSBBig = 8192;   // ... in the instance for large m (kMaxTopMSmall
 constexpr int kMaxTopMSmall = 1024;  // largest m of the default sweep instance
 constexpr int kMaxTopM = 4096;       // largest m served by the guard-band path (kSBBig instance)
 constexpr int kMaxCk = 32;      // pruning checkpoints per work item
+constexpr int kMaxUnitsParam = 4096;   // k*kH (+ 2 groups of padding) the sweep's parameter block holds
 
 struct SweepArgs {
   int k;                        // members
   const float* ea;              // [n_ob][k*kH][kOB]  exp(-A') of outer configurations
   const float* ebp;             // [n_ib][group][thread][4*ebw] exp(-B') / w' of inner configurations
-  const float* u;               // [k*kH]             1 / w'
   int64_t c_in, c_in_pad;       // inner cardinality (and padded to kThreads)
   int64_t o_lo;                 // outer index of ea block 0, row 0
   int n_ob, n_ib;               // outer blocks x inner blocks = work items
@@ -117,6 +110,10 @@ struct SweepArgs {
   unsigned long long* g_work;   // pruning: groups evaluated, summed over work items
   int* g_next;                  // pruning: next work item (dynamic distribution)
   DSpace sp;
+  // 1/w' of every table position (+ padding), read through the constant bank:
+  // the sweep's FFMA2s take it as a uniform-register operand, which costs no
+  // vector register-file bank read (kernel parameter space, per launch).
+  float uc[kMaxUnitsParam];
 };
 
 // Tables of the factored first layer (sweep.cu).

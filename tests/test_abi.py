@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(raw, name), name
     assert set(N.EXPORTS) == declared_symbols()
-    assert lib.mlt_abi_version() == 1
+    assert lib.mlt_abi_version() == N.ABI_VERSION == 1
 
 
 def test_library_targets_sm100a():
