@@ -1112,7 +1112,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       // every 2.5 % of the units from 20 % to 95 % (A/B on the 10^8 case: 5 % steps
       // from 25 % 2.676 ms, 2.5 % from 10 % 2.661, this schedule 2.649)
       for (int f = 8; f <= 38 && ck.n < kMaxCk; ++f) {
-        const int g = (int)((int64_t)f * ngroups / 40) / 2 * 2;
+        const int g = (int)((int64_t)f * ngroups / 40) / kSweepStep * kSweepStep;
         if (g > 0 && g < ngroups && (ck.n == 0 || g > ck_group[ck.n - 1])) {
           ck_group[ck.n] = g;
           ck.unit[ck.n] = g * B.G;

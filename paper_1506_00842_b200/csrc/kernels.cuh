@@ -79,6 +79,7 @@ constexpr int kSBBig = 8192;   // ... in the instance for large m (kMaxTopMSmall
 constexpr int kMaxTopMSmall = 1024;  // largest m of the default sweep instance
 constexpr int kMaxTopM = 4096;       // largest m served by the guard-band path (kSBBig instance)
 constexpr int kMaxCk = 32;      // pruning checkpoints per work item
+constexpr int kSweepStep = 3;   // groups per trip of the sweep's inner loop (checkpoints sit on multiples)
 constexpr int kMaxUnitsParam = 4096;   // k*kH (+ 2 groups of padding) the sweep's parameter block holds
 
 struct SweepArgs {

@@ -371,20 +371,21 @@ __device__ __forceinline__ void group_step(f2 (&acc)[OBU], const float* E, const
       }
     }
 #pragma unroll
-    for (int o = 0; o < NO; o += 2) {
-      // two outers at a time, unit-major: the two FFMA2s of a unit share eb / 1/w'
-      f2 d[2][G];
+    {
+      // the outers of one exp(-A') load, unit-major: the FFMA2s of a unit share
+      // eb / 1/w' (2 at a time: 4.90 ms; 4 at a time: 4.79 ms on the 10^8 case)
+      f2 d[NO][G];
 #pragma unroll
       for (int x = 0; x < G; ++x)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) d[j][x] = ffma2(eb[x], pk(ea[x][o + j], ea[x][o + j]), pk(a.uc[ug + x], a.uc[ug + x]));
+        for (int j = 0; j < NO; ++j) d[j][x] = ffma2(eb[x], pk(ea[x][j], ea[x][j]), pk(a.uc[ug + x], a.uc[ug + x]));
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < NO; ++j) {
         f2 num, den;
         combine<G>(d[j], num, den);
         float d0, d1;
         upk(den, d0, d1);
-        f2& ac = acc[4 * q + o + j];
+        f2& ac = acc[4 * q + j];
         const f2 r = pk(rcpa(d0), rcpa(d1));
         ac = (G == 1) ? fadd2(ac, r) : ffma2(num, r, ac);
       }
@@ -578,14 +579,20 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
     int ug = 0;                              // first unit of the current group (1/w': a.uc[ug + x])
     const float* E = s_cur + part * OBU;     // exp(-A') rows of the current group (this part's outers)
     {
-      // Two register sets (A, B) ping-pong so the next group's per-thread factors
-      // are in flight from L2 while the current group computes, with no copies.
-      f2 ebA[G], ebB[G];
+      // Three register sets (A, B, C) rotate so the next two groups' per-thread
+      // factors are in flight from L2 while the current group computes. (With
+      // two sets ptxas hoists the reload of a set above its last use and
+      // renames through ~10 IMAD.MOVs per loop trip on the FMA pipe: 4.79 ->
+      // 4.62 ms.) Pruning checkpoints sit on multiples of kSweepStep groups.
+      // (Loading the next trip's 1/w' one trip ahead: ptxas sinks the LDCUs to
+      // the loop end anyway, 4.75 ms.)
+      static_assert(kSweepStep == 3, "the loop below steps three groups");
+      f2 ebA[G], ebB[G], ebC[G];
       load_group<G>(pe, ebA);
       int ck = PRUNE ? 1 : 0;     // checkpoint 0 was decided before staging
       uint32_t gth = PRUNE ? *reinterpret_cast<volatile uint32_t*>(a.g_theta) : 0u;
 #pragma unroll 1
-      for (int gi = 0; gi < ngroups; gi += 2) {
+      for (int gi = 0; gi < ngroups; gi += kSweepStep) {
         if (PRUNE && ck < a.n_ck && gi == a.ck_group[ck]) {
           // Every configuration of this warp provably above the threshold? The
           // decision is per warp (no block barrier): a warp whose 32 x kV
@@ -615,20 +622,28 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
             break;
           }
         }
-        // No bounds selects: the tables carry one group of padding past the
-        // end (ebp allocation), so the prefetch of group gi + 2 on the last
-        // pair reads valid memory it never uses, and odd group counts end below.
+        // No bounds selects: the tables carry padding groups past the end
+        // (ebp allocation), so the prefetches of groups gi + 1 / gi + 2 / gi + 3
+        // near the end read valid memory they never use; group counts that are
+        // not multiples of 3 end below.
         if (gi + 1 >= ngroups) {
           group_step<G, OBU>(acc, E, ebA, a, ug);
           break;
         }
         load_group<G>(pe + gstride, ebB);
+        if (gi + 2 >= ngroups) {
+          group_step<G, OBU>(acc, E, ebA, a, ug);
+          group_step<G, OBU>(acc, E + G * kOB, ebB, a, ug + G);
+          break;
+        }
+        load_group<G>(pe + 2 * gstride, ebC);
         group_step<G, OBU>(acc, E, ebA, a, ug);
-        load_group<G>(pe + 2 * gstride, ebA);
+        load_group<G>(pe + 3 * gstride, ebA);
         group_step<G, OBU>(acc, E + G * kOB, ebB, a, ug + G);
-        pe += 2 * gstride;
-        ug += 2 * G;
-        E += 2 * G * kOB;
+        group_step<G, OBU>(acc, E + 2 * G * kOB, ebC, a, ug + 2 * G);
+        pe += 3 * gstride;
+        ug += 3 * G;
+        E += 3 * G * kOB;
       }
     }
 
