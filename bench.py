@@ -551,7 +551,9 @@ def main():
     import copy
     e2e_api = (lambda e: D.top_m_predicted(e, space, M_TOP)) if world > 1 else \
         (lambda e: T.top_m_predicted(e, space, M_TOP))
-    for _ in range(max(2, args.warmup)):
+    # warm-up beyond the plan cache's capacity: the device pool has grown to
+    # its steady state (evicted plans' blocks are reused) before timing starts
+    for _ in range(max(args.warmup, N._PLAN_CACHE_MAX + 2)):
         e2e_api(copy.copy(ens))
     torch.cuda.synchronize()
     if world > 1:

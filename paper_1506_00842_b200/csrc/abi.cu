@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -76,12 +77,16 @@ struct mlt_ctx {
   void* stage = nullptr;        // pinned staging ring for plan uploads (weights, value tables)
   size_t stage_cap = 0;
   size_t stage_off = 0;         // next free byte of the ring
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_switch = nullptr;   // orders work across mlt_ctx_set_stream
   // Serialises every entry point on this context (workspace slots, pinned
   // staging and the stream are per-context state): concurrent callers of one
   // context queue instead of racing. Recursive: mlt_top_m -> mlt_plan_create.
   std::recursive_mutex mu;
+  // kernel -> (dynamic shared memory last granted, resident CTAs per SM at it):
+  // the attribute call and the occupancy query cost host microseconds on every
+  // step otherwise, while the GPU waits for the step's first kernel
+  std::map<const void*, std::pair<size_t, int>> kattr;
 };
 
 namespace {
@@ -154,6 +159,23 @@ int upload_pinned(mlt_ctx* c, void* dst, const void* src, size_t bytes) {
 int check_launch(mlt_ctx* c) {
   c->launches++;
   CU(cudaGetLastError());
+  return MLT_OK;
+}
+
+// Grant `kern` `smem` bytes of dynamic shared memory (once per size) and
+// return its resident CTAs per SM at `threads` threads.
+template <typename K>
+int kernel_smem(mlt_ctx* c, K* kern, int threads, size_t smem, int* nb_out = nullptr) {
+  const void* key = reinterpret_cast<const void*>(kern);
+  auto it = c->kattr.find(key);
+  if (it == c->kattr.end() || it->second.first != smem) {
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
+    c->kattr[key] = {smem, nb};
+    it = c->kattr.find(key);
+  }
+  if (nb_out) *nb_out = it->second.second;
   return MLT_OK;
 }
 
@@ -1153,7 +1175,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     }
     ea = p->t_ea;
     ebp = p->t_ebp;
-    TRY(ws_t(c, S_GSCAL, 8, &gs));
+    TRY(ws_t(c, S_GSCAL, 16, &gs));
     TRY(ws_t(c, S_CIDX, (size_t)c->cand_cap, &cidx));
     TRY(ws_t(c, S_CVAL, (size_t)c->cand_cap, &cval));
     TableArgs ta;
@@ -1177,12 +1199,10 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.n_ob = n_ob;
     ta.ea = ea;
     ta.ebp = ebp;
-    uint32_t* hs = static_cast<uint32_t*>(c->pinned);
-    // gs[0] theta key, [1] candidate count, [2..3] band-stage counters, [4..5]
-    // pruning work (64-bit), [6] pruning: next work item, [7] unused: all 8 set
-    // so the end-of-step 32-byte read-back never copies uninitialised memory
+    // gs[0] theta key, [1] candidate count, [2..4] band-stage counters (n,
+    // status, take), [8..9] pruning work (64-bit), [10] pruning: next work item
     {
-      uint32_t init[8] = {0xFF800000u, 0, 0, 0, 0, 0, 0, 0};   // [0] = fkey(+inf)
+      uint32_t init[16] = {0xFF800000u};   // [0] = fkey(+inf), the rest 0
       TRY(upload_pinned(c, gs, init, sizeof init));   // the ring: safe with no host wait behind it
     }
     if (!tables_cached) {
@@ -1300,8 +1320,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     // fp32 rounding of T = acc + (cst + remlo): a few ulps of the largest partial sum
     sa.prune_eps = (float)(16.0 * std::ldexp(1.0, -23) * (B.mag + 1.0));
     sa.item_order = p->t_order;
-    sa.g_work = reinterpret_cast<unsigned long long*>(gs + 4);
-    sa.g_next = reinterpret_cast<int*>(gs + 6);
+    sa.g_work = reinterpret_cast<unsigned long long*>(gs + 8);
+    sa.g_next = reinterpret_cast<int*>(gs + 10);
     sa.sp = p->ds;
     const bool big = m > kMaxTopMSmall;   // the instance with kSBBig candidate slots per CTA
     const size_t smem = sweep_smem(p->he.k, big ? kSBBig : kSB);
@@ -1332,9 +1352,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     const bool halves = c->opt_half_items == 1;
     const int nt = halves ? kThreads / 2 : kThreads;
     KF kern = kerns[halves ? 1 : 0][big ? 1 : 0][prune ? 1 : 0][B.G - 1];
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int nb = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem));
+    TRY(kernel_smem(c, kern, nt, smem, &nb));
     nb = std::max(nb, 1);
     const int slots = nb * c->sms;   // CTAs resident at once
     int main_hi = whole_items, tail_obu = 0;
@@ -1352,7 +1371,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     TRY(check_launch(c));
     if (main_hi < whole_items) {
       KF tk = tails[tail_obu == 2 ? 0 : 1][big ? 1 : 0][B.G - 1];
-      CU(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      TRY(kernel_smem(c, tk, kThreads, smem));
       SweepArgs ta2 = sa;
       ta2.item_lo = main_hi;
       ta2.item_hi = whole_items;
@@ -1365,10 +1384,6 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     // the band stage right behind the sweep, without a host round trip: its
     // buffers are sized for the candidate capacity and its kernels read the
     // candidate count on the device. One host wait at the end of the step.
-    if (!d_rec) {
-      CU(cudaMemcpyAsync(hs + 8, gs, 8, cudaMemcpyDeviceToHost, c->stream));            // theta, count
-      if (prune) CU(cudaMemcpyAsync(hs + 10, gs + 4, 8, cudaMemcpyDeviceToHost, c->stream));   // work
-    }
     const uint32_t cap = (uint32_t)std::min<int64_t>(c->cand_cap, UINT32_MAX);
     const size_t cap1 = std::max<size_t>(cap, 1);
     double *pa, *pb, *tp;
@@ -1390,14 +1405,28 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     {
       const size_t rsm = ((size_t)p->he.k * p->he.h + p->he.k) * 8;
       if (rsm > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the rescoring kernel (%zu B)", rsm);
-      CU(cudaFuncSetAttribute(k_rescore, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      TRY(kernel_smem(c, k_rescore, 256, rsm));
       k_rescore<<<2 * c->sms, 256, rsm, c->stream>>>(p->de, ia, gs + 2, pa);
     }
     TRY(check_launch(c));
     // 3) sort by (prediction, index) in one CTA when small
-    const int ssmem = 16 * kSmallSort;
-    CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
-    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3);
+    //    (sized for 4m survivors: the band keeps m + a few; more -> CUB below)
+    const int scap = sort_small_cap(4 * m), ssmem = 16 * scap;
+    TRY(kernel_smem(c, k_sort_small, 1024, ssmem));
+    // the host-output step: the sort writes the result and the counters straight
+    // into pinned host memory (mapped, UVA), so no copy follows the kernels
+    const size_t res_bytes = 64 + (size_t)m * 16;
+    if (!d_rec && c->res_cap < res_bytes) {
+      if (c->res_pin) CU(cudaFreeHost(c->res_pin));
+      c->res_pin = nullptr;
+      c->res_cap = 0;
+      CU(cudaHostAlloc(&c->res_pin, res_bytes, cudaHostAllocMapped));
+      c->res_cap = res_bytes;
+    }
+    uint32_t* hres = d_rec ? nullptr : static_cast<uint32_t*>(c->res_pin);
+    uint32_t* dres = nullptr;
+    if (hres) CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), hres, 0));
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3, scap, dres, gs);
     TRY(check_launch(c));
     if (d_rec) {   // device record: pack and return without waiting
       k_pack_record<<<1, 256, 0, c->stream>>>(tp, ti, gs, cap, (int)m, d_rec);
@@ -1409,25 +1438,15 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       *out_n = -1;
       return MLT_OK;
     }
-    if (c->res_cap < (size_t)m * 16) {
-      if (c->res_pin) CU(cudaFreeHost(c->res_pin));
-      c->res_pin = nullptr;
-      c->res_cap = 0;
-      CU(cudaMallocHost(&c->res_pin, (size_t)m * 16));
-      c->res_cap = (size_t)m * 16;
-    }
-    double* rp = static_cast<double*>(c->res_pin);
+    double* rp = reinterpret_cast<double*>(hres + 16);
     int64_t* ri = reinterpret_cast<int64_t*>(rp + m);
-    CU(cudaMemcpyAsync(rp, tp, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));   // valid when the
-    CU(cudaMemcpyAsync(ri, ti, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));   // one-CTA sort ran
-    CU(cudaMemcpyAsync(hs, gs, 32, cudaMemcpyDeviceToHost, c->stream));
+    if (c->prof) CU(cudaEventRecord(c->ev[4], c->stream));   // device work of the step done
     CU(cudaStreamSynchronize(c->stream));
-    const uint32_t theta_key = hs[8], count = hs[9];
-    (void)theta_key;
+    const uint32_t count = hres[1];
     local.evaluated_frac = 1.0;
     if (prune) {
       uint64_t work;
-      std::memcpy(&work, hs + 10, 8);
+      std::memcpy(&work, hres + 8, 8);
       local.evaluated_frac = (double)work / ((double)n_ob * n_ib * ngroups * (kThreads / 32));   // warp-groups
     }
     local.group = B.G;
@@ -1436,7 +1455,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     if ((int64_t)count > c->cand_cap) {
       band = false;   // crowded guard band: fall back to the exact materialising path
     } else {
-      const uint32_t n2 = hs[2], big = hs[3], take = hs[4];
+      const uint32_t n2 = hres[2], big = hres[3], take = hres[4];
       local.candidates = n2;
       if (!big) {   // the lists already landed in pinned memory with the counters
         const int64_t tk = std::min<int64_t>(m, take);
@@ -1459,6 +1478,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       float ms = 0;
       CU(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
       local.sweep_ms = ms;
+      if (std::getenv("MLT_STEP_TRACE")) {   // diagnostics: where the step's device time goes
+        float pre = 0, post = 0;
+        CU(cudaEventElapsedTime(&pre, c->ev[0], c->ev[1]));
+        CU(cudaEventElapsedTime(&post, c->ev[2], c->ev[4]));
+        std::fprintf(stderr, "{\"pre_sweep_ms\": %.4f, \"sweep_ms\": %.4f, \"band_stage_ms\": %.4f}\n", pre, ms, post);
+      }
     }
   }
   if (!band) {
@@ -1610,9 +1635,9 @@ int mlt_merge_records(mlt_ctx* c, const int64_t* d_recs, int64_t n_rec, int64_t 
       const uint32_t cnt = (uint32_t)n;
       TRY(upload_pinned(c, gs + 2, &cnt, 4));
     }
-    const int ssmem = 16 * kSmallSort;
-    CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
-    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)std::min<int64_t>(m, n), tp, ti, gs + 3);
+    const int scap = sort_small_cap(n), ssmem = 16 * scap;
+    TRY(kernel_smem(c, k_sort_small, 1024, ssmem));
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)std::min<int64_t>(m, n), tp, ti, gs + 3, scap);
     TRY(check_launch(c));
     TRY(emit_top(c, tp, ti, std::min(m, n), m, out_idx, out_pred, out_n));
   } else {
@@ -1744,9 +1769,9 @@ int mlt_merge_top_m(mlt_ctx* c, const int64_t* dev_idx, const double* dev_pred, 
     uint32_t* hs = static_cast<uint32_t*>(c->pinned);
     hs[2] = (uint32_t)n;
     CU(cudaMemcpyAsync(gs + 2, hs + 2, 4, cudaMemcpyHostToDevice, c->stream));
-    const int ssmem = 16 * kSmallSort;
-    CU(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
-    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)std::min<int64_t>(m, n), tp, ti, gs + 3);
+    const int scap = sort_small_cap(n), ssmem = 16 * scap;
+    TRY(kernel_smem(c, k_sort_small, 1024, ssmem));
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)std::min<int64_t>(m, n), tp, ti, gs + 3, scap);
     TRY(check_launch(c));
     return emit_top(c, tp, ti, std::min(m, n), m, out_idx, out_pred, out_n);
   }

@@ -49,45 +49,88 @@ __global__ void __launch_bounds__(1024) k_band_filter(const int64_t* __restrict_
 __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ pred, const int64_t* __restrict__ idx,
                                                      const uint32_t* __restrict__ n_ptr, int m,
                                                      double* __restrict__ out_pred, int64_t* __restrict__ out_idx,
-                                                     uint32_t* __restrict__ status) {
-  extern __shared__ unsigned long long sk[];     // [N] prediction bits, then [N] indices
+                                                     uint32_t* __restrict__ status, int cap,
+                                                     uint32_t* __restrict__ host_out, const uint32_t* __restrict__ gs) {
+  // cap: entries the launch's dynamic shared memory holds (a power of two <=
+  // kSmallSort, chosen by the host from m): a small launch keeps the SM's
+  // shared-memory carveout of the kernels around it (a 128 KB request forces
+  // a reconfiguration: 15 -> 3 us for m = 200)
+  // host_out (optional): pinned host memory the kernel writes the step's
+  // result into directly -- a 16-word header (gs[0..1] sweep threshold and
+  // candidate count, n, status, take, gs[8..9] pruning work) then m
+  // predictions and m indices -- so the host needs no copy after its one wait.
+  extern __shared__ unsigned long long sk[];     // [cap] prediction bits, then [cap] indices
   const uint32_t n = *n_ptr;
   const int tid = threadIdx.x;
-  if (n > (uint32_t)kSmallSort) {
+  auto mirror = [&](uint32_t big, uint32_t take) {
+    if (!host_out) return;
+    __syncthreads();   // out_pred / out_idx complete
+    double* hp = reinterpret_cast<double*>(host_out + 16);
+    long long* hi = reinterpret_cast<long long*>(hp + m);
+    for (int e = tid; e < m; e += blockDim.x) {
+      hp[e] = out_pred[e];
+      hi[e] = out_idx[e];
+    }
+    if (tid == 0) {
+      host_out[0] = gs[0];
+      host_out[1] = gs[1];
+      host_out[2] = n;
+      host_out[3] = big;
+      host_out[4] = take;
+      host_out[8] = gs[8];
+      host_out[9] = gs[9];
+    }
+  };
+  if (n > (uint32_t)cap) {
     if (tid == 0) status[0] = 1;                 // caller sorts with CUB
     for (int e = tid; e < m; e += blockDim.x) {  // defined padding (the host copies the
       out_pred[e] = __longlong_as_double(0x7ff0000000000000ll);   // lists unconditionally)
       out_idx[e] = INT64_MAX;
     }
+    mirror(1u, 0u);
     return;
   }
   unsigned long long* key = sk;
-  long long* ix = reinterpret_cast<long long*>(sk + kSmallSort);
+  long long* ix = reinterpret_cast<long long*>(sk + cap);
   if (n <= (uint32_t)kRankSort) {
     // Rank sort: (prediction, index) pairs are distinct (indices are), so the
-    // rank of an entry -- how many entries precede it -- is its position. One
-    // pass of broadcast shared-memory reads, two barriers (a bitonic network
-    // over n = 256 takes 36 barrier-separated passes).
+    // rank of an entry -- how many entries precede it -- is its position.
+    // Entries are stored as {key, index} so one broadcast LDS.128 reads one;
+    // four threads per entry each count a quarter of the entries, branch-free,
+    // and add into the entry's rank (a bitonic network over n = 256 takes 36
+    // barrier-separated passes; the first, one-thread-per-entry version with a
+    // short-circuit compare was latency-bound at ~30 us for n = 200).
+    static_assert(1024 % kRankSort == 0, "segments per entry");
+    constexpr uint32_t S = 1024 / kRankSort;
+    __shared__ uint32_t s_rank[kRankSort];
+    ulonglong2* kv = reinterpret_cast<ulonglong2*>(sk);
     for (uint32_t e = tid; e < n; e += blockDim.x) {
-      key[e] = (unsigned long long)__double_as_longlong(pred[e]);
-      ix[e] = idx[e];
+      kv[e] = make_ulonglong2((unsigned long long)__double_as_longlong(pred[e]), (unsigned long long)idx[e]);
+      s_rank[e] = 0;
     }
     __syncthreads();
     const uint32_t take = min((uint32_t)m, n);
-    for (uint32_t e0 = 0; e0 < n; e0 += blockDim.x) {
-      const uint32_t e = e0 + tid;
-      if (e0 + (tid & ~31u) >= n) break;   // whole warp past the end: skip the O(n) scan
-      const unsigned long long ke = e < n ? key[e] : 0ull;
-      const long long ie = e < n ? ix[e] : 0ll;
-      uint32_t rank = 0;
-#pragma unroll 8
-      for (uint32_t u = 0; u < n; ++u) {
-        const unsigned long long ku = key[u];
-        rank += (ku < ke || (ku == ke && ix[u] < ie)) ? 1u : 0u;
+    {
+      const uint32_t e = tid % kRankSort, sg = tid / kRankSort;
+      if (e < n) {
+        const ulonglong2 me = kv[e];
+        const uint32_t u0 = sg * n / S, u1 = (sg + 1) * n / S;
+        uint32_t r = 0;
+#pragma unroll 4
+        for (uint32_t u = u0; u < u1; ++u) {
+          const ulonglong2 o = kv[u];
+          r += (uint32_t)(o.x < me.x) | ((uint32_t)(o.x == me.x) & (uint32_t)((long long)o.y < (long long)me.y));
+        }
+        atomicAdd(&s_rank[e], r);
       }
-      if (e < n && rank < take) {
-        out_pred[rank] = __longlong_as_double((long long)ke);
-        out_idx[rank] = ie;
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < n; e += blockDim.x) {
+      const uint32_t rank = s_rank[e];
+      if (rank < take) {
+        const ulonglong2 me = kv[e];
+        out_pred[rank] = __longlong_as_double((long long)me.x);
+        out_idx[rank] = (long long)me.y;
       }
     }
     for (uint32_t e = take + tid; e < (uint32_t)m; e += blockDim.x) {   // padded past `take`
@@ -98,6 +141,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
       status[0] = 0;
       status[1] = take;
     }
+    mirror(0u, take);
     return;
   }
   uint32_t N = 1;
@@ -137,6 +181,7 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
     status[0] = 0;
     status[1] = take;
   }
+  mirror(0u, take);
 }
 
 }  // namespace mlt
