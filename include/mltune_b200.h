@@ -102,7 +102,8 @@ typedef struct mlt_ensemble {
 typedef struct mlt_sweep_stats {
   int64_t configs;             /* configurations swept */
   int64_t candidates;          /* guard-band candidates rescored in fp64 */
-  int32_t path;                /* 0 = fp32 sweep + fp64 guard band, 1 = fp64 materialise + sort */
+  int32_t path;                /* 0 = fp32 sweep + fp64 guard band, 1 = fp64 materialise + sort,
+                                  2 = constant ensemble (every configuration ties): first valid indices */
   int32_t group;               /* hidden units per reciprocal in the fp32 sweep (1..4) */
   double delta;                /* a-priori bound on |fp32 - fp64| mean log time */
   float sweep_ms;              /* device time of the sweep kernel (profiling on) */

@@ -466,6 +466,13 @@ struct mlt_plan {
   std::vector<int> unit_of;     // table position -> original unit m*kH + j
   int* d_unit_of = nullptr;
   std::map<int, BandSetup> setups;
+  // Every configuration gets the SAME prediction, bit for bit, in the
+  // reference's arithmetic: each hidden unit with a nonzero output weight has
+  // zero first-layer weights on every parameter with more than one value (and
+  // finite ones on the single-valued parameters, whose feature is 0), so
+  // z = b1 for every configuration (plan_create). The top-m is then the first
+  // m statically valid indices -- lexsort's tie order (run_constant).
+  bool constant = false;
   // Factored tables of the last band sweep: a derived, resident layout of the
   // weights for one (split, group, outer range); repeated sweeps of the same
   // slice with this plan reuse them instead of rebuilding.
@@ -780,6 +787,73 @@ int run_full(mlt_plan* p, int64_t m, int64_t begin, int64_t end, const int64_t* 
   return emit_top(c, pa, ia, n, m, out_idx, out_pred, out_n);
 }
 
+// Constant ensemble (mlt_plan::constant): every configuration ties, so the
+// reference's lexsort((indices, preds)) returns the first m statically valid
+// indices of the slice. Validity is evaluated chunk by chunk from `begin` and
+// the valid indices selected in order (CUB DeviceSelect over a counting
+// iterator) until m are found; the one prediction value is computed once by
+// the fp64 kernel. Replaces a guard band that holds every configuration (an
+// fp32 sweep + overflow + the fp64 materialising path: 350 ms on the 10^8
+// space) by a validity scan of the first ~m configurations.
+int run_constant(mlt_plan* p, int64_t m, int64_t begin, int64_t end, int64_t* out_idx, double* out_pred,
+                 int64_t* out_n) {
+  mlt_ctx* c = p->ctx;
+  std::vector<int64_t> found;
+  found.reserve(m);
+  const int64_t chunk = std::max<int64_t>(4 * m, int64_t(1) << 20);
+  void* fv;
+  int64_t *sel, *nsel;
+  TRY(ws(c, S_OUT_C, (size_t)chunk, &fv));
+  uint8_t* flags = static_cast<uint8_t*>(fv);
+  TRY(ws_t(c, S_OUT_D, (size_t)chunk + 1, &sel));
+  nsel = sel + chunk;
+  size_t tmp_bytes = 0;
+  CU(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, cub::CountingInputIterator<int64_t>(0), flags, sel, nsel,
+                                chunk, c->stream));
+  void* tmp;
+  TRY(ws(c, S_SORT_TMP, tmp_bytes, &tmp));
+  std::vector<int64_t> hsel;
+  for (int64_t lo = begin; lo < end && (int64_t)found.size() < m; lo += chunk) {
+    const int64_t n = std::min(chunk, end - lo);
+    int64_t ns = n;
+    if (p->ds.R > 0) {
+      k_valid_range<<<grid_for(c, n, 256), 256, 0, c->stream>>>(p->ds, lo, n, flags);
+      TRY(check_launch(c));
+      CU(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cub::CountingInputIterator<int64_t>(lo), flags, sel, nsel, n,
+                                    c->stream));
+      CU(cudaMemcpyAsync(&ns, nsel, 8, cudaMemcpyDeviceToHost, c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      const int64_t take = std::min<int64_t>(ns, m - (int64_t)found.size());
+      hsel.resize(take);
+      if (take > 0) {
+        CU(cudaMemcpyAsync(hsel.data(), sel, take * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+      }
+      found.insert(found.end(), hsel.begin(), hsel.end());
+    } else {
+      for (int64_t t = 0; t < n && (int64_t)found.size() < m; ++t) found.push_back(lo + t);
+    }
+  }
+  if (found.empty()) {
+    *out_n = 0;
+    return MLT_OK;
+  }
+  double* pv;
+  int64_t* iv;
+  TRY(ws_t(c, S_OUT_A, 1, &pv));
+  TRY(ws_t(c, S_OUT_B, 1, &iv));
+  TRY(launch_predict64(c, p->de, p->ds, 0, found[0], nullptr, nullptr, 1, pv, iv));
+  double v = 0;
+  CU(cudaMemcpyAsync(&v, pv, 8, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  for (size_t t = 0; t < found.size(); ++t) {
+    out_idx[t] = found[t];
+    out_pred[t] = v;
+  }
+  *out_n = (int64_t)found.size();
+  return MLT_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1048,6 +1122,21 @@ int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens,
                 p->hs.radix[q]);
   if (rc == MLT_OK) rc = plan_upload(p);
   if (rc == MLT_OK) rc = plan_factors(p);
+  if (rc == MLT_OK) {
+    const HostEns& e = p->he;
+    bool constant = true;
+    for (int u = 0; constant && u < e.k * e.h; ++u) {
+      if (e.w2()[u] == 0.0) continue;
+      for (int q = 0; q < e.d; ++q) {
+        const double w = e.w1()[(size_t)u * e.d + q];
+        if (p->hs.radix[q] >= 2 ? w != 0.0 : !std::isfinite(w)) {
+          constant = false;
+          break;
+        }
+      }
+    }
+    p->constant = constant;
+  }
   if (rc != MLT_OK) {
     plan_free(p);
     delete p;
@@ -1099,6 +1188,15 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
   }
   local.configs = n;
   if (n == 0) {
+    if (st) *st = local;
+    return MLT_OK;
+  }
+  if (p->constant && !idx_list && c->opt_path != 1) {
+    // every configuration ties (mlt_plan::constant): the first m valid indices
+    local.path = 2;
+    TRY(run_constant(p, m, begin, end, out_idx, out_pred, out_n));
+    local.candidates = *out_n;
+    local.launches = (int32_t)(c->launches - l0);
     if (st) *st = local;
     return MLT_OK;
   }

@@ -10,6 +10,7 @@ namespace mlt {
 // ---- exact fp64 kernels (predict.cu) --------------------------------------
 __global__ void k_decode(DSpace s, const int64_t* idx, int64_t n, int64_t* out);
 __global__ void k_valid(DSpace s, const int64_t* idx, int64_t n, uint8_t* out);
+__global__ void k_valid_range(DSpace s, int64_t lo, int64_t n, uint8_t* out);
 __global__ void k_encode(DEns e, const int64_t* idx, int64_t n, double* out);
 __global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, const int64_t* idx,
                             const double* feat, int64_t n, double* pred, int64_t* idx_out,

@@ -25,6 +25,16 @@ __global__ void k_valid(DSpace s, const int64_t* __restrict__ idx, int64_t n, ui
   }
 }
 
+// Static validity of the contiguous range [lo, lo + n) (for the order-preserving
+// selection of the first valid indices).
+__global__ void k_valid_range(DSpace s, int64_t lo, int64_t n, uint8_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    int dig[kMaxP];
+    decode_digits(s, (uint64_t)(lo + t), dig);
+    out[t] = rules_ok(s, dig) ? 1 : 0;
+  }
+}
+
 // feature = digit / max(count - 1, 1); IEEE division matches numpy bit-for-bit.
 __global__ void k_encode(DEns e, const int64_t* __restrict__ idx, int64_t n, double* __restrict__ out) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {

@@ -2,7 +2,7 @@
 ensembles so flat that the fp32 guard band holds far more configurations
 than the candidate buffer. For each case: the step time through the
 resident plan, the path taken (0 = fp32 sweep + guard band, 1 = exact fp64
-materialise + sort), candidate counts, and the top-m checked against the
+materialise + sort, 2 = constant ensemble: first valid indices), candidate counts, and the top-m checked against the
 device's exact fp64 path on the whole space (golden top-m where one exists).
 
     python tools/band_worst_case.py [--quick]      (GPU; one JSON line per case)
