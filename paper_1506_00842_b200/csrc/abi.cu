@@ -1345,7 +1345,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       TRY(check_launch(c));
       void (*tin)(TableArgs) = B.G == 4 ? k_table_inner<4>
                                : B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
-      tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads * 4 * ebw, 256), 256, 0, c->stream>>>(ta);
+      tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
       if (prune) {
         double* ext;
