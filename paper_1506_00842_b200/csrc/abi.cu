@@ -1324,14 +1324,16 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       TRY(ws_t(c, S_POL, (size_t)KH * nlo_o, &PoL));
       TRY(ws_t(c, S_PIH, (size_t)KH * nhi_i, &PiH));
       TRY(ws_t(c, S_PIL, (size_t)KH * nlo_i, &PiL));
-      k_table_partial<<<grid_for(c, (int64_t)KH * (he - hb), 256), 256, 0, c->stream>>>(ta, 0, sa_o, hb, he - hb, PoH);
-      TRY(check_launch(c));
-      k_table_partial<<<grid_for(c, (int64_t)KH * nlo_o, 256), 256, 0, c->stream>>>(ta, sa_o, B.split, 0, nlo_o, PoL);
-      TRY(check_launch(c));
-      k_table_partial<<<grid_for(c, (int64_t)KH * nhi_i, 256), 256, 0, c->stream>>>(ta, B.split, sa_i, 0, nhi_i, PiH);
-      TRY(check_launch(c));
-      k_table_partial<<<grid_for(c, (int64_t)KH * nlo_i, 256), 256, 0, c->stream>>>(ta, sa_i, p->hs.P, 0, nlo_i, PiL);
-      TRY(check_launch(c));
+      {
+        const PartialJobs jobs = {{0, sa_o, B.split, sa_i},
+                                  {sa_o, B.split, sa_i, p->hs.P},
+                                  {hb, 0, 0, 0},
+                                  {he - hb, nlo_o, nhi_i, nlo_i},
+                                  {PoH, PoL, PiH, PiL}};
+        const int64_t tot = (int64_t)KH * (he - hb + nlo_o + nhi_i + nlo_i);
+        k_table_partial4<<<grid_for(c, tot, 256), 256, 0, c->stream>>>(ta, jobs);
+        TRY(check_launch(c));
+      }
       ta.PoH = PoH;
       ta.PoL = PoL;
       ta.PiH = PiH;

@@ -153,7 +153,12 @@ struct TableArgs {
 };
 
 __global__ void k_table_factors(TableArgs t);
-__global__ void k_table_partial(TableArgs t, int p_lo, int p_hi, int64_t base, int64_t count, double* P);
+struct PartialJobs {             // k_table_partial4: four (parameter range, sub-index range) tables
+  int p_lo[4], p_hi[4];
+  int64_t base[4], count[4];
+  double* out[4];
+};
+__global__ void k_table_partial4(TableArgs t, PartialJobs j);
 __global__ void k_table_outer(TableArgs t);
 struct CkList {
   int n;

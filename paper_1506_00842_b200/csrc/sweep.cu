@@ -69,20 +69,26 @@ __device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int 
 //   P[mj][q] = prod_{p in [p_lo, p_hi)} F[mj][foff[p] + digit_p(base + q)]
 // where digits are those of the sub-index over [p_lo, p_hi) (last fastest).
 // Every table entry is then ca|cb * P_hi * P_lo: two fp64 multiplies.
-__global__ void k_table_partial(TableArgs t, int p_lo, int p_hi, int64_t base, int64_t count, double* __restrict__ P) {
+// The four partial-product tables of one build (outer hi / lo, inner hi / lo)
+// in ONE launch: each is a few tens of thousands of entries, so four launches
+// cost ~10 us each in launch latency and tails.
+__global__ void k_table_partial4(TableArgs t, PartialJobs j) {
   const int KH = t.k * kH;
-  const int fs = t.foff[t.d];
-  const int64_t total = (int64_t)KH * count;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int mj = (int)(q / count);
+  const int64_t tot = KH * (j.count[0] + j.count[1] + j.count[2] + j.count[3]);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
+    int r = 0;
+    int64_t off = q;
+    while (r < 3 && off >= KH * j.count[r]) off -= KH * j.count[r++];
+    const int64_t count = j.count[r];
+    const int mj = (int)(off / count);
     int dig[kMaxP];
-    sub_digits(t, (uint64_t)(base + q % count), p_lo, p_hi, dig);
-    const double* Fj = t.F + (size_t)mj * fs;
+    sub_digits(t, (uint64_t)(j.base[r] + off % count), j.p_lo[r], j.p_hi[r], dig);
+    const double* Fj = t.F + (size_t)mj * t.foff[t.d];
     double e = 1.0;
 #pragma unroll
     for (int p = 0; p < kMaxP; ++p)
-      if (p >= p_lo && p < p_hi) e *= __ldg(Fj + t.foff[p] + dig[p]);
-    P[q] = e;
+      if (p >= j.p_lo[r] && p < j.p_hi[r]) e *= __ldg(Fj + t.foff[p] + dig[p]);
+    j.out[r][off] = e;
   }
 }
 
