@@ -69,34 +69,42 @@ __device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int 
 //   P[mj][q] = prod_{p in [p_lo, p_hi)} F[mj][foff[p] + digit_p(base + q)]
 // where digits are those of the sub-index over [p_lo, p_hi) (last fastest).
 // Every table entry is then ca|cb * P_hi * P_lo: two fp64 multiplies.
-// The four partial-product tables of one build (outer hi / lo, inner hi / lo)
-// in ONE launch: each is a few tens of thousands of entries, so four launches
-// cost ~10 us each in launch latency and tails.
-__global__ void k_table_partial4(TableArgs t, PartialJobs j) {
-  const int KH = t.k * kH;
-  const int64_t tot = KH * (j.count[0] + j.count[1] + j.count[2] + j.count[3]);
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
-    int r = 0;
-    int64_t off = q;
-    while (r < 3 && off >= KH * j.count[r]) off -= KH * j.count[r++];
-    const int64_t count = j.count[r];
-    const int mj = (int)(off / count);
-    int dig[kMaxP];
-    sub_digits(t, (uint64_t)(j.base[r] + off % count), j.p_lo[r], j.p_hi[r], dig);
-    const double* Fj = t.F + (size_t)mj * t.foff[t.d];
-    double e = 1.0;
-#pragma unroll
-    for (int p = 0; p < kMaxP; ++p)
-      if (p >= j.p_lo[r] && p < j.p_hi[r]) e *= __ldg(Fj + t.foff[p] + dig[p]);
-    j.out[r][off] = e;
-  }
-}
-
 // x / d for non-negative operands, in 32 bits when both fit (a 64-bit
 // division is a ~60-instruction sequence; these index splits run per thread)
 __device__ __forceinline__ int64_t udiv(int64_t x, int64_t d) {
   return ((uint64_t)x | (uint64_t)d) <= 0xffffffffull ? (int64_t)((uint32_t)x / (uint32_t)d) : x / d;
 }
+
+// The four partial-product tables of one build (outer hi / lo, inner hi / lo)
+// in ONE launch: each is a few tens of thousands of entries, so four launches
+// cost ~10 us each in launch latency and tails.
+__global__ void k_table_partial4(TableArgs t, PartialJobs j) {
+  // (jobs are selected with compare chains, not by indexing the parameter
+  // arrays with a runtime index, which would copy them to local memory)
+  const int KH = t.k * kH;
+  const int64_t e0 = KH * j.count[0], e1 = e0 + KH * j.count[1], e2 = e1 + KH * j.count[2],
+                tot = e2 + KH * j.count[3];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
+    const int r = q < e0 ? 0 : (q < e1 ? 1 : (q < e2 ? 2 : 3));
+    const int64_t off = q - (r == 0 ? 0 : (r == 1 ? e0 : (r == 2 ? e1 : e2)));
+    const int64_t count = r == 0 ? j.count[0] : (r == 1 ? j.count[1] : (r == 2 ? j.count[2] : j.count[3]));
+    const int64_t base = r == 0 ? j.base[0] : (r == 1 ? j.base[1] : (r == 2 ? j.base[2] : j.base[3]));
+    const int p_lo = r == 0 ? j.p_lo[0] : (r == 1 ? j.p_lo[1] : (r == 2 ? j.p_lo[2] : j.p_lo[3]));
+    const int p_hi = r == 0 ? j.p_hi[0] : (r == 1 ? j.p_hi[1] : (r == 2 ? j.p_hi[2] : j.p_hi[3]));
+    double* out = r == 0 ? j.out[0] : (r == 1 ? j.out[1] : (r == 2 ? j.out[2] : j.out[3]));
+    const int64_t mj64 = udiv(off, count);
+    const int mj = (int)mj64;
+    int dig[kMaxP];
+    sub_digits(t, (uint64_t)(base + (off - mj64 * count)), p_lo, p_hi, dig);
+    const double* Fj = t.F + (size_t)mj * t.foff[t.d];
+    double e = 1.0;
+#pragma unroll
+    for (int p = 0; p < kMaxP; ++p)
+      if (p >= p_lo && p < p_hi) e *= __ldg(Fj + t.foff[p] + dig[p]);
+    out[off] = e;
+  }
+}
+
 
 // Outer table Ea[ob][mj][r], one thread per element in output order
 // (consecutive threads: consecutive outers of one position, so the PoH / PoL

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -489,7 +490,14 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
   }
   void (*kern)(TrainArgs, int) = pick_train(a.smem_rows != 0, D.d);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool trace = std::getenv("MLT_STEP_TRACE") != nullptr;   // diagnostics: upload / kernel split
+  cudaEvent_t tev[3];
+  if (trace) {
+    for (auto& ev : tev) cudaEventCreate(&ev);
+    cudaEventRecord(tev[0], stream);   // (uploads were enqueued before: time from the call start on host)
+  }
   kern<<<D.k, kTW * 32, smem, stream>>>(a, (int)ftab.size());
+  if (trace) cudaEventRecord(tev[1], stream);
   (*launches)++;
   e = cudaGetLastError();
   if (e == cudaSuccess) {
@@ -501,6 +509,13 @@ extern "C" int mlt_train_members_impl(int dev, cudaStream_t stream, int64_t* lau
     cudaMemcpyAsync(ll, oll, D.k * 8, cudaMemcpyDeviceToHost, stream);
     cudaMemcpyAsync(div, odiv, D.k * 4, cudaMemcpyDeviceToHost, stream);
     e = cudaStreamSynchronize(stream);
+  }
+  if (trace) {
+    float kms = 0;
+    cudaEventElapsedTime(&kms, tev[0], tev[1]);
+    std::fprintf(stderr, "{\"train_kernel_ms\": %.3f, \"steps_per_member\": %lld}\n", kms,
+                 (long long)D.epochs * ((D.n_m[0] + D.batch_size - 1) / D.batch_size));
+    for (auto& ev : tev) cudaEventDestroy(ev);
   }
   cudaFreeAsync(buf, stream);
   if (dcodes) cudaFreeAsync(dcodes, stream);
