@@ -73,6 +73,8 @@ struct mlt_ctx {
   std::vector<size_t> sizes = std::vector<size_t>(32, 0);
   void* pinned = nullptr;       // small pinned staging for scalars
   void* res_pin = nullptr;      // pinned landing zone of a step's top-m (prediction, index) lists
+  void* merge_pin = nullptr;    // ... and of a record merge (mlt_merge_records)
+  size_t merge_cap = 0;
   size_t res_cap = 0;
   void* stage = nullptr;        // pinned staging ring for plan uploads (weights, value tables)
   size_t stage_cap = 0;
@@ -398,19 +400,77 @@ __global__ void k_merge_prep(const int64_t* idx, const double* pred, int64_t n, 
   }
 }
 
-// One shard's top-m as an all-gather record (mlt_plan_top_m_record): gs = the
-// step's counters (gs[1] candidates, gs[3] / gs[4] k_sort_small's status / take).
-__global__ void k_pack_record(const double* tp, const int64_t* ti, const uint32_t* gs, uint32_t cap, int m,
-                              int64_t* rec) {
-  const uint32_t count = gs[1], big = gs[3], take = gs[4];
-  const int64_t status = count > cap ? 1 : (big ? 2 : 0);
-  const int tk = status ? 0 : (int)min(take, (uint32_t)m);
-  for (int t = threadIdx.x; t < m; t += blockDim.x) {
-    const bool ok = t < tk && ti[t] != INT64_MAX && ti[t] >= 0;
-    rec[t] = ok ? ti[t] : -1;
-    rec[m + t] = ok ? __double_as_longlong(tp[t]) : 0x7ff0000000000000ll;
+// One CTA merges n_rec sorted records (each: m indices -- -1 pads at the end
+// -- then m prediction bit patterns, then a status word) by RANK: entry i of
+// record r lands at position
+//   i + sum_{r' < r} #{e in r' : e <= x} + sum_{r' > r} #{e in r' : e < x}
+// in (prediction, index) order (equal entries ordered by record, so ranks are
+// distinct), found by binary searches over the records staged in shared
+// memory -- the records are already sorted, so no sort is needed. The first m
+// land in host-mapped memory ([0] count, [1] OR of the status words, then m
+// predictions and m indices), so the caller's single wait returns the answer.
+constexpr int kMergeMaxEntries = 8192;   // n_rec * m staged in shared memory (128 KB)
+constexpr int kMergeMaxRec = 256;
+__global__ void __launch_bounds__(1024) k_merge_records(const int64_t* __restrict__ recs, int n_rec, int m,
+                                                        int64_t* __restrict__ host_out) {
+  extern __shared__ unsigned long long sm_rec[];   // [n] prediction bits, then [n] indices
+  __shared__ int s_valid[kMergeMaxRec];
+  __shared__ unsigned long long s_status;
+  __shared__ int s_total;
+  const int n = n_rec * m, tid = threadIdx.x;
+  const int64_t stride = 2 * (int64_t)m + 1;
+  unsigned long long* kp = sm_rec;
+  long long* ki = reinterpret_cast<long long*>(sm_rec + n);
+  for (int r = tid; r < n_rec; r += blockDim.x) s_valid[r] = m;
+  if (tid == 0) {
+    s_status = 0;
+    s_total = 0;
   }
-  if (threadIdx.x == 0) rec[2 * m] = status;
+  __syncthreads();
+  for (int e = tid; e < n; e += blockDim.x) {
+    const int r = e / m, i = e - r * m;
+    const long long x = recs[r * stride + i];
+    kp[e] = (unsigned long long)recs[r * stride + m + i];
+    ki[e] = x;
+    if (x < 0) atomicMin(&s_valid[r], i);
+  }
+  for (int r = tid; r < n_rec; r += blockDim.x)
+    if (recs[r * stride + 2 * m] != 0) atomicOr(&s_status, (unsigned long long)recs[r * stride + 2 * m]);
+  __syncthreads();
+  for (int r = tid; r < n_rec; r += blockDim.x) atomicAdd(&s_total, s_valid[r]);
+  unsigned long long* hp = reinterpret_cast<unsigned long long*>(host_out + 2);
+  long long* hx = reinterpret_cast<long long*>(host_out + 2 + m);
+  for (int e = tid; e < n; e += blockDim.x) {
+    const int r = e / m, i = e - r * m;
+    if (i >= s_valid[r]) continue;
+    const unsigned long long p = kp[e];   // positive doubles: bit patterns order like the values
+    const long long x = ki[e];
+    int rank = i;
+    for (int r2 = 0; r2 < n_rec; ++r2) {
+      if (r2 == r) continue;
+      const bool le = r2 < r;           // earlier records win ties
+      int lo = 0, hi = s_valid[r2];
+      const int base = r2 * m;
+      while (lo < hi) {                 // first entry of r2 that comes after (p, x)
+        const int mid = (lo + hi) >> 1;
+        const unsigned long long q = kp[base + mid];
+        const long long y = ki[base + mid];
+        const bool before = q < p || (q == p && (le ? y <= x : y < x));
+        if (before) lo = mid + 1;
+        else hi = mid;
+      }
+      rank += lo;
+    }
+    if (rank < m) {
+      hp[rank] = p;
+      hx[rank] = x;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    host_out[0] = min(m, s_total);
+    host_out[1] = (long long)s_status;
+  }
 }
 
 // Gathered records -> (index, prediction) pairs for the merge sort; padding
@@ -906,6 +966,7 @@ int mlt_ctx_destroy(mlt_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->stage) cudaFreeHost(c->stage);
   if (c->res_pin) cudaFreeHost(c->res_pin);
+  if (c->merge_pin) cudaFreeHost(c->merge_pin);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->ev_switch) cudaEventDestroy(c->ev_switch);
@@ -1526,11 +1587,9 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     uint32_t* hres = d_rec ? nullptr : static_cast<uint32_t*>(c->res_pin);
     uint32_t* dres = nullptr;
     if (hres) CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), hres, 0));
-    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3, scap, dres, gs);
+    k_sort_small<<<1, 1024, ssmem, c->stream>>>(pa, ia, gs + 2, (int)m, tp, ti, gs + 3, scap, dres, gs, d_rec, cap);
     TRY(check_launch(c));
-    if (d_rec) {   // device record: pack and return without waiting
-      k_pack_record<<<1, 256, 0, c->stream>>>(tp, ti, gs, cap, (int)m, d_rec);
-      TRY(check_launch(c));
+    if (d_rec) {   // device record (written by the sort): return without waiting
       local.group = B.G;
       local.delta = B.delta;
       local.launches = (int32_t)(c->launches - l0);
@@ -1709,6 +1768,35 @@ int mlt_merge_records(mlt_ctx* c, const int64_t* d_recs, int64_t n_rec, int64_t 
   *out_status = 0;
   const int64_t n = n_rec * m;
   if (n == 0) return MLT_OK;
+  if (n <= kMergeMaxEntries && n_rec <= kMergeMaxRec) {
+    // one kernel: rank-merge of the sorted records straight into mapped host memory
+    const size_t bytes = (2 + 2 * (size_t)m) * 8;
+    if (c->merge_cap < bytes) {
+      if (c->merge_pin) CU(cudaFreeHost(c->merge_pin));
+      c->merge_pin = nullptr;
+      c->merge_cap = 0;
+      CU(cudaHostAlloc(&c->merge_pin, bytes, cudaHostAllocMapped));
+      c->merge_cap = bytes;
+    }
+    int64_t* hres = static_cast<int64_t*>(c->merge_pin);
+    int64_t* dres = nullptr;
+    CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), hres, 0));
+    const size_t smem = (size_t)n * 16;
+    TRY(kernel_smem(c, k_merge_records, 1024, smem));
+    k_merge_records<<<1, 1024, smem, c->stream>>>(d_recs, (int)n_rec, (int)m, dres);
+    TRY(check_launch(c));
+    CU(cudaStreamSynchronize(c->stream));
+    const int64_t cnt = hres[0];
+    const double* hp = reinterpret_cast<const double*>(hres + 2);
+    const int64_t* hx = hres + 2 + m;
+    for (int64_t t = 0; t < cnt; ++t) {
+      out_idx[t] = hx[t];
+      out_pred[t] = hp[t];
+    }
+    *out_n = cnt;
+    *out_status = hres[1];
+    return MLT_OK;
+  }
   double *pa, *pb;
   int64_t *ia, *ib;
   uint32_t* gs;

@@ -50,7 +50,7 @@ __global__ void k_band_filter(const int64_t* cidx, const float* cval, const uint
                               float band, int64_t* out_idx, float* out_val, uint32_t* out_n);
 __global__ void k_sort_small(const double* pred, const int64_t* idx, const uint32_t* n_ptr, int m, double* out_pred,
                              int64_t* out_idx, uint32_t* status, int cap, uint32_t* host_out = nullptr,
-                             const uint32_t* gs = nullptr);
+                             const uint32_t* gs = nullptr, int64_t* rec = nullptr, uint32_t cand_cap = 0);
 // entries of k_sort_small's shared buffer for at most n survivors (power of two, >= 256)
 inline int sort_small_cap(int64_t n) {
   int c = 256;

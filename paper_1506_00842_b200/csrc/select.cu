@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
                                                      const uint32_t* __restrict__ n_ptr, int m,
                                                      double* __restrict__ out_pred, int64_t* __restrict__ out_idx,
                                                      uint32_t* __restrict__ status, int cap,
-                                                     uint32_t* __restrict__ host_out, const uint32_t* __restrict__ gs) {
+                                                     uint32_t* __restrict__ host_out, const uint32_t* __restrict__ gs,
+                                                     int64_t* __restrict__ rec, uint32_t cand_cap) {
   // cap: entries the launch's dynamic shared memory holds (a power of two <=
   // kSmallSort, chosen by the host from m): a small launch keeps the SM's
   // shared-memory carveout of the kernels around it (a 128 KB request forces
@@ -62,7 +63,23 @@ __global__ void __launch_bounds__(1024) k_sort_small(const double* __restrict__ 
   extern __shared__ unsigned long long sk[];     // [cap] prediction bits, then [cap] indices
   const uint32_t n = *n_ptr;
   const int tid = threadIdx.x;
+  // rec (optional): the sharded step's device record (mlt_plan_top_m_record):
+  // m indices (-1 pads), m prediction bit patterns (+inf pads), status word
+  // (1 = the sweep's candidate buffer overflowed, 2 = too many survivors for
+  // this kernel; the caller's protocol redoes such a shard)
   auto mirror = [&](uint32_t big, uint32_t take) {
+    if (rec) {
+      __syncthreads();
+      const uint32_t count = gs[1];
+      const long long st = count > cand_cap ? 1 : (big ? 2 : 0);
+      const int tk = st ? 0 : (int)min(take, (uint32_t)m);
+      for (int t = tid; t < m; t += blockDim.x) {
+        const bool ok = t < tk && out_idx[t] != INT64_MAX && out_idx[t] >= 0;
+        rec[t] = ok ? out_idx[t] : -1;
+        rec[m + t] = ok ? __double_as_longlong(out_pred[t]) : 0x7ff0000000000000ll;
+      }
+      if (tid == 0) rec[2 * m] = st;
+    }
     if (!host_out) return;
     __syncthreads();   // out_pred / out_idx complete
     double* hp = reinterpret_cast<double*>(host_out + 16);

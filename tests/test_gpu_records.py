@@ -109,3 +109,32 @@ def test_records_protocol_single_rank_gloo(gpu_ok):
         assert np.array_equal(idx, g["m200_i"])
     finally:
         dist.destroy_process_group()
+
+
+def test_records_merge_ties_and_large_merges(gpu_ok):
+    """The rank merge orders equal predictions by index across records (a
+    constant ensemble: every configuration ties, the answer is the first m
+    valid indices); a merge beyond the one-CTA capacity (n_rec * m > 8192)
+    takes the sort path; both equal the single-call top-m."""
+    import torch
+    from paper_1506_00842_b200.model import Encoder, Ensemble, Network
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    sp = product_space("stereo")
+    rng = np.random.default_rng(3)
+    d = len(sp.params)
+    flat = Ensemble([Network(np.zeros((30, d)), rng.uniform(-1, 1, 30), rng.uniform(-1, 1, 30), 0.2, 1.0, 1.5)
+                     for _ in range(4)], Encoder.from_space(sp), sp.name)
+    for world, m in [(4, 300), (8, 100), (3, 1000)]:
+        out = _records(flat, sp, m, world, torch)
+        idx, pred, status = _merge(out, world, m)
+        ref = top_m_arrays(flat, sp, m)
+        assert status == 0
+        assert np.array_equal(idx, ref[0]) and np.array_equal(pred, ref[1]), (world, m)
+    ens = product_ensemble("stereo_k8")
+    for world, m in [(3, 3000), (2, 4096)]:
+        out = _records(ens, sp, m, world, torch)
+        idx, pred, status = _merge(out, world, m)
+        ref = top_m_arrays(ens, sp, m)
+        assert status == 0
+        assert np.array_equal(idx, ref[0]), (world, m)
+        np.testing.assert_allclose(pred, ref[1], rtol=1e-12, atol=0)

@@ -216,8 +216,8 @@ def predict_merge():
 
 
 def records():
-    """mlt_plan_top_m_record (k_pack_record behind the band stage) for 4 shards
-    + mlt_merge_records (k_merge_rec_prep + k_sort_small), and a forced
+    """mlt_plan_top_m_record (the record written by the band stage's sort kernel) for 4 shards
+    + mlt_merge_records (k_merge_records: one-CTA rank merge), and a forced
     overflow record."""
     import torch
     from paper_1506_00842_b200.distributed import shard_bounds
