@@ -1344,7 +1344,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.h = p->he.h;
     ta.split = B.split;
     ta.G = B.G;
-    for (int q = 0; q < p->hs.P; ++q) ta.radix[q] = p->hs.radix[q];
+    for (int q = 0; q < p->hs.P; ++q) {
+      ta.radix[q] = p->hs.radix[q];
+      ta.f_radix[q] = make_fdiv(p->hs.radix[q]);
+    }
+    ta.f_kh = make_fdiv(KH);
+    ta.f_ngroups = make_fdiv(KH / B.G);
     for (int q = 0; q <= p->hs.P; ++q) ta.foff[q] = p->foff[q];
     ta.w1 = p->de.w1;
     ta.F = p->d_F;
@@ -1390,6 +1395,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
                                   {sa_o, B.split, sa_i, p->hs.P},
                                   {hb, 0, 0, 0},
                                   {he - hb, nlo_o, nhi_i, nlo_i},
+                                  {make_fdiv(he - hb), make_fdiv(nlo_o), make_fdiv(nhi_i), make_fdiv(nlo_i)},
                                   {PoH, PoL, PiH, PiL}};
         const int64_t tot = (int64_t)KH * (he - hb + nlo_o + nhi_i + nlo_i);
         k_table_partial4<<<grid_for(c, tot, 256), 256, 0, c->stream>>>(ta, jobs);
@@ -1404,6 +1410,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       ta.o_hi_base = hb;
       ta.i_nlo = nlo_i;
       ta.i_nhi = nhi_i;
+      ta.f_onlo = make_fdiv(nlo_o);
+      ta.f_inlo = make_fdiv(nlo_i);
       k_table_outer<<<grid_for(c, (int64_t)n_ob * KH * kOB, 256), 256, 0, c->stream>>>(ta);
       TRY(check_launch(c));
       void (*tin)(TableArgs) = B.G == 4 ? k_table_inner<4>

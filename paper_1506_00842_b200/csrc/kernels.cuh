@@ -131,6 +131,24 @@ struct SweepArgs {
 //   Ea(outer) = ca[mj] * prod_{p <  split} F[mj][p][digit_p]  ca = exp(-(b1 - c))
 //   Eb'(inner) = cb[mj] * prod_{p >= split} F[mj][p][digit_p] cb = exp(-c) / w'
 // so every table entry is a handful of fp64 multiplies (no exp), rounded once to fp32.
+// Division by a per-launch constant: q = umulhi64(x, ceil(2^64 / d)) is exact
+// for x < 2^32 and 2 <= d < 2^32 (the error term stays below 1 / d); other
+// operands take the plain division. ~4 instructions instead of a ~20-60
+// instruction division sequence in the table kernels' index math.
+struct FDiv {
+  uint64_t m;   // ceil(2^64 / d), 0 when d < 2
+  int64_t d;
+};
+inline FDiv make_fdiv(int64_t d) {
+  FDiv f;
+  f.d = d;
+  f.m = (d >= 2 && d < (int64_t(1) << 32)) ? (~0ull / (uint64_t)d) + 1 : 0;
+  return f;
+}
+__device__ __forceinline__ int64_t fdiv(int64_t x, const FDiv& f) {
+  return (f.m && (uint64_t)x <= 0xffffffffull) ? (int64_t)__umul64hi((uint64_t)x, f.m) : x / f.d;
+}
+
 struct TableArgs {
   int k, d, h, split;           // params [0, split) are outer, [split, d) inner
   int G;                        // units per reciprocal group of the sweep (inner-table layout)
@@ -148,6 +166,7 @@ struct TableArgs {
   const double *PoH, *PoL, *PiH, *PiL;    // [k*kH][n_hi] / [k*kH][n_lo]
   int64_t o_nlo, o_nhi, o_hi_base, i_nlo, i_nhi;
   int n_ob;
+  FDiv f_radix[kMaxP], f_kh, f_onlo, f_inlo, f_ngroups;   // fast divisions (make_fdiv of the above)
   float* ea;
   float* ebp;
 };
@@ -156,6 +175,7 @@ __global__ void k_table_factors(TableArgs t);
 struct PartialJobs {             // k_table_partial4: four (parameter range, sub-index range) tables
   int p_lo[4], p_hi[4];
   int64_t base[4], count[4];
+  FDiv f_count[4];
   double* out[4];
 };
 __global__ void k_table_partial4(TableArgs t, PartialJobs j);

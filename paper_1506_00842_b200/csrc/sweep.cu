@@ -52,15 +52,9 @@ __device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int 
   for (int p = kMaxP - 1; p >= 0; --p) {
     dig[p] = 0;
     if (p >= p_lo && p < p_hi) {
-      const uint32_t c = (uint32_t)t.radix[p];
-      if (id <= 0xffffffffull) {
-        const uint32_t r = (uint32_t)id;
-        dig[p] = (int)(r % c);
-        id = r / c;
-      } else {
-        dig[p] = (int)(id % c);
-        id /= c;
-      }
+      const uint64_t q = (uint64_t)fdiv((int64_t)id, t.f_radix[p]);
+      dig[p] = (int)(id - q * (uint64_t)t.radix[p]);
+      id = q;
     }
   }
 }
@@ -88,11 +82,12 @@ __global__ void k_table_partial4(TableArgs t, PartialJobs j) {
     const int r = q < e0 ? 0 : (q < e1 ? 1 : (q < e2 ? 2 : 3));
     const int64_t off = q - (r == 0 ? 0 : (r == 1 ? e0 : (r == 2 ? e1 : e2)));
     const int64_t count = r == 0 ? j.count[0] : (r == 1 ? j.count[1] : (r == 2 ? j.count[2] : j.count[3]));
+    const FDiv fc = r == 0 ? j.f_count[0] : (r == 1 ? j.f_count[1] : (r == 2 ? j.f_count[2] : j.f_count[3]));
     const int64_t base = r == 0 ? j.base[0] : (r == 1 ? j.base[1] : (r == 2 ? j.base[2] : j.base[3]));
     const int p_lo = r == 0 ? j.p_lo[0] : (r == 1 ? j.p_lo[1] : (r == 2 ? j.p_lo[2] : j.p_lo[3]));
     const int p_hi = r == 0 ? j.p_hi[0] : (r == 1 ? j.p_hi[1] : (r == 2 ? j.p_hi[2] : j.p_hi[3]));
     double* out = r == 0 ? j.out[0] : (r == 1 ? j.out[1] : (r == 2 ? j.out[2] : j.out[3]));
-    const int64_t mj64 = udiv(off, count);
+    const int64_t mj64 = fdiv(off, fc);
     const int mj = (int)mj64;
     int dig[kMaxP];
     sub_digits(t, (uint64_t)(base + (off - mj64 * count)), p_lo, p_hi, dig);
@@ -116,12 +111,12 @@ __global__ void k_table_outer(TableArgs t) {
   const int64_t total = (int64_t)t.n_ob * KH * kOB;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(q % kOB);
-    const int64_t q8 = q / kOB, ob = udiv(q8, KH);
+    const int64_t q8 = q / kOB, ob = fdiv(q8, t.f_kh);
     const int mj = (int)(q8 - ob * KH);
     const int64_t o = t.o_lo + ob * kOB + r;
     float out = 1.0f;
     if (o < t.o_card && t.wprime[mj] != 0.0) {
-      const int64_t oh = udiv(o, t.o_nlo);
+      const int64_t oh = fdiv(o, t.f_onlo);
       const int64_t a = oh - t.o_hi_base, b = o - oh * t.o_nlo;
       out = (float)(t.ca[mj] * __ldg(t.PoH + (size_t)mj * t.o_nhi + a) * __ldg(t.PoL + (size_t)mj * t.o_nlo + b));
     }
@@ -250,7 +245,7 @@ __global__ void k_table_inner(TableArgs t) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
     const int th = (int)(q % kThreads);
     const int64_t rest = q / kThreads;
-    const int64_t ib = udiv(rest, ngroups);
+    const int64_t ib = fdiv(rest, t.f_ngroups);
     const int gi = (int)(rest - ib * ngroups);
     int64_t a[kInner], b[kInner];
     bool in[kInner];
@@ -258,7 +253,7 @@ __global__ void k_table_inner(TableArgs t) {
     for (int s = 0; s < kInner; ++s) {
       const int64_t i = ib * kInnerBlock + (int64_t)s * kThreads + th;
       in[s] = i < t.c_in;
-      a[s] = udiv(i, t.i_nlo);
+      a[s] = fdiv(i, t.f_inlo);
       b[s] = i - a[s] * t.i_nlo;
     }
     float out[WF];
