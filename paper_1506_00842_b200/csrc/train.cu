@@ -122,6 +122,13 @@ __global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a, int ftab_n) {
   }
   __syncthreads();
   const bool active = lane < h;
+  // register-owned parameters (see the momentum update): needs exact-width
+  // inputs with one warp per parameter row and two spare lanes in warp 0
+  constexpr bool kOwn = DC != 0 && DC + 2 <= kTW;
+  const bool own = kOwn && h <= 30;
+  double own_w = 0.0, own_v = 0.0;
+  if (own && lane < h && warp < d + 2) own_w = warp < d ? W1[warp][lane] : (warp == d ? B1[lane] : W2[lane]);
+  if (own && warp == 0 && lane == 30) own_w = s_b2;
   double first = nan(""), last = nan("");
   int diverged = 0;
 
@@ -253,6 +260,36 @@ __global__ void __launch_bounds__(kTW * 32) k_train(TrainArgs a, int ftab_n) {
       }
       __syncthreads();
       // momentum update: v = mu*v - lr*g ; w += v   (model.py:233-240)
+      if (own) {
+        // warp p updates parameter row p, lane j unit j, from registers (the
+        // weight and its velocity live in the updating thread; the shared
+        // copy is what the next step's forward reads); the two idle lanes of
+        // warp 0 (h <= 30) reduce the output bias and the loss
+        if (warp < d + 2 && lane < h) {
+          double g = P(0, warp, lane);
+#pragma unroll
+          for (int w = 1; w < kTW; ++w) g = __dadd_rn(g, P(w, warp, lane));
+          own_v = __dsub_rn(__dmul_rn(a.mu, own_v), __dmul_rn(a.lr, g));
+          own_w = __dadd_rn(own_w, own_v);
+          if (warp < d) W1[warp][lane] = own_w;
+          else if (warp == d) B1[lane] = own_w;
+          else W2[lane] = own_w;
+        } else if (warp == 0 && lane == 30) {
+          double g = pscal[0][0];
+#pragma unroll
+          for (int w = 1; w < kTW; ++w) g = __dadd_rn(g, pscal[w][0]);
+          own_v = __dsub_rn(__dmul_rn(a.mu, own_v), __dmul_rn(a.lr, g));
+          own_w = __dadd_rn(own_w, own_v);
+          s_b2 = own_w;
+        } else if (warp == 0 && lane == 31) {
+          double ss = pscal[0][1];
+#pragma unroll
+          for (int w = 1; w < kTW; ++w) ss = __dadd_rn(ss, pscal[w][1]);
+          s_sse = __dadd_rn(s_sse, ss);
+        }
+        __syncthreads();
+        continue;
+      }
       for (int q = tid; q < (d + 2) * 32; q += blockDim.x) {
         const int p = q / 32, j = q % 32;
         if (j >= h) continue;
