@@ -397,7 +397,6 @@ __device__ __forceinline__ void group_step(f2 (&acc)[OBU], const float* E, const
         ea[x][0] = t.x, ea[x][1] = t.y, ea[x][2] = 0.f, ea[x][3] = 0.f;
       }
     }
-#pragma unroll
     {
       // the outers of one exp(-A') load, unit-major: the FFMA2s of a unit share
       // eb / 1/w' (2 at a time: 4.90 ms; 4 at a time: 4.79 ms on the 10^8 case)
