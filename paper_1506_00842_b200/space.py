@@ -137,18 +137,25 @@ class ParamSpace:
         lo, hi = int(idx.min()), int(idx.max())
         if lo < 0 or hi >= card:
             raise IndexError(f"index {lo if lo < 0 else hi} out of range for {card} configurations")
-        radix = [len(p.values) for p in self.params]
-        table = np.zeros((len(radix), max(radix)), dtype=np.int64)
-        try:
-            for col, p in enumerate(self.params):
-                table[col, :radix[col]] = p.values
-        except OverflowError:   # a parameter value beyond int64: decode one by one
+        dec = self.__dict__.get("_decode")
+        if dec is None:   # (value table, strides, radices, columns): the space is immutable
+            radix = [len(p.values) for p in self.params]
+            table = np.zeros((len(radix), max(radix)), dtype=np.int64)
+            try:
+                for col, p in enumerate(self.params):
+                    table[col, :radix[col]] = p.values
+            except OverflowError:   # a parameter value beyond int64: decode one by one
+                table = None
+            strides = np.ones(len(radix), dtype=np.int64)
+            for col in range(len(radix) - 2, -1, -1):
+                strides[col] = strides[col + 1] * radix[col + 1]
+            dec = (table, strides[None, :], np.asarray(radix, dtype=np.int64)[None, :],
+                   np.arange(len(radix))[None, :])
+            object.__setattr__(self, "_decode", dec)
+        table, strides, radix, cols = dec
+        if table is None:
             return [self.config_at(i) for i in idx.tolist()]
-        strides = np.ones(len(radix), dtype=np.int64)
-        for col in range(len(radix) - 2, -1, -1):
-            strides[col] = strides[col + 1] * radix[col + 1]
-        digits = (idx[:, None] // strides[None, :]) % np.asarray(radix, dtype=np.int64)[None, :]
-        vals = table[np.arange(len(radix))[None, :], digits]
+        vals = table[cols, (idx[:, None] // strides) % radix]
         return list(map(tuple, vals.tolist()))
 
     def validate_config(self, config) -> None:
