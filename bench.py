@@ -624,10 +624,11 @@ def main():
                          "mufu_frac": mufu_rate / mufu_peak,
                          "work_per_config": {"fma_pipe_lane_ops": lane_ops, "reciprocals": rcp_per_config,
                                              "group": G},
-                         # the instruction mix's own ceiling: two of the 3G-1
-                         # packed ops per group read three register pairs (3 issue cycles)
-                         "frac_vs_register_bank_ceiling": achieved / ffma_tflops * (3.0 * G + 1) / (3.0 * G - 1)
-                         if G >= 2 else None,
+                         # the instruction mix's own ceiling: of the 3G-1 packed
+                         # ops per group and register pair, those reading three register pairs
+                         # (num and the accumulate) issue in 3 cycles instead of 2
+                         "frac_vs_register_bank_ceiling": achieved / ffma_tflops
+                         * (2.0 * (3 * G - 1) + {1: 0, 2: 1, 3: 2, 4: 2}.get(G, 2)) / (2.0 * (3 * G - 1)),
                          "sweep_ms_per_launch": t[1].item(),
                          "naive_sec8d_tflops": flops_per_config(k, d) * n_local / sweep_s / 1e12},
             "candidates_rescored": int(np.mean(cands)),
