@@ -329,8 +329,10 @@ int launch_predict64(mlt_ctx* c, const DEns& e, const DSpace& s, int check_rules
                      const int64_t* idx, const double* feat, int64_t n, double* pred, int64_t* idx_out,
                      const float* band_v = nullptr, float band_theta = 0.f) {
   if (n <= 0) return MLT_OK;
-  const size_t smem = predict64_smem(e);
-  if (smem > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem);
+  // the weights are staged in shared memory when they fit; the packed block
+  // in global memory serves wider ensembles (the packed layouts are the same)
+  const int staged = predict64_smem(e) <= 200 * 1024 ? 1 : 0;
+  const size_t smem = staged ? predict64_smem(e) : 0;
   CU(cudaFuncSetAttribute(k_predict64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nb = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_predict64, 128, smem));
@@ -338,7 +340,7 @@ int launch_predict64(mlt_ctx* c, const DEns& e, const DSpace& s, int check_rules
   const int64_t want = (n + 127) / 128;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nb * c->sms));
   k_predict64<<<grid, 128, smem, c->stream>>>(e, s, check_rules, begin, idx, feat, n, pred, idx_out, band_v,
-                                              band_theta);
+                                              band_theta, staged);
   return check_launch(c);
 }
 
@@ -1156,10 +1158,10 @@ int mlt_member_outputs(mlt_ctx* c, const mlt_ensemble* ens, const double* x, int
   TRY(ws_t(c, S_FEAT, (size_t)n * he.d, &dx));
   TRY(ws_t(c, S_OUT_A, (size_t)n * he.k, &dp));
   CU(cudaMemcpyAsync(dx, x, (size_t)n * he.d * 8, cudaMemcpyHostToDevice, c->stream));
-  const size_t smem = predict64_smem(de);
-  if (smem > 200 * 1024) return fail(MLT_EINVAL, "ensemble too large for the fp64 kernel (%zu B)", smem);
+  const int staged = predict64_smem(de) <= 200 * 1024 ? 1 : 0;
+  const size_t smem = staged ? predict64_smem(de) : 0;
   CU(cudaFuncSetAttribute(k_member_out64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_member_out64<<<grid_for(c, n, 128), 128, smem, c->stream>>>(de, dx, n, dp);
+  k_member_out64<<<grid_for(c, n, 128), 128, smem, c->stream>>>(de, dx, n, dp, staged);
   TRY(check_launch(c));
   CU(cudaMemcpyAsync(out, dp, (size_t)n * he.k * 8, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -1266,6 +1268,9 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
   BandSetup* bs = nullptr;
   if (!idx_list && m <= kMaxTopM && c->opt_path != 1) TRY(get_setup(p, choose_split(p, n), &bs));
   bool band = bs && bs->ok && (n >= 4096 || c->opt_path == 0);
+  // the sweep stages two exp(-A') tiles of k*30*8 floats plus its candidate
+  // slots in shared memory: very large ensembles take the exact path instead
+  if (band && sweep_smem(p->he.k, m > kMaxTopMSmall ? kSBBig : kSB) > 227 * 1024) band = false;
 
   if (band) {
     const BandSetup& B = *bs;

@@ -14,8 +14,8 @@ __global__ void k_valid_range(DSpace s, int64_t lo, int64_t n, uint8_t* out);
 __global__ void k_encode(DEns e, const int64_t* idx, int64_t n, double* out);
 __global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, const int64_t* idx,
                             const double* feat, int64_t n, double* pred, int64_t* idx_out,
-                            const float* band_v, float band_theta);
-__global__ void k_member_out64(DEns e, const double* feat, int64_t n, double* out);
+                            const float* band_v, float band_theta, int staged);
+__global__ void k_member_out64(DEns e, const double* feat, int64_t n, double* out, int staged);
 size_t predict64_smem(const DEns& e);
 __global__ void k_rescore(DEns e, const int64_t* idx, const uint32_t* n_ptr, double* pred);
 

@@ -98,10 +98,16 @@ __device__ __forceinline__ double mean_log64(const DEns& e, const double* sm, co
 // `s_check` is set), and optionally the key bits of pred for sorting.
 __global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, const int64_t* __restrict__ idx,
                             const double* __restrict__ feat, int64_t n, double* __restrict__ pred,
-                            int64_t* __restrict__ idx_out, const float* __restrict__ band_v, float band_theta) {
-  extern __shared__ double sm[];
-  stage_weights(e, sm);
-  __syncthreads();
+                            int64_t* __restrict__ idx_out, const float* __restrict__ band_v, float band_theta,
+                            int staged) {
+  // staged: the weights fit the launch's shared memory; otherwise (very wide
+  // ensembles) they are read from the packed global block through L1
+  extern __shared__ double sm_dyn[];
+  if (staged) {
+    stage_weights(e, sm_dyn);
+    __syncthreads();
+  }
+  const double* sm = staged ? sm_dyn : e.w1;   // [W1 | b1 | w2 | b2 | mean | std], the same layout
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     double x[kMaxP];
     bool ok = true;
@@ -137,10 +143,14 @@ __global__ void k_predict64(DEns e, DSpace s, int check_rules, int64_t begin, co
 }
 
 // Raw output of every member (Network.forward_batch): out[m][t].
-__global__ void k_member_out64(DEns e, const double* __restrict__ feat, int64_t n, double* __restrict__ out) {
-  extern __shared__ double sm[];
-  stage_weights(e, sm);
-  __syncthreads();
+__global__ void k_member_out64(DEns e, const double* __restrict__ feat, int64_t n, double* __restrict__ out,
+                               int staged) {
+  extern __shared__ double sm_dyn[];
+  if (staged) {
+    stage_weights(e, sm_dyn);
+    __syncthreads();
+  }
+  const double* sm = staged ? sm_dyn : e.w1;
   const int nw = e.k * e.h * e.d, nh = e.k * e.h;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     double x[kMaxP];

@@ -462,3 +462,26 @@ def test_autotune_end_to_end_on_surrogate():
     best_cfg, best_t = b.exhaustive_search(sp, runner)
     assert rep.best_time <= best_t * 1.10
     assert rep.measurements_total == 2200
+
+
+def test_wide_ensembles_against_oracle():
+    """Ensembles far wider than the benchmark's equal the oracle's lexsort:
+    k = 40 (1200 hidden units on the sweep, also with m = 1500), k = 100 (the
+    widest whose two exp(-A') tiles, 2 * k*30*8*4 B, fit the sweep's shared
+    memory), k = 110 (the exact path answers, its fp64 kernel reading the
+    weights from global memory: they exceed its shared-memory staging)."""
+    import paper_1506_00842_b200 as b
+    from oracle.tuner import top_m as otop
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    sp = product_space("stereo")
+    rng = np.random.default_rng(5)
+    for k, m in [(40, 100), (40, 1500), (100, 60), (110, 60)]:
+        nets = [b.Network(rng.normal(size=(30, 11)), rng.normal(size=30), rng.normal(size=30),
+                          float(rng.normal()), float(rng.normal()), float(rng.uniform(0.2, 2))) for _ in range(k)]
+        ens = b.Ensemble(nets, b.Encoder.from_space(sp), sp.name)
+        osp, oens = _oracle_from(sp, ens)
+        oi, op = otop(oens, osp, m, begin=0, end=1 << 19)
+        idx, pred, st = top_m_arrays(ens, sp, m, begin=0, end=1 << 19, with_stats=True)
+        assert st["path"] == (0 if k <= 100 else 1), (k, st)
+        assert np.array_equal(idx, oi), (k, m)
+        np.testing.assert_allclose(pred, op, rtol=PRED_RTOL, atol=0)
