@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -697,7 +698,11 @@ int get_setup(mlt_plan* p, int split, BandSetup** out) {
   auto it = p->setups.find(key);
   if (it == p->setups.end()) {
     BandSetup b;
+    const auto t0 = std::chrono::steady_clock::now();
     const int rc = band_setup(p, split, b);
+    if (std::getenv("MLT_STEP_TRACE"))
+      std::fprintf(stderr, "{\"band_setup_us\": %.1f}\n",
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     if (rc != MLT_OK) {
       pool_free(p->ctx, b.d_tab);
       return rc;
@@ -1173,10 +1178,17 @@ int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens,
   CTX_GUARD(c);
   *out = nullptr;
   CU(cudaSetDevice(c->dev));
+  const bool trace = std::getenv("MLT_STEP_TRACE") != nullptr;   // diagnostics: host time of the phases
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::micro>(b - a).count();
+  };
+  const auto t0 = now();
   mlt_plan* p = new mlt_plan();
   p->ctx = c;
   int rc = read_space(space, &p->hs);
   if (rc == MLT_OK) rc = read_ens(ens, &p->he);
+  const auto t1 = now();
   if (rc == MLT_OK && p->he.d != p->hs.P)
     rc = fail(MLT_EMISMATCH, "ensemble has %d inputs but the space has %d parameters", p->he.d, p->hs.P);
   for (int q = 0; rc == MLT_OK && q < p->hs.P; ++q)
@@ -1184,7 +1196,12 @@ int mlt_plan_create(mlt_ctx* c, const mlt_space* space, const mlt_ensemble* ens,
       rc = fail(MLT_EMISMATCH, "encoder parameter %d has %d values, space has %d", q, p->he.counts[q],
                 p->hs.radix[q]);
   if (rc == MLT_OK) rc = plan_upload(p);
+  const auto t2 = now();
   if (rc == MLT_OK) rc = plan_factors(p);
+  const auto t3 = now();
+  if (trace)
+    std::fprintf(stderr, "{\"plan_read_us\": %.1f, \"plan_upload_us\": %.1f, \"plan_factors_us\": %.1f}\n",
+                 us(t0, t1), us(t1, t2), us(t2, t3));
   if (rc == MLT_OK) {
     const HostEns& e = p->he;
     bool constant = true;
