@@ -362,6 +362,10 @@ MLT_API int mlt_raybench_destroy(mlt_raybench* bench);
  *              interleaved, unroll_ray}; status/seconds as for conv. */
 MLT_API int mlt_raybench_run(mlt_raybench* bench, const int32_t* knobs, int32_t reps, double* seconds, int32_t* status);
 MLT_API int mlt_raybench_output(mlt_raybench* bench, float* host_rgba);
+/* Budgeted screening for exhaustive sweeps: each launch stops starting new
+ * pixels budget_ns after it began (a slower configuration then times as
+ * >= budget_ns); 0 = normal measurement (the default). */
+MLT_API int mlt_raybench_set_budget(mlt_raybench* bench, uint64_t budget_ns);
 MLT_API int mlt_raybench_volume(mlt_raybench* bench, uint8_t* host_volume);
 MLT_API int mlt_raybench_transfer(mlt_raybench* bench, float* host_rgba256);
 /* 19 floats: centre[3], u[3], v[3], dir[3], 1/dir[3], scale, width/2, height/2, opacity threshold */

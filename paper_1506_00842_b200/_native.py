@@ -125,6 +125,7 @@ _SIGNATURES = [
     ("mlt_raybench_destroy", C.c_int, [C.c_void_p]),
     ("mlt_raybench_run", C.c_int, [C.c_void_p, _i32p, C.c_int32, _f64p, _i32p]),
     ("mlt_raybench_output", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("mlt_raybench_set_budget", C.c_int, [C.c_void_p, C.c_uint64]),
     ("mlt_raybench_volume", C.c_int, [C.c_void_p, _u8p]),
     ("mlt_raybench_transfer", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     ("mlt_raybench_camera", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),

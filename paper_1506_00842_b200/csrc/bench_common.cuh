@@ -31,6 +31,16 @@ __device__ __forceinline__ uint64_t hash_at(uint64_t seed, uint64_t q) {
   return splitmix64(seed + 0x9E3779B97F4A7C15ull * (q + 1));
 }
 
+// %globaltimer (ns): the budgeted measurement mode's clock
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// the launch time stamp a budgeted kernel measures its budget from
+static __global__ void k_stamp(unsigned long long* t0) { *t0 = gtimer(); }
+
 static __global__ void k_flush_l2(uint4* buf, size_t n, uint32_t v) {
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x)
     buf[q] = make_uint4(v, v, v, v);

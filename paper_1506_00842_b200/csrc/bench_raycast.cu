@@ -122,6 +122,8 @@ struct mlt_raybench {
   float tf_host[1024];
   mlt::RayCamera cam;
   mlt::bench::Timer timer;
+  uint64_t budget_ns = 0;                  // mlt_raybench_set_budget (0: normal measurement)
+  unsigned long long* d_t0 = nullptr;      // its launch time stamp
 };
 
 namespace {
@@ -212,9 +214,24 @@ MLT_API int mlt_raybench_destroy(mlt_raybench* b) {
   cudaFree(b->vol);
   cudaFree(b->tf);
   cudaFree(b->out);
+  if (b->d_t0) cudaFree(b->d_t0);
   b->timer.release();
   cudaStreamDestroy(b->stream);
   delete b;
+  return MLT_OK;
+}
+
+// Budgeted screening for exhaustive sweeps over the raycasting space: with
+// budget_ns > 0 every launch stops starting new pixels budget_ns after it
+// began, so a configuration slower than the budget costs about the budget
+// (its measured time is then >= budget_ns: "slower than the budget", not a
+// time); faster ones render completely and time as usual. 0 restores the
+// normal measurement. The image is only complete for unaborted launches.
+MLT_API int mlt_raybench_set_budget(mlt_raybench* b, uint64_t budget_ns) {
+  if (!b) return g_rerr.fail(MLT_EINVAL, "NULL argument");
+  CK(cudaSetDevice(b->dev));
+  if (budget_ns && !b->d_t0) CK(cudaMalloc(&b->d_t0, sizeof(unsigned long long)));
+  b->budget_ns = budget_ns;
   return MLT_OK;
 }
 
@@ -254,9 +271,12 @@ MLT_API int mlt_raybench_run(mlt_raybench* b, const int32_t* knobs, int32_t reps
   a.pptx = pptx;
   a.ppty = ppty;
   a.cam = b->cam;
+  a.budget_ns = b->budget_ns;
+  a.t0 = b->d_t0;
   RayConstTF ctf;
   std::memcpy(ctf.e, b->tf_host, sizeof ctf.e);
   return b->timer.run(g_rerr, reps, [&]() {
+    if (b->budget_ns) bench::k_stamp<<<1, 1, 0, b->stream>>>(b->d_t0);
     k<<<dim3((unsigned)gx, (unsigned)gy), dim3(wgx, wgy), 0, b->stream>>>(a, ctf);
     return cudaGetLastError();
   }, seconds, status);

@@ -33,6 +33,11 @@ struct RayArgs {
   float4* out;                      // IW x IH RGBA
   int pptx, ppty;
   RayCamera cam;
+  // budgeted screening (mlt_raybench_set_budget): threads stop starting new
+  // pixels once budget_ns has passed since *t0 (k_stamp right before the
+  // launch); 0 = the normal measurement, every pixel rendered
+  unsigned long long budget_ns;
+  const unsigned long long* t0;
 };
 
 // the transfer function as a kernel-parameter (constant-bank) array

@@ -37,12 +37,14 @@ __global__ void k_raycast(RayArgs a, const __grid_constant__ RayConstTF ctf) {
   const int bw = wgx * a.pptx, bh = wgy * a.ppty;
   const int X0 = blockIdx.x * bw, Y0 = blockIdx.y * bh;
   const float V[3] = {(float)a.VX, (float)a.VY, (float)a.VZ};
+  const unsigned long long start = a.budget_ns ? *a.t0 : 0ull;
   for (int iy = 0; iy < a.ppty; ++iy) {
     const int py = Y0 + (INTER ? iy * wgy + ty : ty * a.ppty + iy);
     if (py >= a.IH) continue;
     for (int ix = 0; ix < a.pptx; ++ix) {
       const int px = X0 + (INTER ? ix * wgx + tx : tx * a.pptx + ix);
       if (px >= a.IW) continue;
+      if (a.budget_ns && bench::gtimer() - start > a.budget_ns) return;   // screening: over budget
       const float sa = __fmul_rn(__fsub_rn(__fadd_rn((float)px, 0.5f), cam.hw), cam.scale);
       const float sb = __fmul_rn(__fsub_rn(__fadd_rn((float)py, 0.5f), cam.hh), cam.scale);
       float o[3], tn = -INFINITY, tf = INFINITY;

@@ -223,6 +223,13 @@ class B200RaycastRunner(_B200BenchRunner):
             tp = N.ptr(self._t, N.C.c_float)
         self._create(int(device), self.width, self.height, vx, vy, vz, vp, tp, int(seed))
 
+    def set_budget(self, seconds: float | None) -> None:
+        """Budgeted screening for exhaustive sweeps (mlt_raybench_set_budget):
+        a launch stops starting new pixels `seconds` after it began, so a
+        slower configuration measures as >= `seconds`; None restores the
+        normal measurement."""
+        self._check(self._fn("set_budget")(self._h, int(round((seconds or 0.0) * 1e9))))
+
     def output(self) -> np.ndarray:
         out = np.empty((self.height, self.width, 4), dtype=np.float32)
         self._check(self._fn("output")(self._h, N.ptr(out, N.C.c_float)))

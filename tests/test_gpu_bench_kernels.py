@@ -195,3 +195,26 @@ def test_raycast_host_inputs_and_invalid_launches(gpu_ok):
     with pytest.raises(ValueError):
         r.run((8, 8, 1, 1, 0, 0, 0, 0, 0, 3))
     r.close()
+
+
+def test_raycast_budgeted_screening(gpu_ok):
+    """mlt_raybench_set_budget: a configuration far slower than the budget
+    stops early and times at about the budget; with the budget off again the
+    same configuration renders the full, bit-exact image at its normal time."""
+    import paper_1506_00842_b200 as b
+    from oracle.bench_golden import raycast
+    from paper_1506_00842_b200.runners import B200RaycastRunner
+    r = B200RaycastRunner(b.builtin_space("raycasting"), width=512, height=512, volume_shape=(256, 256, 256),
+                          seed=2, default_repetitions=1)
+    slow = (1, 1, 16, 16, 0, 0, 0, 0, 0, 1)          # one thread per 256 pixels: very slow
+    t_full, ok = r.run(slow, 1)
+    assert ok and t_full > 4e-3
+    r.set_budget(5e-4)
+    t_screen, ok = r.run(slow, 1)
+    assert ok and 5e-4 <= t_screen < min(0.5 * t_full, 3e-3), (t_screen, t_full)
+    r.set_budget(None)
+    t_again, ok = r.run(slow, 1)
+    assert ok and t_again > 0.8 * t_full
+    gold = raycast(r.volume(), r.transfer(), r.camera(), 512, 512)
+    assert np.array_equal(r.output(), gold)
+    r.close()

@@ -63,6 +63,9 @@ def main():
     ap.add_argument("--budget-s", type=float, default=1800.0, help="stop the exhaustive sweep after this long")
     ap.add_argument("--rep-cutoff-s", type=float, default=0.05,
                     help="skip further repetitions after one longer than this (0: always run every repetition)")
+    ap.add_argument("--screen-budget-ms", type=float, default=0.0,
+                    help="exhaustive sweep: screen every configuration with a per-launch time budget "
+                         "(raycast: mlt_raybench_set_budget), then re-measure the fastest normally")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
 
@@ -126,6 +129,11 @@ def main():
 
     if args.exhaustive:
         card = space.cardinality()
+        if args.screen_budget_ms:
+            # screening: a launch stops starting new pixels after the budget, so a
+            # configuration slower than it costs ~the budget and times >= it; the
+            # fastest are re-measured below with the budget off (the tuner's protocol)
+            runner.set_budget(args.screen_budget_ms / 1e3)
         t0 = time.perf_counter()
         times = np.full(card, np.nan)
         done = 0
@@ -137,6 +145,10 @@ def main():
             if time.perf_counter() - t0 > args.budget_s:
                 break
         wall = time.perf_counter() - t0
+        screened_slow = None
+        if args.screen_budget_ms:
+            runner.set_budget(None)
+            screened_slow = int(np.sum(times >= 0.999 * args.screen_budget_ms / 1e3))
         order = np.argsort(np.where(np.isnan(times), np.inf, times))[:20]
         # re-measure the 20 fastest with the tuner's repetitions
         best = None
@@ -146,7 +158,10 @@ def main():
                 best = (tt, i)
         res["exhaustive"] = {"measured": int(done), "complete": bool(done == card), "valid": int(np.isfinite(times).sum()),
                              "wall_s": wall, "best_index": best[1], "best_config": space.config_at(best[1]),
-                             "best_time_s": best[0]}
+                             "best_time_s": best[0], "screen_budget_ms": args.screen_budget_ms or None,
+                             "screened_slower_than_budget": screened_slow,
+                             "time_ms_quantiles_screened": {q: float(np.nanquantile(times, q) * 1e3)
+                                                            for q in (0, 0.001, 0.01, 0.1, 0.5)}}
         for t in res.get("tune", []):
             t["slowdown_vs_exhaustive"] = t["best_time_s"] / best[0]
     runner.close()
