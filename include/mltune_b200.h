@@ -346,6 +346,8 @@ MLT_API int mlt_stereobench_destroy(mlt_stereobench* bench);
 MLT_API int mlt_stereobench_run(mlt_stereobench* bench, const int32_t* knobs, int32_t reps, double* seconds,
                                 int32_t* status);
 MLT_API int mlt_stereobench_output(mlt_stereobench* bench, uint8_t* host_disparity);
+/* Budgeted screening for exhaustive sweeps (see mlt_raybench_set_budget). */
+MLT_API int mlt_stereobench_set_budget(mlt_stereobench* bench, uint64_t budget_ns);
 MLT_API int mlt_stereobench_input(mlt_stereobench* bench, uint8_t* host_left, uint8_t* host_right);
 MLT_API const char* mlt_stereobench_last_error(void);
 

@@ -118,6 +118,7 @@ _SIGNATURES = [
     ("mlt_stereobench_destroy", C.c_int, [C.c_void_p]),
     ("mlt_stereobench_run", C.c_int, [C.c_void_p, _i32p, C.c_int32, _f64p, _i32p]),
     ("mlt_stereobench_output", C.c_int, [C.c_void_p, _u8p]),
+    ("mlt_stereobench_set_budget", C.c_int, [C.c_void_p, C.c_uint64]),
     ("mlt_stereobench_input", C.c_int, [C.c_void_p, _u8p, _u8p]),
     ("mlt_stereobench_last_error", C.c_char_p, []),
     ("mlt_raybench_create", C.c_int, [C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _u8p,

@@ -86,6 +86,8 @@ struct mlt_stereobench {
   cudaArray_t arr_l = nullptr, arr_r = nullptr;
   cudaTextureObject_t tex_l = 0, tex_r = 0;
   mlt::bench::Timer timer;
+  uint64_t budget_ns = 0;                  // mlt_stereobench_set_budget (0: normal measurement)
+  unsigned long long* d_t0 = nullptr;      // its launch time stamp
 };
 
 namespace {
@@ -149,9 +151,19 @@ MLT_API int mlt_stereobench_destroy(mlt_stereobench* b) {
   cudaFree(b->left);
   cudaFree(b->right);
   cudaFree(b->out);
+  if (b->d_t0) cudaFree(b->d_t0);
   b->timer.release();
   cudaStreamDestroy(b->stream);
   delete b;
+  return MLT_OK;
+}
+
+// Budgeted screening for exhaustive sweeps (see mlt_raybench_set_budget).
+MLT_API int mlt_stereobench_set_budget(mlt_stereobench* b, uint64_t budget_ns) {
+  if (!b) return g_serr.fail(MLT_EINVAL, "NULL argument");
+  CK(cudaSetDevice(b->dev));
+  if (budget_ns && !b->d_t0) CK(cudaMalloc(&b->d_t0, sizeof(unsigned long long)));
+  b->budget_ns = budget_ns;
   return MLT_OK;
 }
 
@@ -195,7 +207,10 @@ MLT_API int mlt_stereobench_run(mlt_stereobench* b, const int32_t* knobs, int32_
   a.out = b->out;
   a.pptx = pptx;
   a.ppty = ppty;
+  a.budget_ns = b->budget_ns;
+  a.t0 = b->d_t0;
   return b->timer.run(g_serr, reps, [&]() {
+    if (b->budget_ns) bench::k_stamp<<<1, 1, 0, b->stream>>>(b->d_t0);
     k<<<dim3((unsigned)gx, (unsigned)gy), dim3(wgx, wgy), smem, b->stream>>>(a);
     return cudaGetLastError();
   }, seconds, status);

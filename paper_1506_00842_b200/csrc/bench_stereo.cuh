@@ -17,6 +17,10 @@ struct StereoArgs {
   cudaTextureObject_t tex_left, tex_right;
   uint8_t* out;
   int pptx, ppty;
+  // budgeted screening (mlt_stereobench_set_budget): threads stop starting new
+  // pixels once budget_ns has passed since *t0; 0 = the normal measurement
+  unsigned long long budget_ns;
+  const unsigned long long* t0;
 };
 
 typedef void (*StereoKernel)(StereoArgs);

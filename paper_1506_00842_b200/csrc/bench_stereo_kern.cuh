@@ -53,6 +53,7 @@ __global__ void k_stereo(StereoArgs a) {
       }
     __syncthreads();
   }
+  const unsigned long long start = a.budget_ns ? *a.t0 : 0ull;
   for (int iy = 0; iy < a.ppty; ++iy) {
     const int ly = ty * a.ppty + iy;
     const int y = Y0 + ly;
@@ -61,6 +62,7 @@ __global__ void k_stereo(StereoArgs a) {
       const int lx = tx * a.pptx + ix;
       const int x = X0 + lx;
       if (x >= a.W) break;
+      if (a.budget_ns && bench::gtimer() - start > a.budget_ns) return;   // screening: over budget
       unsigned best = 0xffffffffu;
       int bd = 0;
       if (LL && LR && UX == 4 && R == 4) {

@@ -98,6 +98,13 @@ class _B200BenchRunner:
             return Sample(tuple(config), Outcome.invalid(STATUS_INVALID_LAUNCH), reps)
         return Sample(tuple(config), Outcome.valid(t), reps)
 
+    def set_budget(self, seconds: float | None) -> None:
+        """Budgeted screening for exhaustive sweeps (stereo and raycasting:
+        mlt_*bench_set_budget): a launch stops starting new pixels `seconds`
+        after it began, so a slower configuration measures as >= `seconds`;
+        None restores the normal measurement."""
+        self._check(self._fn("set_budget")(self._h, int(round((seconds or 0.0) * 1e9))))
+
     def measured_times(self, indices, repetitions: int = 1):
         idx = np.asarray(indices, dtype=np.int64)
         times = np.full(idx.shape[0], np.nan)
@@ -222,13 +229,6 @@ class B200RaycastRunner(_B200BenchRunner):
                 raise ValueError("transfer function must have 256 RGBA entries")
             tp = N.ptr(self._t, N.C.c_float)
         self._create(int(device), self.width, self.height, vx, vy, vz, vp, tp, int(seed))
-
-    def set_budget(self, seconds: float | None) -> None:
-        """Budgeted screening for exhaustive sweeps (mlt_raybench_set_budget):
-        a launch stops starting new pixels `seconds` after it began, so a
-        slower configuration measures as >= `seconds`; None restores the
-        normal measurement."""
-        self._check(self._fn("set_budget")(self._h, int(round((seconds or 0.0) * 1e9))))
 
     def output(self) -> np.ndarray:
         out = np.empty((self.height, self.width, 4), dtype=np.float32)

@@ -218,3 +218,23 @@ def test_raycast_budgeted_screening(gpu_ok):
     gold = raycast(r.volume(), r.transfer(), r.camera(), 512, 512)
     assert np.array_equal(r.output(), gold)
     r.close()
+
+
+def test_stereo_budgeted_screening(gpu_ok):
+    """mlt_stereobench_set_budget: as for raycasting -- a slow configuration
+    stops early under the budget, and renders the exact disparity map again
+    with the budget off."""
+    import paper_1506_00842_b200 as b
+    from paper_1506_00842_b200.runners import B200StereoRunner
+    r = B200StereoRunner(b.builtin_space("stereo"), width=512, height=512, seed=5, default_repetitions=1)
+    slow = (1, 1, 16, 16, 0, 0, 0, 0, 1, 1, 1)        # one thread per 256 pixels: very slow
+    t_full, ok = r.run(slow, 1)
+    assert ok
+    ref = r.output().copy()
+    r.set_budget(min(2e-4, 0.25 * t_full))
+    t_screen, ok = r.run(slow, 1)
+    assert ok and t_screen < 0.6 * t_full, (t_screen, t_full)
+    r.set_budget(None)
+    t_again, ok = r.run(slow, 1)
+    assert ok and np.array_equal(r.output(), ref)
+    r.close()
