@@ -391,12 +391,13 @@ class PackedEnsemble:
         enc = ensemble.encoder
         self.counts = np.ascontiguousarray([len(vals) for _, vals in enc.params], dtype=np.int32)
         h, d = np.asarray(members[0].weights_hidden).shape
-        self.w1 = np.ascontiguousarray(np.stack([np.asarray(m.weights_hidden, dtype=np.float64) for m in members]))
-        self.b1 = np.ascontiguousarray(np.stack([np.asarray(m.biases_hidden, dtype=np.float64) for m in members]))
-        self.w2 = np.ascontiguousarray(np.stack([np.asarray(m.weights_out, dtype=np.float64) for m in members]))
-        self.b2 = np.ascontiguousarray([float(m.bias_out) for m in members], dtype=np.float64)
-        self.mean = np.ascontiguousarray([float(m.target_mean) for m in members], dtype=np.float64)
-        self.std = np.ascontiguousarray([float(m.target_std) for m in members], dtype=np.float64)
+        # np.array over the member list builds each stacked block in one call (C order)
+        self.w1 = np.array([m.weights_hidden for m in members], dtype=np.float64)
+        self.b1 = np.array([m.biases_hidden for m in members], dtype=np.float64)
+        self.w2 = np.array([m.weights_out for m in members], dtype=np.float64)
+        self.b2 = np.array([m.bias_out for m in members], dtype=np.float64)
+        self.mean = np.array([m.target_mean for m in members], dtype=np.float64)
+        self.std = np.array([m.target_std for m in members], dtype=np.float64)
         if self.w1.shape != (len(members), h, d) or self.counts.shape[0] != d:
             raise ValueError("member input dimensions do not match the encoder")
         self.c = MltEnsemble(len(members), d, h, ptr(self.counts, C.c_int32), ptr(self.w1, C.c_double),
