@@ -1,0 +1,81 @@
+"""The paper's tuning-quality experiment (evaluation.slowdown_grid,
+evaluation.py:189-221) on the B200 stereo / raycasting kernels, against the
+exhaustive optima measured by tools/bench_autotune.py --exhaustive
+--screen-budget-ms (profiles/r02_*_exhaustive.json): the runner answers
+`exhaustive_best` with that optimum (re-measured here with the tuner's
+protocol) instead of re-sweeping the whole space for every grid. Every tuner
+measurement is the B200 kernel (CUDA events, L2 flushed, min over
+repetitions). Prints one JSON line.
+
+    python tools/hw_slowdown_grid.py --bench raycast|stereo [--n 500 1000 2000] [--m 10 200] [--repeats 2]
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_1506_00842_b200 as b  # noqa: E402
+from paper_1506_00842_b200 import evaluation as EV  # noqa: E402
+from paper_1506_00842_b200.runners import B200RaycastRunner, B200StereoRunner  # noqa: E402
+
+
+class KnownOptimumRunner:
+    """Delegates measurement to the B200 runner; `exhaustive_best` returns the
+    exhaustive optimum found by the screened sweep, re-measured now."""
+
+    def __init__(self, runner, space, best_index, reps):
+        self.runner, self.space = runner, space
+        self.runner_id = runner.runner_id
+        self.default_repetitions = runner.default_repetitions
+        t, ok = runner.run(space.config_at(best_index), reps)
+        assert ok
+        self.best = (best_index, t)
+
+    def measure(self, config, repetitions=None):
+        return self.runner.measure(config, repetitions)
+
+    def exhaustive_best(self, *args):
+        i, t = self.best
+        return i, t, 1, 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bench", choices=("raycast", "stereo"), required=True)
+    ap.add_argument("--n", type=int, nargs="+", default=[500, 1000, 2000])
+    ap.add_argument("--m", type=int, nargs="+", default=[10, 200])
+    ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=3, help="repetitions per tuner measurement (the runner default)")
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    prof = json.loads((ROOT / "profiles" / f"r02_{a.bench}_exhaustive.json").read_text())
+    if a.bench == "raycast":
+        space = b.builtin_space("raycasting")
+        runner = B200RaycastRunner(space, 1024, 1024, volume_shape=(512, 512, 512), seed=0,
+                                   default_repetitions=a.reps)
+    else:
+        space = b.builtin_space("stereo")
+        runner = B200StereoRunner(space, 1024, 1024, seed=0, default_repetitions=a.reps)
+    runner.rep_cutoff_s = 0.05     # slow stage-1 configurations: one repetition (as in the exhaustive runs)
+    ko = KnownOptimumRunner(runner, space, prof["exhaustive"]["best_index"], a.reps)
+    t0 = time.perf_counter()
+    cells = EV.slowdown_grid(space, ko, a.n, a.m, a.repeats, 2015, k=11)
+    res = {"experiment": f"slowdown grid, B200 {a.bench} (paper's tuning-quality experiment) vs the exhaustive "
+                         "optimum of profiles/r02_%s_exhaustive.json" % a.bench,
+           "optimum": {"index": ko.best[0], "config": list(space.config_at(ko.best[0])), "time_s": ko.best[1]},
+           "grid_wall_s": time.perf_counter() - t0, "repetitions": a.reps, "rep_cutoff_s": runner.rep_cutoff_s,
+           "cells": [{"n": c.n_train, "m": c.m_candidates, "mean_slowdown": c.mean_slowdown, "n_success": c.n_success,
+                      "n_invalid_runs": c.invalid_run_count} for c in cells]}
+    runner.close()
+    line = json.dumps(res)
+    print(line)
+    if a.out:
+        Path(a.out).write_text(line + "\n")
+
+
+if __name__ == "__main__":
+    main()
