@@ -31,9 +31,17 @@ class KnownOptimumRunner:
         self.runner, self.space = runner, space
         self.runner_id = runner.runner_id
         self.default_repetitions = runner.default_repetitions
+        self.reps = reps
+        runner.run(space.config_at(best_index), 20)      # clocks up from idle before the reference time
         t, ok = runner.run(space.config_at(best_index), reps)
         assert ok
         self.best = (best_index, t)
+
+    def remeasure(self):
+        """min of the optimum's time before and after the grid (same protocol)"""
+        t, ok = self.runner.run(self.space.config_at(self.best[0]), self.reps)
+        if ok and t < self.best[1]:
+            self.best = (self.best[0], t)
 
     def measure(self, config, repetitions=None):
         return self.runner.measure(config, repetitions)
@@ -64,12 +72,17 @@ def main():
     ko = KnownOptimumRunner(runner, space, prof["exhaustive"]["best_index"], a.reps)
     t0 = time.perf_counter()
     cells = EV.slowdown_grid(space, ko, a.n, a.m, a.repeats, 2015, k=11)
+    t_first = ko.best[1]
+    ko.remeasure()
+    scale = t_first / ko.best[1]          # slowdowns were divided by t_first
     res = {"experiment": f"slowdown grid, B200 {a.bench} (paper's tuning-quality experiment) vs the exhaustive "
                          "optimum of profiles/r02_%s_exhaustive.json" % a.bench,
            "optimum": {"index": ko.best[0], "config": list(space.config_at(ko.best[0])), "time_s": ko.best[1]},
            "grid_wall_s": time.perf_counter() - t0, "repetitions": a.reps, "rep_cutoff_s": runner.rep_cutoff_s,
-           "cells": [{"n": c.n_train, "m": c.m_candidates, "mean_slowdown": c.mean_slowdown, "n_success": c.n_success,
-                      "n_invalid_runs": c.invalid_run_count} for c in cells]}
+           "optimum_time_before_after_s": [t_first, ko.best[1]],
+           "cells": [{"n": c.n_train, "m": c.m_candidates,
+                      "mean_slowdown": None if c.mean_slowdown is None else c.mean_slowdown * scale,
+                      "n_success": c.n_success, "n_invalid_runs": c.invalid_run_count} for c in cells]}
     runner.close()
     line = json.dumps(res)
     print(line)
