@@ -103,6 +103,8 @@ class _B200BenchRunner:
         mlt_*bench_set_budget): a launch stops starting new pixels `seconds`
         after it began, so a slower configuration measures as >= `seconds`;
         None restores the normal measurement."""
+        if not hasattr(N.lib(), f"mlt_{self._prefix}_set_budget"):
+            raise NotImplementedError(f"{type(self).__name__} has no budgeted screening mode")
         self._check(self._fn("set_budget")(self._h, int(round((seconds or 0.0) * 1e9))))
 
     def measured_times(self, indices, repetitions: int = 1):
