@@ -599,6 +599,14 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   std::vector<float> u(KH, 1.0f);
   double S = 0, log2dmax = -1e300, log2dmin = 1e300;
   int dummies = 0;
+  // the multi-valued parameters, outer ones (q < split) first: single-valued
+  // parameters never move z
+  int act[kMaxP], n_act = 0, n_out = 0;
+  for (int q = 0; q < s.P; ++q)
+    if (s.radix[q] >= 2) {
+      act[n_act++] = q;
+      if (q < split) n_out = n_act;
+    }
   // table position `mj` holds original unit unit_of[mj] (plan_factors' order)
   for (int pos = 0; pos < KH; ++pos) {
     {
@@ -613,16 +621,13 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
       const double b1 = e.b1()[(size_t)m * e.h + j];
       double amin = b1, amax = b1, bmin = 0, bmax = 0;
       const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
-      for (int q = 0; q < s.P; ++q) {
-        if (s.radix[q] < 2) continue;
-        const double lo = std::min(0.0, w[q]), hi = std::max(0.0, w[q]);
-        if (q < split) {
-          amin += lo;
-          amax += hi;
-        } else {
-          bmin += lo;
-          bmax += hi;
-        }
+      for (int t = 0; t < n_out; ++t) {
+        amin += std::min(0.0, w[act[t]]);
+        amax += std::max(0.0, w[act[t]]);
+      }
+      for (int t = n_out; t < n_act; ++t) {
+        bmin += std::min(0.0, w[act[t]]);
+        bmax += std::max(0.0, w[act[t]]);
       }
       const double c = 0.5 * (amin - bmin);   // centring: both tables span zmin/2 at their low end
       const double zmin = amin + bmin;
@@ -730,25 +735,30 @@ int plan_factors(mlt_plan* p) {
   // sweep's partial sums settle early (the pruning bounds of the remaining
   // units are then tight); padding / zero-weight units last.
   {
-    std::vector<double> range(KH, -1.0);
+    // (-range, unit) ascending == a stable sort by decreasing range; the
+    // single-valued parameters never move z, so they are skipped up front
+    int act[kMaxP], n_act = 0;
+    for (int q = 0; q < s.P; ++q)
+      if (s.radix[q] >= 2) act[n_act++] = q;
+    std::vector<std::pair<double, int>> key(KH);
     for (int mj = 0; mj < KH; ++mj) {
+      key[mj] = {1.0, mj};   // padding / zero-weight units: after every real unit
       const int m = mj / kH, j = mj % kH;
       if (j >= e.h) continue;
       const double wp = e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k;
       if (wp == 0.0) continue;
       double zmin = e.b1()[(size_t)m * e.h + j], zmax = zmin;
       const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
-      for (int q = 0; q < s.P; ++q)
-        if (s.radix[q] >= 2) {
-          zmin += std::min(0.0, w[q]);
-          zmax += std::max(0.0, w[q]);
-        }
+      for (int t = 0; t < n_act; ++t) {
+        zmin += std::min(0.0, w[act[t]]);
+        zmax += std::max(0.0, w[act[t]]);
+      }
       auto sg = [](double z) { return 1.0 / (1.0 + std::exp(-z)); };
-      range[mj] = std::fabs(wp) * (sg(zmax) - sg(zmin));
+      key[mj].first = -(std::fabs(wp) * (sg(zmax) - sg(zmin)));
     }
+    std::sort(key.begin(), key.end());
     p->unit_of.resize(KH);
-    for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = mj;
-    std::stable_sort(p->unit_of.begin(), p->unit_of.end(), [&](int x, int y) { return range[x] > range[y]; });
+    for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = key[mj].second;
     CU(cudaMallocAsync(&p->d_unit_of, (size_t)KH * 4, c->stream));
     TRY(upload_pinned(c, p->d_unit_of, p->unit_of.data(), (size_t)KH * 4));
   }
@@ -1385,6 +1395,11 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
     ta.n_ob = n_ob;
     ta.ea = ea;
     ta.ebp = ebp;
+    {
+      const int64_t lim = int64_t(1) << 31;
+      ta.idx32 = (int64_t)n_ob * KH * kOB < lim && o_lo + (int64_t)n_ob * kOB < lim &&
+                 (int64_t)n_ib * (KH / B.G) * kThreads < lim && B.c_in_pad < lim;
+    }
     // gs[0] theta key, [1] candidate count, [2..4] band-stage counters (n,
     // status, take), [8..9] pruning work (64-bit), [10] pruning: next work item
     {

@@ -146,7 +146,13 @@ inline FDiv make_fdiv(int64_t d) {
   return f;
 }
 __device__ __forceinline__ int64_t fdiv(int64_t x, const FDiv& f) {
-  return (f.m && (uint64_t)x <= 0xffffffffull) ? (int64_t)__umul64hi((uint64_t)x, f.m) : x / f.d;
+  // floor(x * m / 2^64) for x < 2^32 in two 32-bit multiplies: x * m_hi
+  // (m < 2^63, so no overflow) plus the high word of x * m_lo, shifted
+  if (f.m && (uint64_t)x <= 0xffffffffull) {
+    const uint32_t x32 = (uint32_t)x;
+    return (int64_t)(((uint64_t)x32 * (uint32_t)(f.m >> 32) + __umulhi(x32, (uint32_t)f.m)) >> 32);
+  }
+  return x / f.d;
 }
 
 struct TableArgs {
@@ -161,6 +167,7 @@ struct TableArgs {
   const double* cb;             // [k*kH]  (0 for dummy units)
   const double* wprime;         // [k*kH]  w2*std/k (0 for dummy units)
   int n_ib;                     // inner blocks of kInnerBlock inners
+  int idx32;                    // every outer / inner table index of this build < 2^31 (32-bit index math)
   int64_t o_lo, o_card, c_in, c_in_pad;   // o_card = number of outer configurations
   // two-level split of each table: entry = const * P_hi[index / nlo] * P_lo[index % nlo]
   const double *PoH, *PoL, *PiH, *PiL;    // [k*kH][n_hi] / [k*kH][n_lo]
@@ -178,7 +185,7 @@ struct PartialJobs {             // k_table_partial4: four (parameter range, sub
   FDiv f_count[4];
   double* out[4];
 };
-__global__ void k_table_partial4(TableArgs t, PartialJobs j);
+__global__ void k_table_partial4(const __grid_constant__ TableArgs t, const __grid_constant__ PartialJobs j);
 __global__ void k_table_outer(TableArgs t);
 struct CkList {
   int n;

@@ -46,23 +46,12 @@ __global__ void k_table_factors(TableArgs t) {
   }
 }
 
-// digits of the sub-index `id` over parameters [p_lo, p_hi) (last fastest)
-__device__ __forceinline__ void sub_digits(const TableArgs& t, uint64_t id, int p_lo, int p_hi, int (&dig)[kMaxP]) {
-#pragma unroll
-  for (int p = kMaxP - 1; p >= 0; --p) {
-    dig[p] = 0;
-    if (p >= p_lo && p < p_hi) {
-      const uint64_t q = (uint64_t)fdiv((int64_t)id, t.f_radix[p]);
-      dig[p] = (int)(id - q * (uint64_t)t.radix[p]);
-      id = q;
-    }
-  }
-}
-
 // Partial products of the factor rows over a parameter range:
 //   P[mj][q] = prod_{p in [p_lo, p_hi)} F[mj][foff[p] + digit_p(base + q)]
-// where digits are those of the sub-index over [p_lo, p_hi) (last fastest).
+// where digits are those of the sub-index over [p_lo, p_hi) (last fastest),
+// multiplied from the last parameter down (fp64; the tables are fp32).
 // Every table entry is then ca|cb * P_hi * P_lo: two fp64 multiplies.
+
 // x / d for non-negative operands, in 32 bits when both fit (a 64-bit
 // division is a ~60-instruction sequence; these index splits run per thread)
 __device__ __forceinline__ int64_t udiv(int64_t x, int64_t d) {
@@ -71,32 +60,30 @@ __device__ __forceinline__ int64_t udiv(int64_t x, int64_t d) {
 
 // The four partial-product tables of one build (outer hi / lo, inner hi / lo)
 // in ONE launch: each is a few tens of thousands of entries, so four launches
-// cost ~10 us each in launch latency and tails.
-__global__ void k_table_partial4(TableArgs t, PartialJobs j) {
-  // (jobs are selected with compare chains, not by indexing the parameter
-  // arrays with a runtime index, which would copy them to local memory)
+// cost ~10 us each in launch latency and tails. Both arguments are
+// __grid_constant__: the job fields and the per-parameter radix / offset /
+// divisor arrays are indexed at run time straight from the parameter bank,
+// so each entry walks only its own job's parameters (a loop unrolled over all
+// kMaxP parameters with predicates cost ~1,460 instructions per entry).
+__global__ void k_table_partial4(const __grid_constant__ TableArgs t, const __grid_constant__ PartialJobs j) {
   const int KH = t.k * kH;
   const int64_t e0 = KH * j.count[0], e1 = e0 + KH * j.count[1], e2 = e1 + KH * j.count[2],
                 tot = e2 + KH * j.count[3];
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < tot; q += (int64_t)gridDim.x * blockDim.x) {
     const int r = q < e0 ? 0 : (q < e1 ? 1 : (q < e2 ? 2 : 3));
     const int64_t off = q - (r == 0 ? 0 : (r == 1 ? e0 : (r == 2 ? e1 : e2)));
-    const int64_t count = r == 0 ? j.count[0] : (r == 1 ? j.count[1] : (r == 2 ? j.count[2] : j.count[3]));
-    const FDiv fc = r == 0 ? j.f_count[0] : (r == 1 ? j.f_count[1] : (r == 2 ? j.f_count[2] : j.f_count[3]));
-    const int64_t base = r == 0 ? j.base[0] : (r == 1 ? j.base[1] : (r == 2 ? j.base[2] : j.base[3]));
-    const int p_lo = r == 0 ? j.p_lo[0] : (r == 1 ? j.p_lo[1] : (r == 2 ? j.p_lo[2] : j.p_lo[3]));
-    const int p_hi = r == 0 ? j.p_hi[0] : (r == 1 ? j.p_hi[1] : (r == 2 ? j.p_hi[2] : j.p_hi[3]));
-    double* out = r == 0 ? j.out[0] : (r == 1 ? j.out[1] : (r == 2 ? j.out[2] : j.out[3]));
-    const int64_t mj64 = fdiv(off, fc);
+    const int64_t mj64 = fdiv(off, j.f_count[r]);
     const int mj = (int)mj64;
-    int dig[kMaxP];
-    sub_digits(t, (uint64_t)(base + (off - mj64 * count)), p_lo, p_hi, dig);
+    uint64_t id = (uint64_t)(j.base[r] + (off - mj64 * j.count[r]));
     const double* Fj = t.F + (size_t)mj * t.foff[t.d];
+    // digits of the sub-index over [p_lo, p_hi), last parameter fastest
     double e = 1.0;
-#pragma unroll
-    for (int p = 0; p < kMaxP; ++p)
-      if (p >= p_lo && p < p_hi) e *= __ldg(Fj + t.foff[p] + dig[p]);
-    out[off] = e;
+    for (int p = j.p_hi[r] - 1; p >= j.p_lo[r]; --p) {
+      const uint64_t qt = (uint64_t)fdiv((int64_t)id, t.f_radix[p]);
+      e *= __ldg(Fj + t.foff[p] + (int)(id - qt * (uint64_t)t.radix[p]));
+      id = qt;
+    }
+    j.out[r][off] = e;
   }
 }
 
@@ -106,22 +93,29 @@ __global__ void k_table_partial4(TableArgs t, PartialJobs j) {
 // reads of a warp share rows; one thread per (block, position) writing float4s
 // was slower, 22 -> 40 us on the 10^8 space, its loads stride over positions).
 // Row o = o_lo + ob*kOB + r = (o / nlo) * nlo + o % nlo over the outer split.
-__global__ void k_table_outer(TableArgs t) {
+template <typename I>   // index type: uint32_t when every index of the build fits (TableArgs::idx32)
+__device__ __forceinline__ void table_outer(const TableArgs& t) {
   const int KH = t.k * kH;
-  const int64_t total = (int64_t)t.n_ob * KH * kOB;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+  const I total = (I)t.n_ob * KH * kOB, stride = (I)gridDim.x * blockDim.x;
+  for (I q = (I)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
     const int r = (int)(q % kOB);
-    const int64_t q8 = q / kOB, ob = fdiv(q8, t.f_kh);
+    const I q8 = q / kOB, ob = (I)fdiv((int64_t)q8, t.f_kh);
     const int mj = (int)(q8 - ob * KH);
-    const int64_t o = t.o_lo + ob * kOB + r;
+    const I o = (I)t.o_lo + ob * kOB + r;
     float out = 1.0f;
-    if (o < t.o_card && t.wprime[mj] != 0.0) {
-      const int64_t oh = fdiv(o, t.f_onlo);
-      const int64_t a = oh - t.o_hi_base, b = o - oh * t.o_nlo;
+    if ((int64_t)o < t.o_card && t.wprime[mj] != 0.0) {
+      const I oh = (I)fdiv((int64_t)o, t.f_onlo);
+      const I a = oh - (I)t.o_hi_base, b = o - oh * (I)t.o_nlo;
       out = (float)(t.ca[mj] * __ldg(t.PoH + (size_t)mj * t.o_nhi + a) * __ldg(t.PoL + (size_t)mj * t.o_nlo + b));
     }
     t.ea[q] = out;
   }
+}
+__global__ void k_table_outer(TableArgs t) {
+  if (t.idx32)
+    table_outer<uint32_t>(t);
+  else
+    table_outer<int64_t>(t);
 }
 
 // Extremes of the inner part per (table position, inner block): over the
@@ -237,24 +231,24 @@ __global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* 
 // + thread; pad slots are zero): one thread per (inner block, group, thread)
 // computes its 4*ebw slots and writes them as float4s -- consecutive threads
 // write consecutive 16-byte chunks and read consecutive PiL entries.
-template <int G>
-__global__ void k_table_inner(TableArgs t) {
+template <int G, typename I>
+__device__ __forceinline__ void table_inner(const TableArgs& t) {
   constexpr int W = ebw_of(G), WF = 4 * W;
   const int ngroups = t.k * kH / G;
-  const int64_t total = (t.c_in_pad / kInnerBlock) * (int64_t)ngroups * kThreads;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+  const I total = (I)(t.c_in_pad / kInnerBlock) * ngroups * kThreads, stride = (I)gridDim.x * blockDim.x;
+  for (I q = (I)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
     const int th = (int)(q % kThreads);
-    const int64_t rest = q / kThreads;
-    const int64_t ib = fdiv(rest, t.f_ngroups);
+    const I rest = q / kThreads;
+    const I ib = (I)fdiv((int64_t)rest, t.f_ngroups);
     const int gi = (int)(rest - ib * ngroups);
-    int64_t a[kInner], b[kInner];
+    I a[kInner], b[kInner];
     bool in[kInner];
 #pragma unroll
     for (int s = 0; s < kInner; ++s) {
-      const int64_t i = ib * kInnerBlock + (int64_t)s * kThreads + th;
-      in[s] = i < t.c_in;
-      a[s] = fdiv(i, t.f_inlo);
-      b[s] = i - a[s] * t.i_nlo;
+      const I i = ib * kInnerBlock + (I)s * kThreads + th;
+      in[s] = (int64_t)i < t.c_in;
+      a[s] = (I)fdiv((int64_t)i, t.f_inlo);
+      b[s] = i - a[s] * (I)t.i_nlo;
     }
     float out[WF];
 #pragma unroll
@@ -271,6 +265,13 @@ __global__ void k_table_inner(TableArgs t) {
 #pragma unroll
     for (int w = 0; w < W; ++w) dst[w] = make_float4(out[4 * w], out[4 * w + 1], out[4 * w + 2], out[4 * w + 3]);
   }
+}
+template <int G>
+__global__ void k_table_inner(TableArgs t) {
+  if (t.idx32)
+    table_inner<G, uint32_t>(t);
+  else
+    table_inner<G, int64_t>(t);
 }
 
 // ---------------------------------------------------------------------------
