@@ -509,6 +509,7 @@ struct BandSetup {
   double mag = 0;               // sum |w'| + dummies + |cst|: scale of every partial sum
   double* d_tab = nullptr;      // [ca | cb | wprime] (k*kH each)
   std::vector<float> u;         // [k*kH] 1/w' (the sweep's parameter block, SweepArgs::uc)
+  std::vector<double> wabs;     // [k*kH] |w'| per table position, 1 for dummy units
 };
 }  // namespace
 
@@ -692,6 +693,8 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   CU(cudaMallocAsync(&b.d_tab, tab.size() * 8, c->stream));
   TRY(upload_pinned(c, b.d_tab, tab.data(), tab.size() * 8));
   b.u = std::move(u);
+  b.wabs.resize(KH);
+  for (int q = 0; q < KH; ++q) b.wabs[q] = wpv[q] != 0.0 ? std::fabs(wpv[q]) : 1.0;
   b.ok = true;
   return MLT_OK;
 }
@@ -1332,6 +1335,11 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
           ++ck.n;
         }
       }
+      for (int q = 0; q < ck.n; ++q) {
+        double m = 0.0;
+        for (int pos = KH - 1; pos >= ck.unit[q]; --pos) m += B.wabs[pos];
+        ck.mag[q] = m;
+      }
     }
     const size_t n_remlo = prune ? (size_t)n_ob * kOB * n_ib * ck.n : 0;
     const int64_t key[5] = {B.split, B.G, o_lo, n_ob, prune ? 1 : 0};
@@ -1461,14 +1469,12 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
         ta.n_ib = n_ib;
         k_table_ebext<<<grid_for(c, (int64_t)KH * n_ib * 32, 256), 256, 0, c->stream>>>(ta, ext);
         TRY(check_launch(c));
-        double* seg;
-        const int64_t rows_ib = (int64_t)n_ob * kOB * n_ib;
-        CU(cudaMallocAsync(&seg, (size_t)rows_ib * ck.n * 8, c->stream));
-        k_table_remseg<<<grid_for(c, rows_ib * ck.n, 256), 256, 0, c->stream>>>(ta, ck, ext, seg);
+        // CTAs stride over the outer rows (k_table_rem: 256 threads, 22 KB of
+        // shared memory, 6 resident per SM: one wave)
+        const int64_t rows = (int64_t)n_ob * kOB;
+        k_table_rem<<<(int)std::min<int64_t>(rows, (int64_t)c->sms * 6), 256, 0, c->stream>>>(ta, ck, ext,
+                                                                                            p->t_remlo);
         TRY(check_launch(c));
-        k_table_remlo<<<grid_for(c, rows_ib, 256), 256, 0, c->stream>>>(ta, ck, seg, p->t_remlo);
-        TRY(check_launch(c));
-        CU(cudaFreeAsync(seg, c->stream));
         // best-first order of the work items: by the smallest whole-item lower
         // bound, sorted on the device (a stable radix sort: ties keep index order)
         const int items = n_ob * n_ib;

@@ -190,11 +190,11 @@ __global__ void k_table_outer(TableArgs t);
 struct CkList {
   int n;
   int unit[kMaxCk];             // first table position still to come at checkpoint c
+  double mag[kMaxCk];           // sum over positions >= unit[c] of |w'| (1 for dummy units)
 };
 __global__ void k_table_ebext(TableArgs t, double* ext);
 __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, float* keys, int* vals);
-__global__ void k_table_remseg(TableArgs t, CkList ck, const double* ext, double* seg);
-__global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* remlo);
+__global__ void k_table_rem(TableArgs t, CkList ck, const double* ext, float* remlo);
 template <int G>
 __global__ void k_table_inner(TableArgs t);
 

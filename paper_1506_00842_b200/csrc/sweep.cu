@@ -174,54 +174,120 @@ __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, f
 //   remlo[o][ib][c] = sum_{pos >= ck.unit[c]} min over the block's inners of w'*sigmoid(z)
 // = w' / (1 + Ea64(o) * ext(pos, ib)) in fp64 (dummy units contribute exactly 1),
 // rounded down with a safety margin so it stays a bound.
-// Two passes. k_table_remseg: one thread per (outer row, checkpoint interval,
-// inner block), inner block fastest (coalesced ext loads, broadcast outer
-// factors), sums the units between checkpoints c and c + 1 into
-// seg[c][row * n_ib + ib] (fp64). k_table_remlo: one thread per (row, inner
-// block) suffix-sums its intervals and rounds each checkpoint's bound down
-// with a 1e-9 margin (which dwarfs the fp64 summation-order error of <= 480
-// terms).
-__global__ void k_table_remseg(TableArgs t, CkList ck, const double* ext, double* seg) {
-  const int n_ck = ck.n;
-  const int KH = t.k * kH;
-  const int64_t rows_ib = (int64_t)t.n_ob * kOB * t.n_ib;
-  const int64_t total = rows_ib * n_ck;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q1 = udiv(q, t.n_ib);
-    const int ib = (int)(q - q1 * t.n_ib);
-    const int64_t row = udiv(q1, n_ck);
-    const int c = (int)(q1 - row * n_ck);
-    const int64_t o = t.o_lo + row;
-    double acc = 0.0;
-    if (o < t.o_card) {
-      const int64_t oh = udiv(o, t.o_nlo);
-      const int64_t a = oh - t.o_hi_base, b = o - oh * t.o_nlo;
-      const int u1 = c + 1 < n_ck ? ck.unit[c + 1] : KH;
-      for (int pos = ck.unit[c]; pos < u1; ++pos) {
-        const double wp = t.wprime[pos];
-        double lo = 1.0;
-        if (wp != 0.0) {
-          const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) * __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
-          lo = wp / (1.0 + ea * __ldg(ext + (size_t)pos * t.n_ib + ib));
-        }
-        acc += lo;
-      }
-    }
-    seg[(size_t)c * rows_ib + row * t.n_ib + ib] = acc;
-  }
+// CTAs stride over the outer rows: exp(-A') of each position is formed once
+// per row (not once per inner block), and the row's terms go through shared
+// memory in chunks of 256 positions x 8 inner blocks, last chunk first. Warp w
+// owns inner block w: lane l sums positions [8l, 8l + 8) of the chunk from the
+// last one down, a reverse warp scan adds the later runs and a carry the later
+// chunks, and the lane holding a checkpoint's first unit u writes its bound --
+// the suffix sum over [u, KH) -- straight from registers. Each bound is rounded
+// down by 1e-9 (1 + |sum|) + 1e-12 sum_{pos >= u} |w'| (CkList::mag; every
+// term is at most |w'| in magnitude, a dummy unit's exactly 1), which covers the fp64 error of summing
+// <= 4096 terms in any order plus the 2-ulp reciprocal below, whatever the
+// cancellation. (Round 2's thread per (row, interval, block) with a serial
+// loop of dependent loads and divisions: ~250 us on the 10^8 space,
+// profiles/r02_launches_bench_summary.txt.)
+namespace {
+constexpr int kRemIB = 8;        // inner blocks per pass = warps per CTA
+constexpr int kRemChunk = 256;   // positions per pass = threads per CTA
+// 1/d for 1 <= d <= 2^100: a MUFU estimate and two Newton steps in fp64
+// (2^-23 -> 2^-46 -> rounding): within 2 ulp of the correctly rounded quotient
+__device__ __forceinline__ double rcp_newton(double d) {
+  float rf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)d));
+  double r = (double)rf;
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
 }
+}  // namespace
 
-__global__ void k_table_remlo(TableArgs t, CkList ck, const double* seg, float* remlo) {
-  const int n_ck = ck.n;
-  const int64_t rows_ib = (int64_t)t.n_ob * kOB * t.n_ib;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows_ib; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = t.o_lo + q / t.n_ib;
-    float* out = remlo + q * n_ck;
-    double acc = 0.0;
-    for (int c = n_ck - 1; c >= 0; --c) {
-      acc += seg[(size_t)c * rows_ib + q];
-      out[c] = o < t.o_card ? __double2float_rd(acc - 1e-9 * (1.0 + fabs(acc)))
-                            : __int_as_float(0x7f800000);   // no configuration: prune freely
+__global__ void __launch_bounds__(kRemChunk) k_table_rem(TableArgs t, CkList ck, const double* ext,
+                                                           float* remlo) {
+  // s_term[ib][p + p / 8]: one pad slot per 8 positions, so the lanes of a
+  // warp reading position 8l + j of their own run hit distinct bank pairs
+  constexpr int kLd = kRemChunk + kRemChunk / 8;
+  __shared__ double s_term[kRemIB][kLd];
+  __shared__ signed char s_ckat[kMaxUnitsParam];  // checkpoint whose first unit is pos, or -1
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int KH = t.k * kH, n_ck = ck.n, n_ib = t.n_ib;
+  const int64_t rows = (int64_t)t.n_ob * kOB;
+  for (int q = tid; q < KH; q += blockDim.x) s_ckat[q] = -1;
+  __syncthreads();
+  if (tid < n_ck) s_ckat[ck.unit[tid]] = (signed char)tid;
+  __syncthreads();
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t o = t.o_lo + row;
+    float* out = remlo + row * n_ib * n_ck;
+    if (o >= t.o_card) {   // no configuration: prune freely (uniform over the CTA)
+      for (int q = tid; q < n_ib * n_ck; q += blockDim.x) out[q] = __int_as_float(0x7f800000);
+      continue;
+    }
+    const int64_t oh = udiv(o, t.o_nlo);
+    const int64_t a = oh - t.o_hi_base, b = o - oh * t.o_nlo;
+    for (int ib0 = 0; ib0 < n_ib; ib0 += kRemIB) {
+      const int nb = min(kRemIB, n_ib - ib0);
+      double carry = 0.0;   // warp `warp`: the sum over the chunks done (all later positions)
+      for (int base = (KH - 1) / kRemChunk * kRemChunk; base >= 0; base -= kRemChunk) {
+        const int pos = base + tid;
+        if (pos < KH) {
+          // every load up front, then kRemIB independent chains; d >= 2^100
+          // leaves a term below 2^-100 |w'| -- 0 for w' > 0, w' * 2^-100 for
+          // w' < 0, both still lower bounds, and no branch
+          const double wp = t.wprime[pos];
+          const double* ex = ext + (size_t)pos * n_ib + ib0;
+          double e8[kRemIB];
+#pragma unroll
+          for (int x = 0; x < kRemIB; ++x) e8[x] = x < nb ? __ldg(ex + x) : 0.0;
+          const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) *
+                            __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
+          double* st = &s_term[0][tid + tid / 8];
+#pragma unroll
+          for (int x = 0; x < kRemIB; ++x) {
+            if (x < nb) {
+              const double d = 1.0 + ea * e8[x];
+              const double term = (wp > 0.0 && !(d < 0x1p100)) ? 0.0 : wp * rcp_newton(fmin(d, 0x1p100));
+              st[x * kLd] = wp == 0.0 ? 1.0 : term;
+            }
+          }
+        }
+        __syncthreads();
+        if (warp < nb) {
+          // lane run [p0, p0 + 8) of the chunk (positions >= KH count as 0)
+          const int p0 = 8 * lane;
+          const double* sw = &s_term[warp][p0 + lane];   // (p0 + j) + (p0 + j) / 8 = p0 + lane + j
+          double suf[8], run = 0.0;
+#pragma unroll
+          for (int j = 7; j >= 0; --j) {
+            run += base + p0 + j < KH ? sw[j] : 0.0;
+            suf[j] = run;
+          }
+          double inc = run;   // inclusive reverse scan over the lanes
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, inc, off);
+            if (lane + off < 32) inc += y;
+          }
+          const double after = inc - run + carry;
+          carry += __shfl_sync(0xffffffffu, inc, 0);   // the whole chunk
+          // checkpoints whose first unit lies in this run (at most a few)
+          const int pb = base + p0;
+          if (pb < KH) {
+            const int ck8 = min(8, KH - pb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int c = j < ck8 ? s_ckat[pb + j] : -1;
+              if (c >= 0) {
+                const double sum = suf[j] + after;
+                out[(ib0 + warp) * n_ck + c] =
+                    __double2float_rd(sum - 1e-9 * (1.0 + fabs(sum)) - 1e-12 * ck.mag[c]);
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
     }
   }
 }
