@@ -485,3 +485,32 @@ def test_wide_ensembles_against_oracle():
         assert st["path"] == (0 if k <= 100 else 1), (k, st)
         assert np.array_equal(idx, oi), (k, m)
         np.testing.assert_allclose(pred, op, rtol=PRED_RTOL, atol=0)
+
+
+def test_pruning_bounds_on_wide_and_long_shapes():
+    """The pruning-bound kernel (k_table_rem) in its less common shapes, with
+    pruning on and the tables rebuilt, against the oracle's lexsort
+    (tuner.py:110-130): a 40-member ensemble (1200 table positions: five
+    256-position chunks) and a space whose last parameter has 20,000 values
+    (ten 2048-inner blocks: two passes of eight), every m from 1 to 500."""
+    import paper_1506_00842_b200 as b
+    from oracle.tuner import top_m as otop
+    from paper_1506_00842_b200.space import ParamDef, ParamSpace
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    set_opt(N.MLT_OPT_PRUNE, 1)
+    rng = np.random.default_rng(17)
+    long_space = ParamSpace("long", (ParamDef("a", (1, 2, 3)), ParamDef("b", tuple(range(1, 20001)))), ())
+    cases = [(product_space("stereo"), 40, 0, 1 << 19), (long_space, 4, 0, 60000)]
+    for sp, k, lo, hi in cases:
+        d = len(sp.params)
+        nets = [b.Network(rng.normal(size=(30, d)), rng.normal(size=30), rng.normal(size=30),
+                          float(rng.normal()), float(rng.normal()), float(rng.uniform(0.2, 2))) for _ in range(k)]
+        ens = b.Ensemble(nets, b.Encoder.from_space(sp), sp.name)
+        osp, oens = _oracle_from(sp, ens)
+        for m in (1, 37, 500):
+            oi, op = otop(oens, osp, m, begin=lo, end=hi)
+            idx, pred, st = top_m_arrays(ens, sp, m, begin=lo, end=hi, with_stats=True)
+            assert st["path"] == 0, (sp.name, k, m, st)
+            assert np.array_equal(idx, oi), (sp.name, k, m)
+            np.testing.assert_allclose(pred, op, rtol=PRED_RTOL, atol=0)
