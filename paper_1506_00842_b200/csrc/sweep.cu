@@ -138,8 +138,9 @@ __global__ void k_table_ebext(TableArgs t, double* ext) {
       double mx = 0.0, mn = INFINITY;
       const int64_t i0 = (int64_t)ib * kInnerBlock;
       const int64_t i1 = i0 + kInnerBlock < t.c_in ? i0 + kInnerBlock : t.c_in;
+#pragma unroll 4
       for (int64_t i = i0 + lane; i < i1; i += 32) {
-        const int64_t ih = udiv(i, t.i_nlo);
+        const int64_t ih = fdiv(i, t.f_inlo);
         const double v = base * __ldg(t.PiH + (size_t)pos * t.i_nhi + ih) *
                          __ldg(t.PiL + (size_t)pos * t.i_nlo + (i - ih * t.i_nlo));
         mx = fmax(mx, v);
