@@ -191,12 +191,12 @@ __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, f
 namespace {
 constexpr int kRemIB = 8;        // inner blocks per pass = warps per CTA
 constexpr int kRemChunk = 256;   // positions per pass = threads per CTA
-// 1/d for 1 <= d <= 2^100: a MUFU estimate and two Newton steps in fp64
-// (2^-23 -> 2^-46 -> rounding): within 2 ulp of the correctly rounded quotient
+// 1/d for 1 <= d <= 2^100: the MUFU fp64 reciprocal estimate (MUFU.RCP64H,
+// ~2^-20) and two Newton steps (-> 2^-40 -> rounding): within 2 ulp of the
+// correctly rounded quotient, with no fp32 round trip through the converter
 __device__ __forceinline__ double rcp_newton(double d) {
-  float rf;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)d));
-  double r = (double)rf;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
   double e = fma(-d, r, 1.0);
   r = fma(r, e, r);
   e = fma(-d, r, 1.0);
@@ -210,13 +210,18 @@ __global__ void __launch_bounds__(kRemChunk) k_table_rem(TableArgs t, CkList ck,
   // warp reading position 8l + j of their own run hit distinct bank pairs
   constexpr int kLd = kRemChunk + kRemChunk / 8;
   __shared__ double s_term[kRemIB][kLd];
-  __shared__ signed char s_ckat[kMaxUnitsParam];  // checkpoint whose first unit is pos, or -1
+  __shared__ signed char s_ckat[kMaxUnitsParam];       // checkpoint whose first unit is pos, or -1
+  __shared__ __align__(4) unsigned char s_runck[kMaxUnitsParam / 8];  // bit j: a checkpoint starts at pos 8 run + j
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int KH = t.k * kH, n_ck = ck.n, n_ib = t.n_ib;
   const int64_t rows = (int64_t)t.n_ob * kOB;
   for (int q = tid; q < KH; q += blockDim.x) s_ckat[q] = -1;
+  for (int q = tid; q < (KH + 31) / 32; q += blockDim.x) reinterpret_cast<unsigned int*>(s_runck)[q] = 0u;
   __syncthreads();
-  if (tid < n_ck) s_ckat[ck.unit[tid]] = (signed char)tid;
+  if (tid < n_ck) {
+    s_ckat[ck.unit[tid]] = (signed char)tid;
+    atomicOr(reinterpret_cast<unsigned int*>(s_runck) + ck.unit[tid] / 32, 1u << (ck.unit[tid] % 32));
+  }
   __syncthreads();
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     const int64_t o = t.o_lo + row;
@@ -244,12 +249,17 @@ __global__ void __launch_bounds__(kRemChunk) k_table_rem(TableArgs t, CkList ck,
           const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) *
                             __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
           double* st = &s_term[0][tid + tid / 8];
+          if (wp == 0.0) {   // dummy unit: exactly 1
 #pragma unroll
-          for (int x = 0; x < kRemIB; ++x) {
-            if (x < nb) {
-              const double d = 1.0 + ea * e8[x];
-              const double term = (wp > 0.0 && !(d < 0x1p100)) ? 0.0 : wp * rcp_newton(fmin(d, 0x1p100));
-              st[x * kLd] = wp == 0.0 ? 1.0 : term;
+            for (int x = 0; x < kRemIB; ++x)
+              if (x < nb) st[x * kLd] = 1.0;
+          } else {
+#pragma unroll
+            for (int x = 0; x < kRemIB; ++x) {
+              if (x < nb) {
+                const double d = 1.0 + ea * e8[x];
+                st[x * kLd] = (wp > 0.0 && !(d < 0x1p100)) ? 0.0 : wp * rcp_newton(fmin(d, 0x1p100));
+              }
             }
           }
         }
@@ -272,19 +282,19 @@ __global__ void __launch_bounds__(kRemChunk) k_table_rem(TableArgs t, CkList ck,
           }
           const double after = inc - run + carry;
           carry += __shfl_sync(0xffffffffu, inc, 0);   // the whole chunk
-          // checkpoints whose first unit lies in this run (at most a few)
+          // the checkpoints whose first unit lies in this run (usually none or
+          // one: a loop over the set bits, suf[j] picked by a select chain)
           const int pb = base + p0;
-          if (pb < KH) {
-            const int ck8 = min(8, KH - pb);
+          unsigned mask = pb < KH ? s_runck[pb / 8] : 0u;
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            double sj = suf[0];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int c = j < ck8 ? s_ckat[pb + j] : -1;
-              if (c >= 0) {
-                const double sum = suf[j] + after;
-                out[(ib0 + warp) * n_ck + c] =
-                    __double2float_rd(sum - 1e-9 * (1.0 + fabs(sum)) - 1e-12 * ck.mag[c]);
-              }
-            }
+            for (int q = 1; q < 8; ++q) sj = j == q ? suf[q] : sj;
+            const int c = s_ckat[pb + j];
+            const double sum = sj + after;
+            out[(ib0 + warp) * n_ck + c] = __double2float_rd(sum - 1e-9 * (1.0 + fabs(sum)) - 1e-12 * ck.mag[c]);
           }
         }
         __syncthreads();
