@@ -237,41 +237,48 @@ __global__ void __launch_bounds__(kRemChunk) k_table_rem(TableArgs t, CkList ck,
       double carry = 0.0;   // warp `warp`: the sum over the chunks done (all later positions)
       for (int base = (KH - 1) / kRemChunk * kRemChunk; base >= 0; base -= kRemChunk) {
         const int pos = base + tid;
-        if (pos < KH) {
+        double* st = &s_term[0][tid + tid / 8];
+        if (pos >= KH) {   // past the last position: zero terms, so the sums need no guard
+#pragma unroll
+          for (int x = 0; x < kRemIB; ++x)
+            if (x < nb) st[x * kLd] = 0.0;
+        } else {
           // every load up front, then kRemIB independent chains; d >= 2^100
           // leaves a term below 2^-100 |w'| -- 0 for w' > 0, w' * 2^-100 for
           // w' < 0, both still lower bounds, and no branch
           const double wp = t.wprime[pos];
           const double* ex = ext + (size_t)pos * n_ib + ib0;
-          double e8[kRemIB];
-#pragma unroll
-          for (int x = 0; x < kRemIB; ++x) e8[x] = x < nb ? __ldg(ex + x) : 0.0;
           const double ea = t.ca[pos] * __ldg(t.PoH + (size_t)pos * t.o_nhi + a) *
                             __ldg(t.PoL + (size_t)pos * t.o_nlo + b);
-          double* st = &s_term[0][tid + tid / 8];
+          auto term = [&](double e) {
+            const double d = 1.0 + ea * e;
+            return (wp > 0.0 && !(d < 0x1p100)) ? 0.0 : wp * rcp_newton(fmin(d, 0x1p100));
+          };
           if (wp == 0.0) {   // dummy unit: exactly 1
 #pragma unroll
             for (int x = 0; x < kRemIB; ++x)
               if (x < nb) st[x * kLd] = 1.0;
+          } else if (nb == kRemIB) {   // (uniform) all eight blocks: no predicates
+            double e8[kRemIB];
+#pragma unroll
+            for (int x = 0; x < kRemIB; ++x) e8[x] = __ldg(ex + x);
+#pragma unroll
+            for (int x = 0; x < kRemIB; ++x) st[x * kLd] = term(e8[x]);
           } else {
 #pragma unroll
-            for (int x = 0; x < kRemIB; ++x) {
-              if (x < nb) {
-                const double d = 1.0 + ea * e8[x];
-                st[x * kLd] = (wp > 0.0 && !(d < 0x1p100)) ? 0.0 : wp * rcp_newton(fmin(d, 0x1p100));
-              }
-            }
+            for (int x = 0; x < kRemIB; ++x)
+              if (x < nb) st[x * kLd] = term(__ldg(ex + x));
           }
         }
         __syncthreads();
         if (warp < nb) {
-          // lane run [p0, p0 + 8) of the chunk (positions >= KH count as 0)
+          // lane run [p0, p0 + 8) of the chunk (positions >= KH hold 0)
           const int p0 = 8 * lane;
           const double* sw = &s_term[warp][p0 + lane];   // (p0 + j) + (p0 + j) / 8 = p0 + lane + j
           double suf[8], run = 0.0;
 #pragma unroll
           for (int j = 7; j >= 0; --j) {
-            run += base + p0 + j < KH ? sw[j] : 0.0;
+            run += sw[j];
             suf[j] = run;
           }
           double inc = run;   // inclusive reverse scan over the lanes
