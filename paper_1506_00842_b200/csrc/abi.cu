@@ -1485,20 +1485,27 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
           CU(cudaMallocAsync(&p->t_order, (size_t)items * 4, c->stream));
           p->t_order_cap = items;
         }
-        float *kin, *kout;
-        int* vin;
-        void* tmp = nullptr;
-        size_t tmp_bytes = 0;
-        CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const float*)nullptr, (float*)nullptr,
-                                           (const int*)nullptr, (int*)nullptr, items, 0, 32, c->stream));
-        CU(cudaMallocAsync(&kin, (size_t)items * 4, c->stream));
-        CU(cudaMallocAsync(&kout, (size_t)items * 4, c->stream));
-        CU(cudaMallocAsync(&vin, (size_t)items * 4, c->stream));
-        CU(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), c->stream));
-        k_item_keys<<<grid_for(c, items, 256), 256, 0, c->stream>>>(p->t_remlo, ck.n, n_ib, items, kin, vin);
-        TRY(check_launch(c));
-        CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, p->t_order, items, 0, 32, c->stream));
-        for (void* q : {(void*)kin, (void*)kout, (void*)vin, tmp}) CU(cudaFreeAsync(q, c->stream));
+        if (items <= kItemSortMax) {   // one CTA (the 10^8 space: 6144 items)
+          const size_t smem = item_order_smem();
+          TRY(kernel_smem(c, k_item_order, kItemSortThreads, smem));
+          k_item_order<<<1, kItemSortThreads, smem, c->stream>>>(p->t_remlo, ck.n, n_ib, items, p->t_order);
+          TRY(check_launch(c));
+        } else {
+          float *kin, *kout;
+          int* vin;
+          void* tmp = nullptr;
+          size_t tmp_bytes = 0;
+          CU(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const float*)nullptr, (float*)nullptr,
+                                             (const int*)nullptr, (int*)nullptr, items, 0, 32, c->stream));
+          CU(cudaMallocAsync(&kin, (size_t)items * 4, c->stream));
+          CU(cudaMallocAsync(&kout, (size_t)items * 4, c->stream));
+          CU(cudaMallocAsync(&vin, (size_t)items * 4, c->stream));
+          CU(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), c->stream));
+          k_item_keys<<<grid_for(c, items, 256), 256, 0, c->stream>>>(p->t_remlo, ck.n, n_ib, items, kin, vin);
+          TRY(check_launch(c));
+          CU(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, p->t_order, items, 0, 32, c->stream));
+          for (void* q : {(void*)kin, (void*)kout, (void*)vin, tmp}) CU(cudaFreeAsync(q, c->stream));
+        }
       }
       std::copy(key, key + 5, p->t_key);
     }

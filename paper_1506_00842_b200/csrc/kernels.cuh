@@ -194,6 +194,10 @@ struct CkList {
 };
 __global__ void k_table_ebext(TableArgs t, double* ext);
 __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, float* keys, int* vals);
+constexpr int kItemSortThreads = 1024, kItemSortPer = 8, kItemSortMax = kItemSortThreads * kItemSortPer;
+constexpr int kItemSortBits = 4;   // radix digit width of k_item_order's passes (8 spills to local memory)
+__global__ void k_item_order(const float* remlo, int n_ck, int n_ib, int items, int* order);
+size_t item_order_smem();   // dynamic shared memory of k_item_order (cub::BlockRadixSort storage)
 __global__ void k_table_rem(TableArgs t, CkList ck, const double* ext, float* remlo);
 template <int G>
 __global__ void k_table_inner(TableArgs t);

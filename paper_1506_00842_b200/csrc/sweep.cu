@@ -20,6 +20,8 @@
 // lexsort((indices, preds)) selection exactly.
 #include "kernels.cuh"
 
+#include <cub/block/block_radix_sort.cuh>
+
 namespace mlt {
 
 // ---------------------------------------------------------------------------
@@ -169,6 +171,42 @@ __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, f
     keys[w] = mn;
     vals[w] = w;
   }
+}
+
+// Up to kItemSortMax work items: keys (as k_item_keys) and their stable
+// ascending order in ONE CTA (cub::BlockRadixSort over 1024 x 8 keys in
+// shared memory) -- the same order as the device-wide radix sort (stable,
+// same key bits), without its six launches and four allocations.
+__global__ void __launch_bounds__(kItemSortThreads) k_item_order(const float* remlo, int n_ck, int n_ib, int items,
+                                                                 int* order) {
+  using Sort = cub::BlockRadixSort<float, kItemSortThreads, kItemSortPer, int, kItemSortBits>;
+  extern __shared__ __align__(16) unsigned char s_sort[];
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(s_sort);
+  float key[kItemSortPer];
+  int val[kItemSortPer];
+#pragma unroll
+  for (int j = 0; j < kItemSortPer; ++j) {
+    const int w = threadIdx.x * kItemSortPer + j;   // blocked arrangement: input rank = item index
+    key[j] = __int_as_float(0x7f800000);
+    val[j] = 0x7fffffff;                           // padding: after every item, +inf ones included
+    if (w < items) {
+      const int ob = w / n_ib, ib = w - ob * n_ib;
+      float mn = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int r = 0; r < kOB; ++r) mn = fminf(mn, __ldg(remlo + (((size_t)ob * kOB + r) * n_ib + ib) * n_ck));
+      key[j] = mn;
+      val[j] = w;
+    }
+  }
+  Sort(tmp).Sort(key, val);
+#pragma unroll
+  for (int j = 0; j < kItemSortPer; ++j) {
+    const int w = threadIdx.x * kItemSortPer + j;
+    if (w < items) order[w] = val[j];
+  }
+}
+size_t item_order_smem() {
+  return sizeof(typename cub::BlockRadixSort<float, kItemSortThreads, kItemSortPer, int, kItemSortBits>::TempStorage);
 }
 
 // Lower bounds of the units still to come, per (outer row, inner block) and checkpoint:

@@ -514,3 +514,25 @@ def test_pruning_bounds_on_wide_and_long_shapes():
             assert st["path"] == 0, (sp.name, k, m, st)
             assert np.array_equal(idx, oi), (sp.name, k, m)
             np.testing.assert_allclose(pred, op, rtol=PRED_RTOL, atol=0)
+
+
+def test_pruned_order_with_many_work_items():
+    """Best-first item order on both sides of the one-CTA sort's capacity
+    (kItemSortMax = 8192 items; larger spaces use the device-wide radix sort):
+    a 4^14 = 2.7e8-configuration space (~16k work items) pruned equals the
+    same space swept in full, whose path the oracle pins on the 10^8 space."""
+    import paper_1506_00842_b200 as b
+    from paper_1506_00842_b200.space import ParamDef, ParamSpace
+    from paper_1506_00842_b200.tuner import top_m_arrays
+    N = _lib()
+    sp = ParamSpace("p4x14", tuple(ParamDef(f"q{i}", (1, 2, 4, 8)) for i in range(14)), ())
+    rng = np.random.default_rng(23)
+    nets = [b.Network(rng.normal(size=(30, 14)), rng.normal(size=30), rng.normal(size=30),
+                      float(rng.normal()), float(rng.normal()), float(rng.uniform(0.2, 2))) for _ in range(2)]
+    ens = b.Ensemble(nets, b.Encoder.from_space(sp), sp.name)
+    full = top_m_arrays(ens, sp, 200)
+    set_opt(N.MLT_OPT_PRUNE, 1)
+    idx, pred, st = top_m_arrays(ens, sp, 200, with_stats=True)
+    assert st["path"] == 0 and st["evaluated_frac"] < 1.0, st
+    assert np.array_equal(idx, full[0])
+    np.testing.assert_array_equal(pred, full[1])
