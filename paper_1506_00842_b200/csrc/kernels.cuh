@@ -194,10 +194,10 @@ struct CkList {
 };
 __global__ void k_table_ebext(TableArgs t, double* ext);
 __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, float* keys, int* vals);
-constexpr int kItemSortThreads = 1024, kItemSortPer = 8, kItemSortMax = kItemSortThreads * kItemSortPer;
-constexpr int kItemSortBits = 4;   // radix digit width of k_item_order's passes (8 spills to local memory)
-__global__ void k_item_order(const float* remlo, int n_ck, int n_ib, int items, int* order);
-size_t item_order_smem();   // dynamic shared memory of k_item_order (cub::BlockRadixSort storage)
+// best-first item order for <= kItemSortMax items: sorted runs, then a rank merge
+constexpr int kItemSortThreads = 1024, kItemSortMax = 8192, kItemRun = 1024, kItemRunThreads = 256;
+__global__ void k_item_runs(const float* remlo, int n_ck, int n_ib, int items, unsigned* run_key, int* run_val);
+__global__ void k_item_merge(const unsigned* run_key, const int* run_val, int items, int* order);
 __global__ void k_table_rem(TableArgs t, CkList ck, const double* ext, float* remlo);
 template <int G>
 __global__ void k_table_inner(TableArgs t);
