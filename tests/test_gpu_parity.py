@@ -517,8 +517,9 @@ def test_pruning_bounds_on_wide_and_long_shapes():
 
 
 def test_pruned_order_with_many_work_items():
-    """Best-first item order on both sides of the one-CTA sort's capacity
-    (kItemSortMax = 8192 items; larger spaces use the device-wide radix sort):
+    """Best-first item order on both sides of the run-and-merge sort's
+    capacity (kItemSortMax = 8192 items; larger spaces use the device-wide
+    radix sort):
     a 4^14 = 2.7e8-configuration space (~16k work items) pruned equals the
     same space swept in full, whose path the oracle pins on the 10^8 space."""
     import paper_1506_00842_b200 as b
