@@ -1485,7 +1485,7 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
           CU(cudaMallocAsync(&p->t_order, (size_t)items * 4, c->stream));
           p->t_order_cap = items;
         }
-        if (items <= kItemSortMax) {   // sorted runs + one-CTA rank merge (the 10^8 space: 6144 items)
+        if (items <= kItemSortMax) {   // sorted runs + rank merge (the 10^8 space: 6144 items)
           unsigned* run_key;
           CU(cudaMallocAsync(&run_key, (size_t)items * 8, c->stream));
           int* run_val = reinterpret_cast<int*>(run_key + items);
@@ -1494,7 +1494,8 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
           TRY(check_launch(c));
           const size_t smem = (size_t)kItemSortMax * 4;
           TRY(kernel_smem(c, k_item_merge, kItemSortThreads, smem));
-          k_item_merge<<<1, kItemSortThreads, smem, c->stream>>>(run_key, run_val, items, p->t_order);
+          k_item_merge<<<(items + kItemSortThreads - 1) / kItemSortThreads, kItemSortThreads, smem, c->stream>>>(
+              run_key, run_val, items, p->t_order);
           TRY(check_launch(c));
           CU(cudaFreeAsync(run_key, c->stream));
         } else {

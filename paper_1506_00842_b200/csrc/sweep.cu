@@ -176,7 +176,8 @@ __global__ void k_item_keys(const float* remlo, int n_ck, int n_ib, int items, f
 // Best-first order of up to kItemSortMax work items in two launches (the
 // device-wide radix sort takes six, plus four allocations): k_item_runs sorts
 // runs of kItemRun items, one CTA each (keys as k_item_keys; a stable
-// cub::BlockRadixSort), and k_item_merge places every item at its rank in the
+// cub::BlockRadixSort), and k_item_merge (a CTA per 1024 items, each with all
+// the keys in shared memory) places every item at its rank in the
 // whole: its position in its run plus, per other run, a binary search for the
 // items ahead of it -- keys compared as cub's order-preserving bits, ties by
 // item index (runs are index-contiguous: an earlier run's equal keys come
@@ -220,11 +221,11 @@ __global__ void __launch_bounds__(kItemRunThreads) k_item_runs(const float* reml
 }
 __global__ void __launch_bounds__(kItemSortThreads) k_item_merge(const unsigned* run_key, const int* run_val,
                                                                  int items, int* order) {
-  extern __shared__ unsigned s_rk[];   // [kItemSortMax] keys
+  extern __shared__ unsigned s_rk[];   // [kItemSortMax] keys: every CTA stages all of them
   for (int e = threadIdx.x; e < items; e += blockDim.x) s_rk[e] = run_key[e];
   __syncthreads();
   const int n_runs = (items + kItemRun - 1) / kItemRun;
-  for (int e = threadIdx.x; e < items; e += blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < items; e += gridDim.x * blockDim.x) {
     const int r = e / kItemRun;
     const unsigned k = s_rk[e];
     int rank = e - r * kItemRun;
