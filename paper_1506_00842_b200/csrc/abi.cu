@@ -529,6 +529,7 @@ struct mlt_plan {
   bool factors_ok = false;
   std::vector<int> unit_of;     // table position -> original unit m*kH + j
   int* d_unit_of = nullptr;
+  bool units_sorted = false;    // unit_of in plan_sort_units' order (pruning), else the identity
   std::map<int, BandSetup> setups;
   // Every configuration gets the SAME prediction, bit for bit, in the
   // reference's arithmetic: each hidden unit with a nonzero output weight has
@@ -721,51 +722,12 @@ int get_setup(mlt_plan* p, int split, BandSetup** out) {
   return MLT_OK;
 }
 
-// exp factors of every (unit, parameter, digit): computed once per plan.
-int plan_factors(mlt_plan* p) {
+// F[position][digit] = exp factors of the unit at each table position
+int launch_factors(mlt_plan* p) {
   const HostEns& e = p->he;
   const HostSpace& s = p->hs;
-  p->factors_ok = false;
-  double wmax = 0;
-  for (size_t q = 0; q < (size_t)e.k * e.h * e.d; ++q) wmax = std::max(wmax, std::fabs(e.w1()[q]));
-  if (wmax > 600.0) return MLT_OK;          // a single factor could overflow fp64
-  p->foff[0] = 0;
-  for (int q = 0; q < s.P; ++q) p->foff[q + 1] = p->foff[q] + s.radix[q];
-  const int KH = e.k * kH;
   mlt_ctx* c = p->ctx;
-  // Unit order of every table: decreasing range of the unit's contribution
-  // over the whole space, |w'| * (sigmoid(zmax) - sigmoid(zmin)), so that the
-  // sweep's partial sums settle early (the pruning bounds of the remaining
-  // units are then tight); padding / zero-weight units last.
-  {
-    // (-range, unit) ascending == a stable sort by decreasing range; the
-    // single-valued parameters never move z, so they are skipped up front
-    int act[kMaxP], n_act = 0;
-    for (int q = 0; q < s.P; ++q)
-      if (s.radix[q] >= 2) act[n_act++] = q;
-    std::vector<std::pair<double, int>> key(KH);
-    for (int mj = 0; mj < KH; ++mj) {
-      key[mj] = {1.0, mj};   // padding / zero-weight units: after every real unit
-      const int m = mj / kH, j = mj % kH;
-      if (j >= e.h) continue;
-      const double wp = e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k;
-      if (wp == 0.0) continue;
-      double zmin = e.b1()[(size_t)m * e.h + j], zmax = zmin;
-      const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
-      for (int t = 0; t < n_act; ++t) {
-        zmin += std::min(0.0, w[act[t]]);
-        zmax += std::max(0.0, w[act[t]]);
-      }
-      auto sg = [](double z) { return 1.0 / (1.0 + std::exp(-z)); };
-      key[mj].first = -(std::fabs(wp) * (sg(zmax) - sg(zmin)));
-    }
-    std::sort(key.begin(), key.end());
-    p->unit_of.resize(KH);
-    for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = key[mj].second;
-    CU(cudaMallocAsync(&p->d_unit_of, (size_t)KH * 4, c->stream));
-    TRY(upload_pinned(c, p->d_unit_of, p->unit_of.data(), (size_t)KH * 4));
-  }
-  CU(cudaMallocAsync(&p->d_F, (size_t)KH * p->foff[s.P] * 8, c->stream));
+  const int KH = e.k * kH;
   TableArgs ta;
   std::memset(&ta, 0, sizeof ta);
   ta.k = e.k;
@@ -778,6 +740,74 @@ int plan_factors(mlt_plan* p) {
   ta.F = p->d_F;
   k_table_factors<<<grid_for(c, (int64_t)KH * p->foff[s.P], 256), 256, 0, c->stream>>>(ta);
   TRY(check_launch(c));
+  return MLT_OK;
+}
+
+// Unit order for the pruned sweep: decreasing range of the unit's
+// contribution over the whole space, |w'| * (sigmoid(zmax) - sigmoid(zmin)),
+// so that the sweep's partial sums settle early (the pruning bounds of the
+// remaining units are then tight); padding / zero-weight units last. Done on
+// the first pruned call of a plan: F is rebuilt in the new order and every
+// setup and table derived from the old one is dropped.
+int plan_sort_units(mlt_plan* p) {
+  const HostEns& e = p->he;
+  const HostSpace& s = p->hs;
+  mlt_ctx* c = p->ctx;
+  const int KH = e.k * kH;
+  // (-range, unit) ascending == a stable sort by decreasing range; the
+  // single-valued parameters never move z, so they are skipped up front
+  int act[kMaxP], n_act = 0;
+  for (int q = 0; q < s.P; ++q)
+    if (s.radix[q] >= 2) act[n_act++] = q;
+  std::vector<std::pair<double, int>> key(KH);
+  for (int mj = 0; mj < KH; ++mj) {
+    key[mj] = {1.0, mj};   // padding / zero-weight units: after every real unit
+    const int m = mj / kH, j = mj % kH;
+    if (j >= e.h) continue;
+    const double wp = e.w2()[(size_t)m * e.h + j] * e.sd()[m] / e.k;
+    if (wp == 0.0) continue;
+    double zmin = e.b1()[(size_t)m * e.h + j], zmax = zmin;
+    const double* w = e.w1() + ((size_t)m * e.h + j) * e.d;
+    for (int t = 0; t < n_act; ++t) {
+      zmin += std::min(0.0, w[act[t]]);
+      zmax += std::max(0.0, w[act[t]]);
+    }
+    auto sg = [](double z) { return 1.0 / (1.0 + std::exp(-z)); };
+    key[mj].first = -(std::fabs(wp) * (sg(zmax) - sg(zmin)));
+  }
+  std::sort(key.begin(), key.end());
+  for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = key[mj].second;
+  TRY(upload_pinned(c, p->d_unit_of, p->unit_of.data(), (size_t)KH * 4));
+  TRY(launch_factors(p));
+  for (auto& kv : p->setups) pool_free(c, kv.second.d_tab);
+  p->setups.clear();
+  std::fill(p->t_key, p->t_key + 5, -1);
+  p->units_sorted = true;
+  return MLT_OK;
+}
+
+// exp factors of every (unit, parameter, digit): computed once per plan.
+int plan_factors(mlt_plan* p) {
+  const HostEns& e = p->he;
+  const HostSpace& s = p->hs;
+  p->factors_ok = false;
+  double wmax = 0;
+  for (size_t q = 0; q < (size_t)e.k * e.h * e.d; ++q) wmax = std::max(wmax, std::fabs(e.w1()[q]));
+  if (wmax > 600.0) return MLT_OK;          // a single factor could overflow fp64
+  p->foff[0] = 0;
+  for (int q = 0; q < s.P; ++q) p->foff[q + 1] = p->foff[q] + s.radix[q];
+  const int KH = e.k * kH;
+  mlt_ctx* c = p->ctx;
+  // Table position = unit (m*kH + j) until a pruned sweep asks for the
+  // range order (plan_sort_units): the full sweep's exactness does not depend
+  // on the order, so a fresh plan skips the ordering's host math
+  p->unit_of.resize(KH);
+  for (int mj = 0; mj < KH; ++mj) p->unit_of[mj] = mj;
+  p->units_sorted = false;
+  CU(cudaMallocAsync(&p->d_unit_of, (size_t)KH * 4, c->stream));
+  TRY(upload_pinned(c, p->d_unit_of, p->unit_of.data(), (size_t)KH * 4));
+  CU(cudaMallocAsync(&p->d_F, (size_t)KH * p->foff[s.P] * 8, c->stream));
+  TRY(launch_factors(p));
   p->factors_ok = true;
   return MLT_OK;
 }
@@ -1296,7 +1326,10 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
   if (c->prof) CU(cudaEventRecord(c->ev[0], c->stream));
 
   BandSetup* bs = nullptr;
-  if (!idx_list && m <= kMaxTopM && c->opt_path != 1) TRY(get_setup(p, choose_split(p, n), &bs));
+  if (!idx_list && m <= kMaxTopM && c->opt_path != 1) {
+    if (c->opt_prune == 1 && p->factors_ok && !p->units_sorted) TRY(plan_sort_units(p));
+    TRY(get_setup(p, choose_split(p, n), &bs));
+  }
   bool band = bs && bs->ok && (n >= 4096 || c->opt_path == 0);
   // the sweep stages two exp(-A') tiles of k*30*8 floats plus its candidate
   // slots in shared memory: very large ensembles take the exact path instead
