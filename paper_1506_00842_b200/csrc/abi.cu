@@ -600,6 +600,12 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   double* wpv = cb + KH;
   std::vector<float> u(KH, 1.0f);
   double S = 0, log2dmax = -1e300, log2dmin = 1e300;
+  // log2 of the largest d' = (1 + exp(-zmin)) / |w'| needs log1p(exp(.)) per
+  // unit; first an upper bound with log1p(e^x) <= max(x, 0) + ln 2 (no
+  // transcendental), the exact value only when the bound decides nothing
+  double log2dmax_ub = -1e300;
+  std::vector<std::pair<double, double>> zl;   // (-zmin, log|w'|) per real unit
+  zl.reserve(KH);
   int dummies = 0;
   // the multi-valued parameters, outer ones (q < split) first: single-valued
   // parameters never move z
@@ -646,8 +652,8 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
       wpv[mj] = wp;
       u[mj] = (float)(1.0 / wp);
       S += std::fabs(wp);
-      const double l2max = (std::log1p(std::exp(std::min(-zmin, 700.0))) - lw) / std::log(2.0);
-      log2dmax = std::max(log2dmax, l2max);
+      log2dmax_ub = std::max(log2dmax_ub, (std::max(-zmin, 0.0) + std::log(2.0) - lw) / std::log(2.0));
+      zl.emplace_back(-zmin, lw);
       log2dmin = std::min(log2dmin, -lw / std::log(2.0));
     }
   }
@@ -655,6 +661,12 @@ int band_setup(mlt_plan* p, int split, BandSetup& b) {
   // (MLT_OPT_GROUP, default kDefaultGroup) whose G-fold products of d' stay
   // inside the normal fp32 range and that divides the unit count.
   const int gmax = (p->ctx->opt_group >= 1 && p->ctx->opt_group <= 4) ? p->ctx->opt_group : kDefaultGroup;
+  if (gmax * std::max(log2dmax_ub, 0.0) < 124.0) {
+    log2dmax = log2dmax_ub;   // the bound already admits the largest grouping
+  } else {
+    for (const auto& v : zl)
+      log2dmax = std::max(log2dmax, (std::log1p(std::exp(std::min(v.first, 700.0))) - v.second) / std::log(2.0));
+  }
   int G = 0;
   for (int g = gmax; g >= 1; --g) {
     if (KH % g == 0 && g * std::max(log2dmax, 0.0) < 124.0 && g * std::min(log2dmin, 0.0) > -124.0) {
