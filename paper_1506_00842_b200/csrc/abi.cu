@@ -562,7 +562,7 @@ int choose_split(const mlt_plan* p, int64_t n) {
   int64_t cin = 1;
   for (int sp = s.P - 1; sp >= 0; --sp) {
     cin *= s.radix[sp];
-    if (cin > 16384 || s.P - sp > 16) break;    // k_table_inner handles <= 16 inner params
+    if (cin > 16384 || s.P - sp > 16) break;    // k_table_tiles handles <= 16 inner params
     const int64_t pad = (cin + kInnerBlock - 1) / kInnerBlock * kInnerBlock;
     const double rows = std::ceil((double)n / cin) + 1.0;
     const double waste = (double)n * ((double)pad / cin - 1.0);
@@ -1502,12 +1502,14 @@ static int plan_top_m_impl(mlt_plan* p, int64_t m, int64_t begin, int64_t end, c
       ta.i_nhi = nhi_i;
       ta.f_onlo = make_fdiv(nlo_o);
       ta.f_inlo = make_fdiv(nlo_i);
-      k_table_outer<<<grid_for(c, (int64_t)n_ob * KH * kOB, 256), 256, 0, c->stream>>>(ta);
-      TRY(check_launch(c));
-      void (*tin)(TableArgs) = B.G == 4 ? k_table_inner<4>
-                               : B.G == 3 ? k_table_inner<3> : (B.G == 2 ? k_table_inner<2> : k_table_inner<1>);
-      tin<<<grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads, 256), 256, 0, c->stream>>>(ta);
-      TRY(check_launch(c));
+      {
+        const int nb_outer = grid_for(c, (int64_t)n_ob * KH * kOB, 256);
+        const int nb_inner = grid_for(c, (int64_t)n_ib * (KH / B.G) * kThreads, 256);
+        void (*tiles)(TableArgs, int) = B.G == 4 ? k_table_tiles<4>
+                                        : B.G == 3 ? k_table_tiles<3> : (B.G == 2 ? k_table_tiles<2> : k_table_tiles<1>);
+        tiles<<<nb_outer + nb_inner, 256, 0, c->stream>>>(ta, nb_outer);
+        TRY(check_launch(c));
+      }
       if (prune) {
         double* ext;
         TRY(ws_t(c, S_SORT_TMP, (size_t)KH * n_ib, &ext));

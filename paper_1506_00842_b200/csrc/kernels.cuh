@@ -186,7 +186,6 @@ struct PartialJobs {             // k_table_partial4: four (parameter range, sub
   double* out[4];
 };
 __global__ void k_table_partial4(const __grid_constant__ TableArgs t, const __grid_constant__ PartialJobs j);
-__global__ void k_table_outer(TableArgs t);
 struct CkList {
   int n;
   int unit[kMaxCk];             // first table position still to come at checkpoint c
@@ -200,7 +199,7 @@ __global__ void k_item_runs(const float* remlo, int n_ck, int n_ib, int items, u
 __global__ void k_item_merge(const unsigned* run_key, const int* run_val, int items, int* order);
 __global__ void k_table_rem(TableArgs t, CkList ck, const double* ext, float* remlo);
 template <int G>
-__global__ void k_table_inner(TableArgs t);
+__global__ void k_table_tiles(TableArgs t, int nb_outer);   // outer + inner tables, one launch
 
 template <int G, bool PRUNE, int SB, int NT, int OBU>
 __global__ void k_sweep(SweepArgs a);

@@ -96,10 +96,10 @@ __global__ void k_table_partial4(const __grid_constant__ TableArgs t, const __gr
 // was slower, 22 -> 40 us on the 10^8 space, its loads stride over positions).
 // Row o = o_lo + ob*kOB + r = (o / nlo) * nlo + o % nlo over the outer split.
 template <typename I>   // index type: uint32_t when every index of the build fits (TableArgs::idx32)
-__device__ __forceinline__ void table_outer(const TableArgs& t) {
+__device__ __forceinline__ void table_outer(const TableArgs& t, int bid, int nblk) {
   const int KH = t.k * kH;
-  const I total = (I)t.n_ob * KH * kOB, stride = (I)gridDim.x * blockDim.x;
-  for (I q = (I)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
+  const I total = (I)t.n_ob * KH * kOB, stride = (I)nblk * blockDim.x;
+  for (I q = (I)bid * blockDim.x + threadIdx.x; q < total; q += stride) {
     const int r = (int)(q % kOB);
     const I q8 = q / kOB, ob = (I)fdiv((int64_t)q8, t.f_kh);
     const int mj = (int)(q8 - ob * KH);
@@ -112,12 +112,6 @@ __device__ __forceinline__ void table_outer(const TableArgs& t) {
     }
     t.ea[q] = out;
   }
-}
-__global__ void k_table_outer(TableArgs t) {
-  if (t.idx32)
-    table_outer<uint32_t>(t);
-  else
-    table_outer<int64_t>(t);
 }
 
 // Extremes of the inner part per (table position, inner block): over the
@@ -395,11 +389,11 @@ __global__ void __launch_bounds__(kRemChunk) k_table_rem(TableArgs t, CkList ck,
 // computes its 4*ebw slots and writes them as float4s -- consecutive threads
 // write consecutive 16-byte chunks and read consecutive PiL entries.
 template <int G, typename I>
-__device__ __forceinline__ void table_inner(const TableArgs& t) {
+__device__ __forceinline__ void table_inner(const TableArgs& t, int bid, int nblk) {
   constexpr int W = ebw_of(G), WF = 4 * W;
   const int ngroups = t.k * kH / G;
-  const I total = (I)(t.c_in_pad / kInnerBlock) * ngroups * kThreads, stride = (I)gridDim.x * blockDim.x;
-  for (I q = (I)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
+  const I total = (I)(t.c_in_pad / kInnerBlock) * ngroups * kThreads, stride = (I)nblk * blockDim.x;
+  for (I q = (I)bid * blockDim.x + threadIdx.x; q < total; q += stride) {
     const int th = (int)(q % kThreads);
     const I rest = q / kThreads;
     const I ib = (I)fdiv((int64_t)rest, t.f_ngroups);
@@ -429,12 +423,23 @@ __device__ __forceinline__ void table_inner(const TableArgs& t) {
     for (int w = 0; w < W; ++w) dst[w] = make_float4(out[4 * w], out[4 * w + 1], out[4 * w + 2], out[4 * w + 3]);
   }
 }
+// Both sweep tables in ONE launch: blocks [0, nb_outer) build the outer
+// table, the rest the inner one -- the two are independent and each is
+// latency-bound, so they overlap instead of running back to back.
 template <int G>
-__global__ void k_table_inner(TableArgs t) {
-  if (t.idx32)
-    table_inner<G, uint32_t>(t);
-  else
-    table_inner<G, int64_t>(t);
+__global__ void k_table_tiles(TableArgs t, int nb_outer) {
+  const int b = blockIdx.x;
+  if (b < nb_outer) {
+    if (t.idx32)
+      table_outer<uint32_t>(t, b, nb_outer);
+    else
+      table_outer<int64_t>(t, b, nb_outer);
+  } else {
+    if (t.idx32)
+      table_inner<G, uint32_t>(t, b - nb_outer, (int)gridDim.x - nb_outer);
+    else
+      table_inner<G, int64_t>(t, b - nb_outer, (int)gridDim.x - nb_outer);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -507,7 +512,7 @@ __device__ __forceinline__ void combine<4>(const f2 (&d)[4], f2& num, f2& den) {
 }
 
 // Per-thread factors of one group of G units: exp(-B')/w' of the thread's
-// two inners for each unit, stored thread-contiguously (k_table_inner layout,
+// two inners for each unit, stored thread-contiguously (k_table_tiles layout,
 // slot x*kInner + s) so that unit x's pair (inner 0, inner 1) is one aligned
 // 64-bit register pair (1/w' comes from the parameter block, see group_step).
 static_assert(kInner == 2, "the sweep packs the thread's two inners into one f32x2 register");
@@ -998,10 +1003,10 @@ __global__ void __launch_bounds__(NT, MLT_MINB * (kThreads / NT)) k_sweep(SweepA
   }
 }
 
-template __global__ void k_table_inner<1>(TableArgs t);
-template __global__ void k_table_inner<2>(TableArgs t);
-template __global__ void k_table_inner<3>(TableArgs t);
-template __global__ void k_table_inner<4>(TableArgs t);
+template __global__ void k_table_tiles<1>(TableArgs t, int nb_outer);
+template __global__ void k_table_tiles<2>(TableArgs t, int nb_outer);
+template __global__ void k_table_tiles<3>(TableArgs t, int nb_outer);
+template __global__ void k_table_tiles<4>(TableArgs t, int nb_outer);
 // every G of the host's dispatch table (abi.cu) for each instance shape
 // (MLT_SWEEP_INSPECT: only the default full-sweep instance, for SASS inspection)
 #ifdef MLT_SWEEP_INSPECT
